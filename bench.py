@@ -1,0 +1,331 @@
+#!/usr/bin/env python
+"""bench.py — the compressed aggregate + update step of arXiv 2105.07829 on B200.
+
+One step = one pass of the whole hot path over one
+synthetic gradient per rank: bpc_compress (worker EF + compression) ->
+bpc_aggregate (all-to-all of payloads over NCCL/NVLink, server
+decompress-sum-recompress, all-gather) -> bpc_step (fused decode + Adam).
+
+Metric (BASELINE.json): gradient GB/s = (ranks x 4 bytes x d) / step time,
+d = the model's parameter count; whole-job aggregate over all ranks.
+
+Launch: python bench.py [--config C2] [--steps K] [--warmup W]
+        torchrun --nproc-per-node N bench.py --gpus N ...
+        python bench.py --impl reference   (the CPU oracle, timed on host cores)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "compressed aggregate+update step: gradient GB/s per step at 1/2/4/8 B200, % roofline"
+DESCR = {
+    "C1": "d=4096 synthetic gradient, onebit scaled-sign + EF (configs[0])",
+    "C2": "ResNet-50-shaped gradient (25.6M params, 161 tensors), onebit two-way + EF + Adam (configs[1])",
+    "C3": "VGG16-shaped gradient (138M params), top-k 0.1% + EF + Adam (configs[2])",
+    "C4": "BERT-base-shaped gradient (110M params), linear dithering 7 bits (Alg. 3) + Adam (configs[3])",
+    "C5": "BERT-large-shaped gradient (336M params), onebit two-way + EF + Adam (configs[4])",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------- clocks
+class Clocks:
+    """nvidia-smi sampler running around the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "50", "-i", str(index)], stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.f.name)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- byte models
+def kernel_bytes(chunks, comp, n, rank):
+    """Algorithmic HBM bytes per launch of each kernel."""
+    ef = comp.use_ef
+    w = s = u = 0
+    for c in chunks:
+        L, pb = c.len, c.payload_bytes
+        if c.raw:
+            w += 8 * L
+            if c.owner == rank:
+                s += 4 * n * L + 4 * L
+            u += 24 * L + 4 * L
+        else:
+            w += (12 if ef else 4) * L + pb
+            if c.owner == rank:
+                s += n * pb + (8 * L if ef else 0) + pb
+            u += 24 * L + pb
+    return {"compress": w, "server": s, "update": u}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------- CPU oracle leg
+def oracle_sample(wcfg, n, seconds):
+    """Time the oracle as it stands (single host core) on a bounded sample of the
+    workload: whole rounds of the full config at n simulated workers, repeated
+    until `seconds` of CPU work; returns gradient GB/s (n x 4d / s)."""
+    import numpy as np
+
+    import oracle
+    from workloads import gen_grad, gen_params, layout
+    oracle.build()
+    numels = wcfg.tensor_numels()
+    offs, D = layout(numels)
+    d = sum(numels)
+    cfg = oracle.Cfg.from_workload(wcfg, n=n)
+    st = oracle.State(n, D, gen_params(wcfg))
+    grads = [np.stack([gen_grad(wcfg, i, s) for i in range(n)]) for s in (1, 2)]
+    steps, busy = 0, 0.0
+    while busy < seconds or steps == 0:
+        t0 = time.perf_counter()
+        oracle.round_(cfg, st, grads[steps % 2], wcfg.lr, want_payloads=False)
+        busy += time.perf_counter() - t0
+        steps += 1
+    return n * 4 * d * steps / busy / 1e9, steps, busy
+
+
+def run_reference(args):
+    world, rank, local = dist_env()
+    if rank != 0:
+        return
+    from workloads import config
+    w = config(args.config, n=args.gpus)
+    d = sum(w.tensor_numels())
+    # each "step" is one full oracle round of the workload (n = --gpus workers simulated)
+    val, steps, busy = oracle_sample(w, args.gpus, max(1.0, min(args.cpu_seconds, 20.0)))
+    ms = busy / steps * 1e3
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(val, 6), "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": steps, "warmup": 0, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {DESCR[args.config]}", "ranks_simulated": args.gpus, "d": d},
+        "cpu_baseline": {"value": round(val, 6), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                         "sample": f"{steps} full oracle rounds of {args.config} with {args.gpus} simulated workers"},
+        "e2e": {"value": round(val, 6), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    if world != args.gpus and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2105_07829_b200 import build as bbuild
+    if rank == 0 and not os.path.exists(bbuild.LIB):
+        bbuild.build()
+    if world > 1:
+        dist.barrier()
+    import paper_2105_07829_b200 as bpc
+    from workloads import config, gen_grad_torch, gen_params, layout
+
+    w = config(args.config, n=world)
+    numels = w.tensor_numels()
+    offs, D = layout(numels)
+    d = sum(numels)
+    nid = None
+    if world > 1:
+        obj = [bpc.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nid = obj[0]
+    stream = torch.cuda.current_stream(dev)
+    ctx = bpc.context_for(w, rank=rank, world_size=world, device=local, stream=stream.cuda_stream, nccl_id=nid)
+    chunks = ctx.chunks()
+    grads = [gen_grad_torch(w, rank, s, dev) for s in (1, 2)]
+    x = torch.tensor(gen_params(w), device=dev)
+    torch.cuda.synchronize()
+
+    def step(i):
+        ctx.compress(grads[i % 2])
+        ctx.aggregate()
+        ctx.step(x, w.lr)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    clocks = Clocks(local)
+    for i in range(args.warmup):
+        step(i)
+    launches0 = ctx.launch_count()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.steps):
+        step(i)
+    e1.record(stream)
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    launches = ctx.launch_count() - launches0
+    clk = clocks.stop()
+    ctx.sync()
+
+    # per-kernel device timing (events recorded by libbpc around each launch, same stream)
+    ctx.set_timing(True)
+    for i in range(args.steps):
+        step(i)
+    barrier()
+    tim = ctx.timing()
+    ctx.set_timing(False)
+    kb = kernel_bytes(chunks, w.comp, world, rank)
+    per = {k: (tim[k][0] / max(1, tim[k][1]), tim[k][1]) for k in ("compress", "server", "update", "push", "pull")}
+    dom = max(("compress", "server", "update"), key=lambda k: per[k][0])
+    peak, peak_src = peaks()
+    achieved = kb[dom] / (per[dom][0] * 1e-3) / 1e9
+    kern = {k: {"ms": round(per[k][0], 5), "GB/s": round(kb[k] / max(per[k][0], 1e-9) / 1e6, 1) if k in kb else None,
+                "alg_bytes": kb.get(k)} for k in per if per[k][1]}
+
+    # end to end through the public API: pinned host gradient -> device, step, params -> host
+    e2e = None
+    if not args.no_e2e:
+        hg = [grads[s].cpu().pin_memory() for s in (0, 1)]
+        hx = torch.empty(x.shape, dtype=torch.float32).pin_memory()
+        dg = torch.empty_like(grads[0])
+        for i in range(2):
+            dg.copy_(hg[i % 2], non_blocking=True)
+            ctx.compress(dg)
+            ctx.aggregate()
+            ctx.step(x, w.lr)
+            hx.copy_(x, non_blocking=True)
+        barrier()
+        k2 = max(2, min(args.steps, 50))
+        e0.record(stream)
+        for i in range(k2):
+            dg.copy_(hg[i % 2], non_blocking=True)
+            ctx.compress(dg)
+            ctx.aggregate()
+            ctx.step(x, w.lr)
+            hx.copy_(x, non_blocking=True)
+        e1.record(stream)
+        barrier()
+        ms_e2e = max_over_ranks(e0.elapsed_time(e1) / k2)
+        e2e = {"value": round(world * 4 * d / (ms_e2e * 1e-3) / 1e9, 3), "unit": "GB/s",
+               "h2d_bytes_per_step": 4 * D, "d2h_bytes_per_step": 4 * D, "ms_per_step": round(ms_e2e, 4)}
+    ctx.sync()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        val, steps, busy = oracle_sample(w, 1, args.cpu_seconds)
+        cpu = {"value": round(val, 6), "unit": "GB/s", "cores": 1, "kind": "oracle",
+               "sample": f"{steps} full oracle rounds of {args.config} (n=1), {busy:.1f} s on 1 host core"}
+
+    if rank == 0:
+        s = ctx.summary()
+        line = {
+            "metric": METRIC, "value": round(world * 4 * d / (ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 5),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": f"{args.config}: {DESCR[args.config]}", "d": d, "tensors": len(numels),
+                       "chunks": s.num_chunks, "compressed_chunks": s.num_compressed,
+                       "payload_bytes_per_rank": s.payload_total,
+                       "compression_rate_vs_fp32": round(4 * d / s.payload_total, 2),
+                       "l2": "inputs larger than L2 (g, e, m, v, x = %.0f MB per rank)" % (20 * D / 1e6),
+                       "parallelism": f"dp{world} (sharded server: all-to-all + all-gather)"},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                         "peak_source": peak_src, "alg_bytes_per_launch": kb[dom]},
+            "kernels": kern,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.finalize()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

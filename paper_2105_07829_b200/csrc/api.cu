@@ -1,0 +1,700 @@
+// api.cu — the libbpc C ABI (include/bpc.h): validation, chunk plan, owner map,
+// buffers, the NCCL exchange and the kernel launches of one step.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "bpc.h"
+#include "kernels.h"
+
+namespace {
+using namespace bpc;
+
+constexpr uint64_t kSlice = 16384;   // == SLICE of the kernels
+
+uint64_t round_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+struct PlanChunk {
+  bpc_chunk_info info;
+};
+
+struct Plan {
+  std::vector<bpc_chunk_info> chunks;
+  uint32_t cs = 16;
+  uint64_t D = 0;
+  std::vector<uint64_t> seg_off, seg_bytes;   // per peer segment of SEND / P
+  uint64_t send_bytes = 0, etl_elems = 0, payload_total = 0;
+  uint32_t num_compressed = 0, num_owned = 0;
+};
+
+// k = max(1, floor(L * num / den))  (R8)
+uint64_t sparse_k(const bpc_compressor& c, uint64_t L) {
+  const uint64_t k = (L * (uint64_t)c.k_num) / (uint64_t)c.k_den;
+  return k < 1 ? 1 : k;
+}
+
+// closed-form payload sizes
+uint64_t payload_size(const bpc_compressor& c, bool raw, uint64_t L) {
+  if (raw || c.kind == BPC_NONE) return 4 * L;
+  switch (c.kind) {
+    case BPC_SCALED_SIGN: return 4 + (L + 7) / 8;
+    case BPC_TOP_K:
+    case BPC_RANDOM_K: return 8 + 8 * sparse_k(c, L);
+    case BPC_LINEAR_DITHER:
+    case BPC_NATURAL_DITHER: return 4 + ((uint64_t)c.bits * L + 7) / 8;
+  }
+  return 0;
+}
+
+bpc_status make_plan(const bpc_config* cfg, Plan* P, std::string* err) {
+  auto fail = [&](bpc_status s, const char* msg) {
+    *err = msg;
+    return s;
+  };
+  if (!cfg) return fail(BPC_ERR_INVALID_ARGUMENT, "cfg is NULL");
+  if (cfg->world_size < 1 || cfg->rank < 0 || cfg->rank >= cfg->world_size)
+    return fail(BPC_ERR_INVALID_ARGUMENT, "bad world_size / rank");
+  if (cfg->num_tensors < 1 || !cfg->tensor_numel || !cfg->tensor_offset)
+    return fail(BPC_ERR_INVALID_ARGUMENT, "no tensors");
+  const bpc_compressor& C = cfg->comp;
+  switch (C.kind) {
+    case BPC_NONE: case BPC_SCALED_SIGN: break;
+    case BPC_TOP_K: case BPC_RANDOM_K:
+      if (C.k_num < 1 || C.k_den < 1) return fail(BPC_ERR_INVALID_ARGUMENT, "k_num/k_den must be >= 1");
+      if (C.k_num > C.k_den) return fail(BPC_ERR_K_TOO_LARGE, "k fraction > 1");
+      break;
+    case BPC_LINEAR_DITHER: case BPC_NATURAL_DITHER:
+      if (C.bits < 2 || C.bits > 8) return fail(BPC_ERR_INVALID_ARGUMENT, "dither bits must be 2..8");
+      break;
+    default: return fail(BPC_ERR_UNSUPPORTED_KIND, "unknown compressor kind");
+  }
+  if (!(cfg->beta1 > 0.f && cfg->beta1 < 1.f && cfg->beta2 > 0.f && cfg->beta2 < 1.f))
+    return fail(BPC_ERR_INVALID_ARGUMENT, "betas must lie in (0, 1)");
+  if (!(cfg->eps >= 0.f) || !(cfg->weight_decay >= 0.f))
+    return fail(BPC_ERR_INVALID_ARGUMENT, "eps and weight_decay must be >= 0");
+  uint64_t ce = cfg->chunk_elems ? cfg->chunk_elems : (1ull << 18);
+  if (ce < kSlice || ce > 16 * kSlice || (ce & (ce - 1)))
+    return fail(BPC_ERR_INVALID_ARGUMENT, "chunk_elems must be a power of two in [2^14, 2^18]");
+  P->cs = (uint32_t)(ce / kSlice);
+  // tensors: numel >= 1, offsets 16-byte aligned, disjoint
+  std::vector<std::pair<uint64_t, uint64_t>> iv;
+  P->D = 0;
+  for (uint32_t t = 0; t < cfg->num_tensors; t++) {
+    const uint64_t L = cfg->tensor_numel[t], o = cfg->tensor_offset[t];
+    if (L == 0) return fail(BPC_ERR_EMPTY_BLOCK, "tensor with numel 0");
+    if (L >= (1ull << 31)) return fail(BPC_ERR_INVALID_ARGUMENT, "tensor numel >= 2^31");
+    if (o % 4) return fail(BPC_ERR_INVALID_ARGUMENT, "tensor offsets must be multiples of 4 elements");
+    iv.push_back({o, o + L});
+    P->D = std::max(P->D, o + L);
+  }
+  std::sort(iv.begin(), iv.end());
+  for (size_t i = 1; i < iv.size(); i++)
+    if (iv[i].first < iv[i - 1].second) return fail(BPC_ERR_SIZE_MISMATCH, "tensors overlap");
+  // chunk plan: raw below threshold (R3), else units of chunk_elems (R1)
+  P->chunks.clear();
+  P->num_compressed = 0;
+  for (uint32_t t = 0; t < cfg->num_tensors; t++) {
+    const uint64_t L = cfg->tensor_numel[t];
+    const bool raw = (4 * L < cfg->size_threshold_bytes) || C.kind == BPC_NONE;
+    const uint64_t unit = raw ? L : ce;
+    for (uint64_t s = 0; s < L; s += unit) {
+      bpc_chunk_info ci = {};
+      ci.tensor = t;
+      ci.raw = raw;
+      ci.offset = cfg->tensor_offset[t] + s;
+      ci.len = std::min(unit, L - s);
+      ci.k = (!raw && (C.kind == BPC_TOP_K || C.kind == BPC_RANDOM_K)) ? (uint32_t)sparse_k(C, ci.len) : 0;
+      ci.payload_bytes = payload_size(C, raw, ci.len);
+      P->chunks.push_back(ci);
+      if (!raw) P->num_compressed++;
+    }
+  }
+  // owner map: LPT (largest first) over the server cost model
+  const uint32_t n = (uint32_t)cfg->world_size;
+  std::vector<std::pair<uint64_t, uint32_t>> cost;
+  for (uint32_t c = 0; c < P->chunks.size(); c++) {
+    const auto& ci = P->chunks[c];
+    const uint64_t pb = ci.payload_bytes;
+    const uint64_t w = ci.raw ? (4 * n * ci.len + 4 * ci.len) : (n * pb + 8 * ci.len * (C.use_ef ? 1 : 0) + pb);
+    cost.push_back({w, c});
+  }
+  std::sort(cost.begin(), cost.end(), [](auto a, auto b) {
+    return a.first != b.first ? a.first > b.first : a.second < b.second;
+  });
+  std::vector<uint64_t> load(n, 0);
+  for (auto& wc : cost) {
+    uint32_t best = 0;
+    for (uint32_t r = 1; r < n; r++)
+      if (load[r] < load[best]) best = r;
+    load[best] += wc.first;
+    P->chunks[wc.second].owner = best;
+  }
+  // payload layout grouped by owner, 16-byte slots with >= 4 spare bytes
+  P->seg_off.assign(n, 0);
+  P->seg_bytes.assign(n, 0);
+  P->payload_total = 0;
+  uint64_t off = 0;
+  for (uint32_t r = 0; r < n; r++) {
+    P->seg_off[r] = off;
+    for (auto& ci : P->chunks) {
+      if (ci.owner != r) continue;
+      ci.payload_offset = off;
+      ci.recv_offset = off - P->seg_off[r];
+      off += round_up(ci.payload_bytes + 4, 16);
+      P->payload_total += ci.payload_bytes;
+    }
+    P->seg_bytes[r] = off - P->seg_off[r];
+  }
+  P->send_bytes = off;
+  // compact server error for the owned compressed chunks
+  P->etl_elems = 0;
+  P->num_owned = 0;
+  for (auto& ci : P->chunks) {
+    if (ci.owner != (uint32_t)cfg->rank) continue;
+    P->num_owned++;
+    if (!ci.raw && C.use_ef) {
+      ci.server_err_offset = P->etl_elems;
+      P->etl_elems += round_up(ci.len, 4);
+    }
+  }
+  return BPC_OK;
+}
+
+void fill_summary(const Plan& P, int rank, bpc_plan_summary* s) {
+  s->num_chunks = (uint32_t)P.chunks.size();
+  s->num_compressed = P.num_compressed;
+  s->num_owned = P.num_owned;
+  s->cluster_ctas = P.cs;
+  s->flat_elems = P.D;
+  s->send_bytes = P.send_bytes;
+  s->recv_slot_bytes = P.seg_bytes[rank];
+  s->server_err_elems = P.etl_elems;
+  s->payload_total = P.payload_total;
+}
+
+}  // namespace
+
+struct bpc_ctx {
+  bpc_config cfg;
+  std::vector<uint64_t> numel, offset;
+  Plan plan;
+  cudaStream_t stream = nullptr;
+  float *e = nullptr, *etl = nullptr, *m = nullptr, *v = nullptr;
+  uint8_t *send = nullptr, *recv = nullptr, *pbuf = nullptr;
+  uint64_t recv_bytes = 0;
+  DevChunk* d_chunks = nullptr;
+  uint32_t *d_witems = nullptr, *d_sitems = nullptr;
+  Tile *d_wraw = nullptr, *d_sraw = nullptr, *d_utiles = nullptr;
+  uint32_t n_witems = 0, n_sitems = 0, n_wraw = 0, n_sraw = 0, n_utiles = 0;
+  unsigned int* d_flag = nullptr;
+  ncclComm_t comm = nullptr;
+  uint32_t t = 1;
+  int phase = 0;   // 0 compress, 1 push, 2 server, 3 pull, 4 step
+  bool timing = false;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> events;
+  uint64_t launches = 0;
+  std::string err;
+};
+
+namespace {
+
+bpc_status cuda_fail(bpc_ctx* c, cudaError_t e, const char* what) {
+  if (c) c->err = std::string(what) + ": " + cudaGetErrorString(e);
+  return e == cudaErrorMemoryAllocation ? BPC_ERR_OUT_OF_MEMORY : BPC_ERR_CUDA;
+}
+#define CK(call, what)                                 \
+  do {                                                 \
+    cudaError_t _e = (call);                           \
+    if (_e != cudaSuccess) return cuda_fail(ctx, _e, what); \
+  } while (0)
+#define NK(call, what)                                              \
+  do {                                                              \
+    ncclResult_t _r = (call);                                       \
+    if (_r != ncclSuccess) {                                        \
+      ctx->err = std::string(what) + ": " + ncclGetErrorString(_r); \
+      return BPC_ERR_NCCL;                                          \
+    }                                                               \
+  } while (0)
+
+void timer_begin(bpc_ctx* ctx, int id, cudaEvent_t* ev) {
+  if (!ctx->timing) return;
+  cudaEventCreate(ev);
+  cudaEventRecord(*ev, ctx->stream);
+  (void)id;
+}
+void timer_end(bpc_ctx* ctx, int id, cudaEvent_t b) {
+  if (!ctx->timing) return;
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  cudaEventRecord(e, ctx->stream);
+  ctx->events.push_back({id, {b, e}});
+}
+
+template <class T>
+bpc_status upload(bpc_ctx* ctx, T** dst, const std::vector<T>& src) {
+  if (src.empty()) return BPC_OK;
+  CK(cudaMalloc((void**)dst, sizeof(T) * src.size()), "cudaMalloc table");
+  CK(cudaMemcpy(*dst, src.data(), sizeof(T) * src.size(), cudaMemcpyHostToDevice), "upload table");
+  return BPC_OK;
+}
+
+void free_ctx(bpc_ctx* ctx) {
+  if (!ctx) return;
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  for (void* p : {(void*)ctx->e, (void*)ctx->etl, (void*)ctx->m, (void*)ctx->v, (void*)ctx->send,
+                  (void*)ctx->pbuf, (void*)ctx->d_chunks, (void*)ctx->d_witems, (void*)ctx->d_sitems,
+                  (void*)ctx->d_wraw, (void*)ctx->d_sraw, (void*)ctx->d_utiles, (void*)ctx->d_flag})
+    if (p) cudaFree(p);
+  if (ctx->recv && ctx->recv != ctx->send) cudaFree(ctx->recv);
+  for (auto& ev : ctx->events) {
+    cudaEventDestroy(ev.second.first);
+    cudaEventDestroy(ev.second.second);
+  }
+  delete ctx;
+}
+
+CompressParams base_params(bpc_ctx* ctx) {
+  CompressParams p = {};
+  p.chunks = ctx->d_chunks;
+  p.cs = ctx->plan.cs;
+  p.n = (uint32_t)ctx->cfg.world_size;
+  p.inv_n = 1.0 / (double)ctx->cfg.world_size;
+  p.t = ctx->t;
+  p.rank = (uint32_t)ctx->cfg.rank;
+  p.seed = ctx->cfg.seed;
+  p.bits = ctx->cfg.comp.bits;
+  p.randk_scaled = ctx->cfg.comp.randk_scaled;
+  p.use_ef = ctx->cfg.comp.use_ef;
+  p.check_finite = ctx->cfg.check_finite;
+  p.flag = ctx->d_flag;
+  return p;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* bpc_status_string(bpc_status s) {
+  switch (s) {
+    case BPC_OK: return "ok";
+    case BPC_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case BPC_ERR_SIZE_MISMATCH: return "size mismatch";
+    case BPC_ERR_EMPTY_BLOCK: return "empty block";
+    case BPC_ERR_K_TOO_LARGE: return "k too large";
+    case BPC_ERR_UNSUPPORTED_KIND: return "unsupported compressor kind";
+    case BPC_ERR_BAD_STATE: return "bad state (call order / mode)";
+    case BPC_ERR_NONFINITE: return "non-finite gradient";
+    case BPC_ERR_CUDA: return "CUDA error";
+    case BPC_ERR_NCCL: return "NCCL error";
+    case BPC_ERR_OUT_OF_MEMORY: return "out of device memory";
+  }
+  return "unknown status";
+}
+
+const char* bpc_last_error(const bpc_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
+
+bpc_status bpc_get_unique_id(uint8_t out[128]) {
+  if (!out) return BPC_ERR_INVALID_ARGUMENT;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return BPC_ERR_NCCL;
+  static_assert(sizeof(id) == 128, "NCCL unique id size");
+  memcpy(out, &id, 128);
+  return BPC_OK;
+}
+
+bpc_status bpc_plan(const bpc_config* cfg, bpc_plan_summary* summary, bpc_chunk_info* infos, uint32_t cap) {
+  Plan P;
+  std::string err;
+  const bpc_status s = make_plan(cfg, &P, &err);
+  if (s != BPC_OK) return s;
+  if (summary) fill_summary(P, cfg->rank, summary);
+  if (infos)
+    for (uint32_t i = 0; i < cap && i < P.chunks.size(); i++) infos[i] = P.chunks[i];
+  return BPC_OK;
+}
+
+bpc_status bpc_init(const bpc_config* cfg, bpc_ctx** out) {
+  if (!out) return BPC_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  bpc_ctx* ctx = new bpc_ctx();
+  std::string err;
+  bpc_status s = make_plan(cfg, &ctx->plan, &err);
+  if (s != BPC_OK) {
+    delete ctx;
+    return s;
+  }
+  ctx->cfg = *cfg;
+  ctx->numel.assign(cfg->tensor_numel, cfg->tensor_numel + cfg->num_tensors);
+  ctx->offset.assign(cfg->tensor_offset, cfg->tensor_offset + cfg->num_tensors);
+  ctx->cfg.tensor_numel = ctx->numel.data();
+  ctx->cfg.tensor_offset = ctx->offset.data();
+  ctx->cfg.nccl_unique_id = nullptr;
+  ctx->stream = (cudaStream_t)cfg->cuda_stream;
+  auto bail = [&](bpc_status st) {
+    free_ctx(ctx);
+    return st;
+  };
+  // device: must be sm_100 (no CPU fallback)
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || cfg->device < 0 || cfg->device >= ndev) return bail(BPC_ERR_CUDA);
+  if (cudaSetDevice(cfg->device) != cudaSuccess) return bail(BPC_ERR_CUDA);
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, cfg->device) != cudaSuccess || prop.major != 10) return bail(BPC_ERR_CUDA);
+  const Plan& P = ctx->plan;
+  const uint32_t n = (uint32_t)cfg->world_size;
+  const uint32_t rank = (uint32_t)cfg->rank;
+  const uint64_t D = round_up(P.D, 4);
+  auto alloc = [&](void** p, uint64_t bytes) -> cudaError_t {
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e == cudaSuccess) e = cudaMemset(*p, 0, bytes);
+    return e;
+  };
+  cudaError_t ce;
+  if ((ce = alloc((void**)&ctx->e, 4 * D)) != cudaSuccess) return bail(cuda_fail(ctx, ce, "alloc e"));
+  if ((ce = alloc((void**)&ctx->etl, 4 * P.etl_elems)) != cudaSuccess) return bail(cuda_fail(ctx, ce, "alloc e~"));
+  if ((ce = alloc((void**)&ctx->m, 4 * D)) != cudaSuccess) return bail(cuda_fail(ctx, ce, "alloc m"));
+  if ((ce = alloc((void**)&ctx->v, 4 * D)) != cudaSuccess) return bail(cuda_fail(ctx, ce, "alloc v"));
+  if ((ce = alloc((void**)&ctx->send, P.send_bytes)) != cudaSuccess) return bail(cuda_fail(ctx, ce, "alloc send"));
+  if ((ce = alloc((void**)&ctx->pbuf, P.send_bytes)) != cudaSuccess) return bail(cuda_fail(ctx, ce, "alloc p"));
+  if (n == 1) {
+    ctx->recv = ctx->send;   // the worker's payloads are the server's input
+    ctx->recv_bytes = P.send_bytes;
+  } else {
+    ctx->recv_bytes = n * P.seg_bytes[rank];
+    if ((ce = alloc((void**)&ctx->recv, ctx->recv_bytes)) != cudaSuccess) return bail(cuda_fail(ctx, ce, "alloc recv"));
+  }
+  if ((ce = alloc((void**)&ctx->d_flag, 4)) != cudaSuccess) return bail(cuda_fail(ctx, ce, "alloc flag"));
+  // device tables
+  std::vector<DevChunk> dch(P.chunks.size());
+  std::vector<uint32_t> witems, sitems;
+  std::vector<Tile> wraw, sraw, utiles;
+  for (uint32_t c = 0; c < P.chunks.size(); c++) {
+    const auto& ci = P.chunks[c];
+    DevChunk& d = dch[c];
+    d.off = ci.offset;
+    d.pay = ci.payload_offset;
+    d.recv = ci.recv_offset;
+    d.etl = ci.server_err_offset;
+    d.len = (uint32_t)ci.len;
+    d.k = ci.k;
+    d.id = c;
+    d.raw = ci.raw ? 1 : 0;
+    const bool mine = ci.owner == rank;
+    if (!ci.raw) {
+      witems.push_back(c);
+      if (mine) sitems.push_back(c);
+    } else {
+      for (uint64_t s0 = 0; s0 < ci.len; s0 += kSlice) {
+        Tile tl = {c, (uint32_t)s0, (uint32_t)std::min<uint64_t>(kSlice, ci.len - s0), 0};
+        wraw.push_back(tl);
+        if (mine) sraw.push_back(tl);
+      }
+    }
+    for (uint64_t s0 = 0; s0 < ci.len; s0 += 4096) {
+      Tile tl = {c, (uint32_t)s0, (uint32_t)std::min<uint64_t>(4096, ci.len - s0), 0};
+      utiles.push_back(tl);
+    }
+  }
+  if ((s = upload(ctx, &ctx->d_chunks, dch)) != BPC_OK) return bail(s);
+  if ((s = upload(ctx, &ctx->d_witems, witems)) != BPC_OK) return bail(s);
+  if ((s = upload(ctx, &ctx->d_sitems, sitems)) != BPC_OK) return bail(s);
+  if ((s = upload(ctx, &ctx->d_wraw, wraw)) != BPC_OK) return bail(s);
+  if ((s = upload(ctx, &ctx->d_sraw, sraw)) != BPC_OK) return bail(s);
+  if ((s = upload(ctx, &ctx->d_utiles, utiles)) != BPC_OK) return bail(s);
+  ctx->n_witems = (uint32_t)witems.size();
+  ctx->n_sitems = (uint32_t)sitems.size();
+  ctx->n_wraw = (uint32_t)wraw.size();
+  ctx->n_sraw = (uint32_t)sraw.size();
+  ctx->n_utiles = (uint32_t)utiles.size();
+  // the cluster shape must be schedulable
+  int maxc = 0;
+  ce = compress_max_active_clusters(cfg->comp.kind, false, P.cs, &maxc);
+  if (ce != cudaSuccess || maxc < 1) {
+    ctx->err = "cluster of " + std::to_string(P.cs) + " CTAs is not schedulable";
+    return bail(BPC_ERR_CUDA);
+  }
+  if ((ce = cudaDeviceSynchronize()) != cudaSuccess) return bail(cuda_fail(ctx, ce, "init sync"));
+  // NCCL communicator (collective over all ranks)
+  if (cfg->nccl_unique_id && n > 1) {
+    ncclUniqueId id;
+    memcpy(&id, cfg->nccl_unique_id, 128);
+    ncclResult_t r = ncclCommInitRank(&ctx->comm, (int)n, id, (int)rank);
+    if (r != ncclSuccess) {
+      ctx->comm = nullptr;
+      return bail(BPC_ERR_NCCL);
+    }
+  }
+  *out = ctx;
+  return BPC_OK;
+}
+
+bpc_status bpc_compress(bpc_ctx* ctx, const float* d_grad) {
+  if (!ctx || !d_grad) return BPC_ERR_INVALID_ARGUMENT;
+  if (ctx->phase != 0) return BPC_ERR_BAD_STATE;
+  CompressParams p = base_params(ctx);
+  p.grad = d_grad;
+  p.err = ctx->e;
+  p.out = ctx->send;
+  p.items = ctx->d_witems;
+  p.n_items = ctx->n_witems;
+  p.raw_tiles = ctx->d_wraw;
+  p.n_raw_tiles = ctx->n_wraw;
+  p.stage = 0;
+  cudaEvent_t b = nullptr;
+  timer_begin(ctx, BPC_TIMER_COMPRESS, &b);
+  CK(launch_compress(ctx->cfg.comp.kind, false, p, ctx->stream), "worker compress launch");
+  timer_end(ctx, BPC_TIMER_COMPRESS, b);
+  ctx->launches++;
+  ctx->phase = 1;
+  return BPC_OK;
+}
+
+bpc_status bpc_exchange_push(bpc_ctx* ctx) {
+  if (!ctx) return BPC_ERR_INVALID_ARGUMENT;
+  if (ctx->phase != 1) return BPC_ERR_BAD_STATE;
+  const int n = ctx->cfg.world_size, rank = ctx->cfg.rank;
+  if (n > 1 && ctx->comm) {
+    const Plan& P = ctx->plan;
+    cudaEvent_t b = nullptr;
+    timer_begin(ctx, BPC_TIMER_PUSH, &b);
+    const uint64_t slot = P.seg_bytes[rank];
+    NK(ncclGroupStart(), "group start");
+    for (int r = 0; r < n; r++) {
+      if (r == rank) continue;
+      if (P.seg_bytes[r]) NK(ncclSend(ctx->send + P.seg_off[r], P.seg_bytes[r], ncclUint8, r, ctx->comm, ctx->stream), "send");
+      if (slot) NK(ncclRecv(ctx->recv + r * slot, slot, ncclUint8, r, ctx->comm, ctx->stream), "recv");
+    }
+    NK(ncclGroupEnd(), "group end");
+    if (slot) CK(cudaMemcpyAsync(ctx->recv + rank * slot, ctx->send + P.seg_off[rank], slot,
+                                 cudaMemcpyDeviceToDevice, ctx->stream), "self copy");
+    timer_end(ctx, BPC_TIMER_PUSH, b);
+  }
+  // n == 1: RECV aliases SEND.  n > 1 without a communicator: the caller performed
+  // the exchange through bpc_buffer / bpc_peer_segment (external exchange).
+  ctx->phase = 2;
+  return BPC_OK;
+}
+
+bpc_status bpc_server(bpc_ctx* ctx) {
+  if (!ctx) return BPC_ERR_INVALID_ARGUMENT;
+  if (ctx->phase != 2) return BPC_ERR_BAD_STATE;
+  CompressParams p = base_params(ctx);
+  p.recv = ctx->recv;
+  p.slot_bytes = ctx->cfg.world_size == 1 ? 0 : ctx->plan.seg_bytes[ctx->cfg.rank];
+  p.etl = ctx->etl;
+  p.out = ctx->pbuf;
+  p.items = ctx->d_sitems;
+  p.n_items = ctx->n_sitems;
+  p.raw_tiles = ctx->d_sraw;
+  p.n_raw_tiles = ctx->n_sraw;
+  p.stage = 1;
+  if (ctx->cfg.world_size == 1) {
+    // RECV aliases SEND: recv offsets equal payload offsets (one segment)
+  }
+  cudaEvent_t b = nullptr;
+  timer_begin(ctx, BPC_TIMER_SERVER, &b);
+  CK(launch_compress(ctx->cfg.comp.kind, true, p, ctx->stream), "server launch");
+  timer_end(ctx, BPC_TIMER_SERVER, b);
+  ctx->launches++;
+  ctx->phase = 3;
+  return BPC_OK;
+}
+
+bpc_status bpc_exchange_pull(bpc_ctx* ctx) {
+  if (!ctx) return BPC_ERR_INVALID_ARGUMENT;
+  if (ctx->phase != 3) return BPC_ERR_BAD_STATE;
+  const int n = ctx->cfg.world_size, rank = ctx->cfg.rank;
+  if (n > 1 && ctx->comm) {
+    const Plan& P = ctx->plan;
+    cudaEvent_t b = nullptr;
+    timer_begin(ctx, BPC_TIMER_PULL, &b);
+    NK(ncclGroupStart(), "group start");
+    for (int r = 0; r < n; r++) {
+      if (r == rank) continue;
+      if (P.seg_bytes[rank]) NK(ncclSend(ctx->pbuf + P.seg_off[rank], P.seg_bytes[rank], ncclUint8, r, ctx->comm, ctx->stream), "send");
+      if (P.seg_bytes[r]) NK(ncclRecv(ctx->pbuf + P.seg_off[r], P.seg_bytes[r], ncclUint8, r, ctx->comm, ctx->stream), "recv");
+    }
+    NK(ncclGroupEnd(), "group end");
+    timer_end(ctx, BPC_TIMER_PULL, b);
+  }
+  ctx->phase = 4;
+  return BPC_OK;
+}
+
+bpc_status bpc_aggregate(bpc_ctx* ctx) {
+  if (!ctx) return BPC_ERR_INVALID_ARGUMENT;
+  if (ctx->cfg.world_size > 1 && !ctx->comm) return BPC_ERR_BAD_STATE;
+  bpc_status s = bpc_exchange_push(ctx);
+  if (s != BPC_OK) return s;
+  if ((s = bpc_server(ctx)) != BPC_OK) return s;
+  return bpc_exchange_pull(ctx);
+}
+
+bpc_status bpc_step(bpc_ctx* ctx, float* d_params, float lr) {
+  if (!ctx || !d_params) return BPC_ERR_INVALID_ARGUMENT;
+  if (ctx->phase != 4) return BPC_ERR_BAD_STATE;
+  const bpc_config& c = ctx->cfg;
+  UpdateParams p = {};
+  p.pbuf = ctx->pbuf;
+  p.chunks = ctx->d_chunks;
+  p.tiles = ctx->d_utiles;
+  p.n_tiles = ctx->n_utiles;
+  p.m = ctx->m;
+  p.v = ctx->v;
+  p.x = d_params;
+  p.beta1 = c.beta1;
+  p.beta2 = c.beta2;
+  p.omb1 = (float)(1.0 - (double)c.beta1);
+  p.omb2 = (float)(1.0 - (double)c.beta2);
+  p.bc1 = (float)(1.0 - std::pow((double)c.beta1, (double)ctx->t));   // R16
+  p.bc2 = (float)(1.0 - std::pow((double)c.beta2, (double)ctx->t));
+  p.eps = c.eps;
+  p.lr = lr;
+  p.wd = c.weight_decay;
+  p.bits = c.comp.bits;
+  cudaEvent_t b = nullptr;
+  timer_begin(ctx, BPC_TIMER_UPDATE, &b);
+  CK(launch_update(c.comp.kind, p, ctx->stream), "update launch");
+  timer_end(ctx, BPC_TIMER_UPDATE, b);
+  ctx->launches++;
+  ctx->t++;
+  ctx->phase = 0;
+  return BPC_OK;
+}
+
+bpc_status bpc_sync(bpc_ctx* ctx) {
+  if (!ctx) return BPC_ERR_INVALID_ARGUMENT;
+  CK(cudaStreamSynchronize(ctx->stream), "stream sync");
+  if (ctx->comm) {
+    ncclResult_t ar;
+    if (ncclCommGetAsyncError(ctx->comm, &ar) != ncclSuccess || ar != ncclSuccess) {
+      ctx->err = "NCCL async error";
+      return BPC_ERR_NCCL;
+    }
+  }
+  unsigned int flag = 0;
+  CK(cudaMemcpy(&flag, ctx->d_flag, 4, cudaMemcpyDeviceToHost), "flag read");
+  if (flag) {
+    CK(cudaMemset(ctx->d_flag, 0, 4), "flag reset");
+    ctx->err = "non-finite gradient";
+    return BPC_ERR_NONFINITE;
+  }
+  return BPC_OK;
+}
+
+bpc_status bpc_finalize(bpc_ctx* ctx) {
+  if (!ctx) return BPC_ERR_INVALID_ARGUMENT;
+  cudaStreamSynchronize(ctx->stream);
+  free_ctx(ctx);
+  return BPC_OK;
+}
+
+bpc_status bpc_get_plan(const bpc_ctx* ctx, bpc_plan_summary* out) {
+  if (!ctx || !out) return BPC_ERR_INVALID_ARGUMENT;
+  fill_summary(ctx->plan, ctx->cfg.rank, out);
+  return BPC_OK;
+}
+
+bpc_status bpc_get_chunk(const bpc_ctx* ctx, uint32_t chunk, bpc_chunk_info* out) {
+  if (!ctx || !out || chunk >= ctx->plan.chunks.size()) return BPC_ERR_INVALID_ARGUMENT;
+  *out = ctx->plan.chunks[chunk];
+  return BPC_OK;
+}
+
+bpc_status bpc_peer_segment(const bpc_ctx* ctx, int32_t peer, uint64_t* offset, uint64_t* bytes) {
+  if (!ctx || !offset || !bytes || peer < 0 || peer >= ctx->cfg.world_size) return BPC_ERR_INVALID_ARGUMENT;
+  *offset = ctx->plan.seg_off[peer];
+  *bytes = ctx->plan.seg_bytes[peer];
+  return BPC_OK;
+}
+
+static bool buffer_of(const bpc_ctx* ctx, int32_t which, void** p, uint64_t* bytes) {
+  const uint64_t D = round_up(ctx->plan.D, 4);
+  switch (which) {
+    case BPC_BUF_SEND: *p = ctx->send; *bytes = ctx->plan.send_bytes; return true;
+    case BPC_BUF_RECV: *p = ctx->recv; *bytes = ctx->recv_bytes; return true;
+    case BPC_BUF_P: *p = ctx->pbuf; *bytes = ctx->plan.send_bytes; return true;
+    case BPC_BUF_WORKER_ERR: *p = ctx->e; *bytes = 4 * D; return true;
+    case BPC_BUF_SERVER_ERR: *p = ctx->etl; *bytes = 4 * ctx->plan.etl_elems; return true;
+    case BPC_BUF_M: *p = ctx->m; *bytes = 4 * D; return true;
+    case BPC_BUF_V: *p = ctx->v; *bytes = 4 * D; return true;
+  }
+  return false;
+}
+
+bpc_status bpc_buffer(const bpc_ctx* ctx, int32_t which, void** d_ptr, uint64_t* bytes) {
+  if (!ctx || !d_ptr || !bytes) return BPC_ERR_INVALID_ARGUMENT;
+  return buffer_of(ctx, which, d_ptr, bytes) ? BPC_OK : BPC_ERR_INVALID_ARGUMENT;
+}
+
+bpc_status bpc_copy_state(bpc_ctx* ctx, int32_t which, void* host_dst, uint64_t bytes) {
+  void* p;
+  uint64_t b;
+  if (!ctx || !host_dst || !buffer_of(ctx, which, &p, &b)) return BPC_ERR_INVALID_ARGUMENT;
+  if (bytes != b) return BPC_ERR_SIZE_MISMATCH;
+  CK(cudaStreamSynchronize(ctx->stream), "sync");
+  if (b) CK(cudaMemcpy(host_dst, p, b, cudaMemcpyDeviceToHost), "copy state");
+  return BPC_OK;
+}
+
+bpc_status bpc_load_state(bpc_ctx* ctx, int32_t which, const void* host_src, uint64_t bytes) {
+  void* p;
+  uint64_t b;
+  if (!ctx || !host_src || !buffer_of(ctx, which, &p, &b)) return BPC_ERR_INVALID_ARGUMENT;
+  if (bytes != b) return BPC_ERR_SIZE_MISMATCH;
+  CK(cudaStreamSynchronize(ctx->stream), "sync");
+  if (b) CK(cudaMemcpy(p, host_src, b, cudaMemcpyHostToDevice), "load state");
+  return BPC_OK;
+}
+
+bpc_status bpc_get_step(const bpc_ctx* ctx, uint32_t* t) {
+  if (!ctx || !t) return BPC_ERR_INVALID_ARGUMENT;
+  *t = ctx->t;
+  return BPC_OK;
+}
+
+bpc_status bpc_set_step(bpc_ctx* ctx, uint32_t t) {
+  if (!ctx || t < 1) return BPC_ERR_INVALID_ARGUMENT;
+  ctx->t = t;
+  return BPC_OK;
+}
+
+bpc_status bpc_set_timing(bpc_ctx* ctx, int32_t enable) {
+  if (!ctx) return BPC_ERR_INVALID_ARGUMENT;
+  cudaStreamSynchronize(ctx->stream);
+  for (auto& ev : ctx->events) {
+    cudaEventDestroy(ev.second.first);
+    cudaEventDestroy(ev.second.second);
+  }
+  ctx->events.clear();
+  ctx->timing = enable != 0;
+  return BPC_OK;
+}
+
+bpc_status bpc_get_timing(bpc_ctx* ctx, float ms[BPC_NUM_TIMERS], uint32_t count[BPC_NUM_TIMERS]) {
+  if (!ctx || !ms || !count) return BPC_ERR_INVALID_ARGUMENT;
+  for (int i = 0; i < BPC_NUM_TIMERS; i++) {
+    ms[i] = 0.f;
+    count[i] = 0;
+  }
+  CK(cudaStreamSynchronize(ctx->stream), "sync");
+  for (auto& ev : ctx->events) {
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, ev.second.first, ev.second.second), "elapsed");
+    ms[ev.first] += t;
+    count[ev.first]++;
+  }
+  return BPC_OK;
+}
+
+uint64_t bpc_launch_count(const bpc_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+}  // extern "C"

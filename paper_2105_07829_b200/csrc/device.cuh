@@ -1,0 +1,166 @@
+// device.cuh — sm_100a device helpers shared by the libbpc kernels:
+// thread-block-cluster barriers and DSMEM, the fp64 pairwise tree (R6),
+// Philox4x32-10 (R13), warp bit packing, exact-IEEE fp32
+// arithmetic wrappers.  Nothing here is shared with oracle/.
+#pragma once
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kernels.h"
+
+namespace bpc {
+namespace cg = cooperative_groups;
+
+constexpr int SLICE = 16384;           // elements per CTA of a compression unit
+constexpr int NT = 512;                // threads per compress CTA
+constexpr int NWARP = NT / 32;         // 16
+constexpr int IT = SLICE / 4 / NT;     // float4 per thread per slice = 8
+static_assert(IT * NWARP == 128, "slice reduction expects 128 warp subtrees");
+constexpr int UNT = 256;               // threads per update CTA
+constexpr int UTILE = 4096;            // elements per update tile
+constexpr int UIT = UTILE / 4 / UNT;   // 4
+
+// ---------------------------------------------------------------- cluster
+__device__ __forceinline__ uint32_t cta_rank_in_cluster() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_index() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  cluster_arrive();
+  cluster_wait();
+}
+// address of `p` (a shared variable of this CTA) in CTA `rank` of the cluster
+template <class T>
+__device__ __forceinline__ T* dsmem(T* p, uint32_t rank) {
+  return cg::this_cluster().map_shared_rank(p, rank);
+}
+
+// ---------------------------------------------------------------- exact fp32 ops
+// -fmad=false is also set, these keep every operation a single IEEE op.
+__device__ __forceinline__ float fadd(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float fsub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float fmul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float fdiv(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+// server mean (R5): (float)(acc * (1/n) + e~), two fp64 roundings then one to fp32
+__device__ __forceinline__ float mean_plus(double acc, double inv_n, double et) {
+  return __double2float_rn(dadd(dmul(acc, inv_n), et));
+}
+
+// ---------------------------------------------------------------- pairwise tree (R6)
+// Lane l holds the subtree sum of its 4 consecutive elements; the xor butterfly
+// with masks 1..16 builds the perfect binary tree over the warp's 128 elements
+// (both lanes of a pair hold a+b == b+a).
+__device__ __forceinline__ double warp_tree(double a) {
+#pragma unroll
+  for (int m = 1; m < 32; m <<= 1) a = a + __shfl_xor_sync(0xffffffffu, a, m);
+  return a;
+}
+__device__ __forceinline__ double leaf4_abs(float4 q) {
+  return ((double)fabsf(q.x) + (double)fabsf(q.y)) + ((double)fabsf(q.z) + (double)fabsf(q.w));
+}
+__device__ __forceinline__ double leaf4_sq(float4 q) {
+  return ((double)q.x * (double)q.x + (double)q.y * (double)q.y) +
+         ((double)q.z * (double)q.z + (double)q.w * (double)q.w);
+}
+
+// ---------------------------------------------------------------- Philox4x32-10 (R13)
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; r++) {
+    if (r) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+  }
+  return c;
+}
+// the 4 words of elements 4*g .. 4*g+3 of unit `chunk` (counter layout R13)
+__device__ __forceinline__ uint4 rng4(uint64_t seed, uint32_t g, uint32_t chunk, uint32_t t,
+                                      uint32_t stage, uint32_t rank) {
+  return philox4x32_10(make_uint4(g, chunk, t, (stage << 31) | rank), (uint32_t)seed,
+                       (uint32_t)(seed >> 32));
+}
+
+// ---------------------------------------------------------------- bit packing
+// Lane l owns a field of nb bits at bit nb*l of the warp's 32*nb bits (= nb words).
+// Returns, in lanes 0..nb-1, word `lane` of the packed stream (LSB-first).
+__device__ __forceinline__ uint32_t warp_pack(uint32_t field, int nb) {
+  const int lane = threadIdx.x & 31;
+  const int w = lane < nb ? lane : 0;
+  const int first = (32 * w) / nb;
+  const int last = (32 * w + 31) / nb;
+  uint32_t acc = 0;
+#pragma unroll
+  for (int it = 0; it < 9; it++) {
+    const int src = min(first + it, 31);
+    const uint32_t v = __shfl_sync(0xffffffffu, field, src);
+    if (first + it <= last) {
+      const int pos = nb * (first + it) - 32 * w;
+      acc |= pos >= 0 ? (v << pos) : (v >> (-pos));
+    }
+    if (it * nb >= 32 + nb) break;   // uniform: enough lanes visited for any word
+  }
+  return acc;
+}
+// nb-bit field (nb <= 32) starting at bit `pos` of a little-endian u32 stream
+__device__ __forceinline__ uint32_t load_field(const uint32_t* words, uint64_t pos, int nb) {
+  const uint64_t w = pos >> 5;
+  const int sh = (int)(pos & 31);
+  uint64_t v = words[w];
+  if (sh + nb > 32) v |= (uint64_t)words[w + 1] << 32;
+  const uint64_t mask = nb == 32 ? 0xFFFFFFFFull : ((1ull << nb) - 1);
+  return (uint32_t)((v >> sh) & mask);
+}
+
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ float4 ldg4_stream(const float* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+
+__device__ __forceinline__ float4 load4_masked(const float* p, uint32_t j, uint32_t L) {
+  if (j + 4 <= L) return ld4(p + j);
+  float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (j < L) r.x = p[j];
+  if (j + 1 < L) r.y = p[j + 1];
+  if (j + 2 < L) r.z = p[j + 2];
+  return r;
+}
+__device__ __forceinline__ void store4_masked(float* p, uint32_t j, uint32_t L, float4 v) {
+  if (j + 4 <= L) {
+    st4(p + j, v);
+    return;
+  }
+  if (j < L) p[j] = v.x;
+  if (j + 1 < L) p[j + 1] = v.y;
+  if (j + 2 < L) p[j + 2] = v.z;
+}
+__device__ __forceinline__ float get(const float4& v, int u) {
+  return u == 0 ? v.x : (u == 1 ? v.y : (u == 2 ? v.z : v.w));
+}
+__device__ __forceinline__ void set(float4& v, int u, float x) {
+  if (u == 0) v.x = x; else if (u == 1) v.y = x; else if (u == 2) v.z = x; else v.w = x;
+}
+
+}  // namespace bpc

@@ -1,0 +1,69 @@
+// kernels.h — device-side tables and host launchers of libbpc (internal).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace bpc {
+
+// one compression unit (chunk) as the kernels see it
+struct DevChunk {
+  uint64_t off;    // flat element offset
+  uint64_t pay;    // byte offset of its payload in SEND / P
+  uint64_t recv;   // byte offset inside each RECV slot (owned chunks)
+  uint64_t etl;    // element offset in SERVER_ERR (owned, compressed, use_ef)
+  uint32_t len;    // L
+  uint32_t k;      // sparse k
+  uint32_t id;     // global chunk id (Philox counter word 1)
+  uint32_t raw;    // 1 = NONE payload
+};
+
+// a piece of a chunk processed by one CTA (raw tiles, update tiles)
+struct Tile {
+  uint32_t chunk;  // index into the chunk table
+  uint32_t start;  // first element, relative to the chunk
+  uint32_t len;
+  uint32_t pad;
+};
+
+struct CompressParams {
+  const float* grad;      // worker: g (flat)
+  float* err;             // worker: e (flat)
+  uint8_t* out;           // worker: SEND; server: P
+  const uint8_t* recv;    // server: RECV (n slots)
+  uint64_t slot_bytes;    // server: bytes per RECV slot
+  float* etl;             // server: e~ (compact)
+  const DevChunk* chunks;
+  const uint32_t* items;  // compressed chunk indices handled by this launch
+  uint32_t n_items;
+  const Tile* raw_tiles;  // raw tiles handled by this launch
+  uint32_t n_raw_tiles;
+  uint32_t cs;            // CTAs per cluster
+  uint32_t n;             // world size
+  double inv_n;           // 1.0 / n
+  uint32_t t, rank, stage;
+  uint64_t seed;
+  uint32_t bits;
+  int32_t randk_scaled, use_ef;
+  int32_t check_finite;
+  unsigned int* flag;     // non-finite flag
+};
+
+struct UpdateParams {
+  const uint8_t* pbuf;
+  const DevChunk* chunks;
+  const Tile* tiles;
+  uint32_t n_tiles;
+  float* m;
+  float* v;
+  float* x;
+  float beta1, beta2, omb1, omb2, bc1, bc2, eps, lr, wd;
+  uint32_t bits;
+};
+
+// host launchers (return the launch error)
+cudaError_t launch_compress(int kind, bool server, const CompressParams& p, cudaStream_t s);
+cudaError_t launch_update(int kind, const UpdateParams& p, cudaStream_t s);
+size_t compress_smem_bytes();
+cudaError_t compress_max_active_clusters(int kind, bool server, uint32_t cs, int* out);
+
+}  // namespace bpc

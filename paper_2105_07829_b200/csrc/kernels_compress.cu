@@ -1,0 +1,663 @@
+// kernels_compress.cu — worker compress and server
+// decompress-sum-recompress (A5-A7) kernels for sm_100a.
+//
+// One thread-block cluster per compression unit (chunk of <= cs * 2^14
+// elements, R1): CTA r of the cluster owns slice
+// [r * 2^14, (r + 1) * 2^14) of the unit and keeps it on chip (64 KB of shared
+// memory) between the unit-wide reduction and the write-back, so every HBM
+// byte is read and written once:
+//   worker  q = g + e (Alg. 4 l.5) -> C(q) (l.6) -> e = q - dec (l.7)
+//   server  Delta = (1/n) sum_i dec(delta_i) + e~ (l.10)
+//           -> p = C(Delta) (l.11) -> e~ = Delta - dec(p) (l.13)
+// The unit-wide fp64 reduction (the ||.||_1 of the scaled sign, PAPER.md:318,
+// or the ||.||_2 of dithering) follows the pairwise tree of DESIGN.md R6:
+// lane -> warp butterfly -> CTA -> cluster over DSMEM.  Top-k / random-k run a
+// cluster-wide 4 x 8-bit radix select (R9, R10) and an ordered compaction.
+// Raw (below-threshold) units ride the same launch as plain tiles.
+#include "device.cuh"
+
+namespace bpc {
+
+enum { K_NONE = 0, K_SIGN = 2, K_TOPK = 3, K_RANDK = 4, K_LDITHER = 5, K_NDITHER = 6 };
+
+struct __align__(16) Smem {
+  float4 q[SLICE / 4];      // the slice of q (worker) or Delta (server)
+  double red[128];          // warp subtree sums
+  double part;              // this slice's subtree sum (read through DSMEM)
+  double total;             // unit total
+  uint32_t hist[2][256];    // radix-select histograms (read through DSMEM)
+  uint32_t tot[256];
+  uint32_t cnt[2];          // (#key > T, #key == T) of this slice (DSMEM)
+  uint32_t scan[NWARP + 1];
+  uint32_t info[4];
+};
+
+size_t compress_smem_bytes() { return sizeof(Smem); }
+
+// ---------------------------------------------------------------- reductions
+__device__ __forceinline__ double cluster_tree_total(Smem& sm, const double (&lv)[IT],
+                                                     uint32_t cs) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int it = 0; it < IT; it++) {
+    const double a = warp_tree(lv[it]);
+    if (lane == 0) sm.red[it * NWARP + warp] = a;   // subtree of elements [128 m, 128 m + 128)
+  }
+  __syncthreads();
+  if (warp == 0) {
+    double r = (sm.red[4 * lane] + sm.red[4 * lane + 1]) + (sm.red[4 * lane + 2] + sm.red[4 * lane + 3]);
+    r = warp_tree(r);
+    if (lane == 0) sm.part = r;
+  }
+  cluster_sync_all();   // publish every slice's sum to the cluster
+  if (threadIdx.x == 0) {
+    double v[16];
+    for (uint32_t r = 0; r < cs; r++) v[r] = *dsmem(&sm.part, r);
+    for (uint32_t w = 1; w < cs; w <<= 1)
+      for (uint32_t r = 0; r + w < cs; r += 2 * w) v[r] = v[r] + v[r + w];
+    sm.total = v[0];
+  }
+  __syncthreads();
+  return sm.total;
+}
+
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* scan, uint32_t& total) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) scan[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t w = lane < NWARP ? scan[lane] : 0u;
+    uint32_t wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    if (lane < NWARP) scan[lane] = wi - w;
+    if (lane == NWARP - 1) scan[NWARP] = wi;
+  }
+  __syncthreads();
+  const uint32_t r = scan[warp] + incl - v;
+  total = scan[NWARP];
+  __syncthreads();
+  return r;
+}
+
+// ---------------------------------------------------------------- producers
+// worker: q = g + e (use_ef) or q = g; slice -> sm.q; leaf sums -> lv
+template <bool L2, bool LEAF>
+__device__ __forceinline__ void produce_worker(const CompressParams& p, const DevChunk& c, Smem& sm,
+                                               uint32_t s0, double (&lv)[IT]) {
+  const float* g = p.grad + c.off;
+  const float* e = p.err + c.off;
+  const uint32_t L = c.len;
+  bool bad = false;
+#pragma unroll
+  for (int it = 0; it < IT; it++) {
+    const uint32_t i4 = it * NT + threadIdx.x;
+    const uint32_t j = s0 + 4 * i4;
+    float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (j < L) {
+      const float4 g4 = load4_masked(g, j, L);
+      if (p.check_finite)
+        bad |= !(isfinite(g4.x) && isfinite(g4.y) && isfinite(g4.z) && isfinite(g4.w));
+      if (p.use_ef) {
+        const float4 e4 = load4_masked(e, j, L);
+        q = make_float4(fadd(g4.x, e4.x), fadd(g4.y, e4.y), fadd(g4.z, e4.z), fadd(g4.w, e4.w));
+        // masked lanes: 0 + 0 = +0 (padding)
+      } else {
+        q = g4;
+      }
+    }
+    sm.q[i4] = q;
+    if (LEAF) lv[it] = L2 ? leaf4_sq(q) : leaf4_abs(q);
+  }
+  if (bad) atomicOr(p.flag, 1u);
+}
+
+// server, dense kinds: Delta_j = (float)(sum_i dec(delta_i)_j * (1/n) + e~_j)
+template <int KIND>
+__device__ __forceinline__ void produce_server_dense(const CompressParams& p, const DevChunk& c,
+                                                     Smem& sm, uint32_t s0, double (&lv)[IT]) {
+  const uint32_t L = c.len;
+  const int b = (int)p.bits;
+  const float sl = (float)((1u << (b - 1)) - 1u);
+  const int cmax = (1 << (b - 1)) - 1;
+  const float* et = p.etl + c.etl;
+#pragma unroll 2
+  for (int it = 0; it < IT; it++) {
+    const uint32_t i4 = it * NT + threadIdx.x;
+    const uint32_t j = s0 + 4 * i4;
+    float4 d = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (j < L) {
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (uint32_t r = 0; r < p.n; r++) {
+        const uint8_t* pl = p.recv + r * p.slot_bytes + c.recv;
+        const uint32_t* words = reinterpret_cast<const uint32_t*>(pl + 4);
+        const float hdr = *reinterpret_cast<const float*>(pl);
+        if (KIND == K_SIGN) {
+          const uint32_t nib = (words[j >> 5] >> (j & 31)) & 15u;
+#pragma unroll
+          for (int u = 0; u < 4; u++)
+            if (j + u < L) acc[u] += (double)(((nib >> u) & 1u) ? hdr : -hdr);
+        } else {
+          const uint32_t field = load_field(words, (uint64_t)b * j, 4 * b);
+          const float unit = fdiv(hdr, sl);
+#pragma unroll
+          for (int u = 0; u < 4; u++) {
+            const uint32_t code = (field >> (b * u)) & ((1u << b) - 1u);
+            float mag;
+            if (KIND == K_LDITHER) {
+              mag = fmul((float)(code >> 1), unit);
+            } else {
+              const uint32_t cl = code >> 1;
+              const float level = cl == 0 ? 0.f : __uint_as_float((uint32_t)(127 - (cmax - (int)cl)) << 23);
+              mag = fmul(level, hdr);
+            }
+            if (j + u < L) acc[u] += (double)((code & 1u) ? mag : -mag);
+          }
+        }
+      }
+      float4 e4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (p.use_ef) e4 = load4_masked(et, j, L);
+      d.x = mean_plus(acc[0], p.inv_n, (double)e4.x);
+      d.y = j + 1 < L ? mean_plus(acc[1], p.inv_n, (double)e4.y) : 0.f;
+      d.z = j + 2 < L ? mean_plus(acc[2], p.inv_n, (double)e4.z) : 0.f;
+      d.w = j + 3 < L ? mean_plus(acc[3], p.inv_n, (double)e4.w) : 0.f;
+    }
+    sm.q[i4] = d;
+    lv[it] = (KIND == K_SIGN) ? leaf4_abs(d) : leaf4_sq(d);
+  }
+}
+
+__device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* a, uint32_t n, uint32_t key) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (a[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// server, sparse kinds: Delta_j = (float)(sum over ranks holding j of val * (1/n) + e~_j)
+// (adding the implicit zeros of the other ranks leaves an fp64 sum that starts at +0 unchanged)
+__device__ __forceinline__ void produce_server_sparse(const CompressParams& p, const DevChunk& c,
+                                                      Smem& sm, uint32_t s0) {
+  const uint32_t L = c.len, k = c.k;
+  const float* et = p.etl + c.etl;
+  float* sq = reinterpret_cast<float*>(sm.q);
+#pragma unroll 2
+  for (int it = 0; it < IT; it++) {
+    const uint32_t i4 = it * NT + threadIdx.x;
+    const uint32_t j = s0 + 4 * i4;
+    float4 e4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (p.use_ef && j < L) e4 = load4_masked(et, j, L);
+    float4 d;
+    d.x = mean_plus(0.0, p.inv_n, (double)e4.x);
+    d.y = mean_plus(0.0, p.inv_n, (double)e4.y);
+    d.z = mean_plus(0.0, p.inv_n, (double)e4.z);
+    d.w = mean_plus(0.0, p.inv_n, (double)e4.w);
+    sm.q[i4] = d;
+  }
+  __syncthreads();
+  const uint32_t jlo = s0, jhi = min(s0 + (uint32_t)SLICE, L);
+  if (jlo >= jhi) return;
+  for (uint32_t r = 0; r < p.n; r++) {
+    const uint8_t* pl = p.recv + r * p.slot_bytes + c.recv;
+    const uint32_t* idx = reinterpret_cast<const uint32_t*>(pl + 8);
+    const float* val = reinterpret_cast<const float*>(pl + 8 + 4ull * k);
+    const uint32_t lo = lower_bound_u32(idx, k, jlo), hi = lower_bound_u32(idx, k, jhi);
+    for (uint32_t e = lo + threadIdx.x; e < hi; e += NT) {
+      const uint32_t j = idx[e];
+      bool first = true;
+      for (uint32_t r2 = 0; r2 < r && first; r2++) {
+        const uint32_t* idx2 = reinterpret_cast<const uint32_t*>(p.recv + r2 * p.slot_bytes + c.recv + 8);
+        const uint32_t pos = lower_bound_u32(idx2, k, j);
+        first = !(pos < k && idx2[pos] == j);
+      }
+      if (!first) continue;
+      double acc = 0.0;
+      acc += (double)val[e];
+      for (uint32_t r2 = r + 1; r2 < p.n; r2++) {
+        const uint8_t* pl2 = p.recv + r2 * p.slot_bytes + c.recv;
+        const uint32_t* idx2 = reinterpret_cast<const uint32_t*>(pl2 + 8);
+        const uint32_t pos = lower_bound_u32(idx2, k, j);
+        if (pos < k && idx2[pos] == j) acc += (double)reinterpret_cast<const float*>(pl2 + 8 + 4ull * k)[pos];
+      }
+      const double ev = p.use_ef ? (double)et[j] : 0.0;
+      sq[j - s0] = mean_plus(acc, p.inv_n, ev);
+    }
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------- emitters
+// scaled sign: s = (float)(||q||_1 / L), bit = q >= 0, err = q - dec
+__device__ __forceinline__ void emit_sign(const DevChunk& c, Smem& sm, uint32_t s0, uint32_t crank,
+                                          double total, uint8_t* pay, float* errp) {
+  const uint32_t L = c.len;
+  const float s = __double2float_rn(total / (double)L);
+  uint32_t* words = reinterpret_cast<uint32_t*>(pay + 4);
+  const int lane = threadIdx.x & 31;
+#pragma unroll 4
+  for (int it = 0; it < IT; it++) {
+    const uint32_t i4 = it * NT + threadIdx.x;
+    const uint32_t j = s0 + 4 * i4;
+    const float4 q = sm.q[i4];
+    uint32_t nib = 0;
+    float4 ev;
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const float qu = get(q, u);
+      const bool bit = !(qu < 0.f);
+      if (bit && j + u < L) nib |= 1u << u;
+      set(ev, u, bit ? fsub(qu, s) : fadd(qu, s));
+    }
+    if (errp && j < L) store4_masked(errp, j, L, ev);
+    uint32_t w = nib << (4 * (lane & 7));
+    w |= __shfl_xor_sync(0xffffffffu, w, 1);
+    w |= __shfl_xor_sync(0xffffffffu, w, 2);
+    w |= __shfl_xor_sync(0xffffffffu, w, 4);
+    if ((lane & 7) == 0 && j < L) words[j >> 5] = w;
+  }
+  if (crank == 0 && threadIdx.x == 0) *reinterpret_cast<float*>(pay) = s;
+}
+
+// linear dithering code (R11-R13)
+__device__ __forceinline__ uint32_t lin_code(float q, float N, float sl, float inv, uint32_t w) {
+  const uint32_t sign = !(q < 0.f);
+  uint32_t level = 0;
+  if (N != 0.f) {
+    const float r = fminf(fmul(fabsf(q), inv), sl);
+    const float l = floorf(r);
+    const float f = fsub(r, l);
+    const float u = (float)(w >> 8) * 0x1p-24f;
+    level = (uint32_t)l + (u < f ? 1u : 0u);
+  }
+  return sign | (level << 1);
+}
+// natural dithering code (R11-R13)
+__device__ __forceinline__ uint32_t nat_code(float q, float N, int cmax, float lmin, uint32_t w) {
+  const uint32_t sign = !(q < 0.f);
+  uint32_t code = 0;
+  if (N != 0.f) {
+    const float r = fminf(fdiv(fabsf(q), N), 1.0f);
+    const float u = (float)(w >> 8) * 0x1p-24f;
+    if (r >= lmin) {
+      const int eb = (int)(__float_as_uint(r) >> 23);        // r is normal and positive
+      const float lo = __uint_as_float((uint32_t)eb << 23);  // 2^floor(log2 r)
+      const float pup = fsub(fdiv(r, lo), 1.0f);
+      const int e_lev = (u < pup) ? eb - 127 + 1 : eb - 127;
+      code = (uint32_t)(cmax + e_lev);
+    } else {
+      code = (u < fdiv(r, lmin)) ? 1u : 0u;
+    }
+  }
+  return sign | (code << 1);
+}
+
+template <int KIND>
+__device__ __forceinline__ void emit_dither(const CompressParams& p, const DevChunk& c, Smem& sm,
+                                            uint32_t s0, uint32_t crank, double total, uint8_t* pay,
+                                            float* errp, uint32_t stage, uint32_t rrank) {
+  const uint32_t L = c.len;
+  const int b = (int)p.bits, nb = 4 * b;
+  const float N = __double2float_rn(sqrt(total));
+  const float sl = (float)((1u << (b - 1)) - 1u);
+  const float inv = N != 0.f ? fdiv(sl, N) : 0.f;
+  const float unit = fdiv(N, sl);
+  const int cmax = (1 << (b - 1)) - 1;
+  const float lmin = __uint_as_float((uint32_t)(127 - (cmax - 1)) << 23);
+  const uint32_t mask = (1u << b) - 1u;
+  uint32_t* words = reinterpret_cast<uint32_t*>(pay + 4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t nwords = ((uint64_t)b * L + 31) / 32;
+#pragma unroll 2
+  for (int it = 0; it < IT; it++) {
+    const uint32_t i4 = it * NT + threadIdx.x;
+    const uint32_t j = s0 + 4 * i4;
+    const float4 q = sm.q[i4];
+    uint32_t field = 0;
+    float4 ev = q;
+    if (j < L) {
+      const uint4 w4 = rng4(p.seed, j >> 2, c.id, p.t, stage, rrank);
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const uint32_t w = u == 0 ? w4.x : (u == 1 ? w4.y : (u == 2 ? w4.z : w4.w));
+        const float qu = get(q, u);
+        const uint32_t code = KIND == K_LDITHER ? lin_code(qu, N, sl, inv, w) : nat_code(qu, N, cmax, lmin, w);
+        if (j + u < L) field |= (code & mask) << (b * u);
+        float mag;
+        if (KIND == K_LDITHER) {
+          mag = fmul((float)(code >> 1), unit);
+        } else {
+          const uint32_t cl = code >> 1;
+          mag = fmul(cl == 0 ? 0.f : __uint_as_float((uint32_t)(127 - (cmax - (int)cl)) << 23), N);
+        }
+        set(ev, u, fsub(qu, (code & 1u) ? mag : -mag));
+      }
+      if (errp) store4_masked(errp, j, L, ev);
+    }
+    const uint32_t wd = warp_pack(field, nb);
+    const uint64_t wbase = (uint64_t)(s0 + 4 * (it * NT + 32 * warp)) / 32 * b;
+    if (lane < nb && wbase + lane < nwords) words[wbase + lane] = wd;
+  }
+  if (crank == 0 && threadIdx.x == 0) *reinterpret_cast<float*>(pay) = N;
+}
+
+// key of an element for the "k largest keys, lowest index first" selection:
+// top-k: |q| bits (R9); random-k: ~Philox word (k smallest words, R10)
+template <int KIND>
+__device__ __forceinline__ uint4 keys4(float4 q, uint32_t j, const CompressParams& p, uint32_t id,
+                                       uint32_t stage, uint32_t rrank) {
+  if (KIND == K_TOPK) {
+    return make_uint4(__float_as_uint(q.x) & 0x7fffffffu, __float_as_uint(q.y) & 0x7fffffffu,
+                      __float_as_uint(q.z) & 0x7fffffffu, __float_as_uint(q.w) & 0x7fffffffu);
+  } else {
+    const uint4 w = rng4(p.seed, j >> 2, id, p.t, stage, rrank);
+    return make_uint4(~w.x, ~w.y, ~w.z, ~w.w);
+  }
+}
+__device__ __forceinline__ uint32_t getu(const uint4& v, int u) {
+  return u == 0 ? v.x : (u == 1 ? v.y : (u == 2 ? v.z : v.w));
+}
+
+template <int KIND>
+__device__ void emit_sparse(const CompressParams& p, const DevChunk& c, Smem& sm, uint32_t s0,
+                            uint32_t crank, uint8_t* pay, float* errp, uint32_t stage, uint32_t rrank) {
+  const uint32_t L = c.len, k = c.k, cs = p.cs;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t prefix = 0, pmask = 0, kk = k;
+  // ---- radix select of the k-th largest key over the whole unit (cluster)
+  for (int pass = 0; pass < 4; pass++) {
+    const int shift = 24 - 8 * pass;
+    uint32_t* h = sm.hist[pass & 1];
+    if (threadIdx.x < 256) h[threadIdx.x] = 0;
+    __syncthreads();
+#pragma unroll 2
+    for (int it = 0; it < IT; it++) {
+      const uint32_t i4 = it * NT + threadIdx.x;
+      const uint32_t j = s0 + 4 * i4;
+      uint4 kq = make_uint4(0, 0, 0, 0);
+      if (j < L) kq = keys4<KIND>(sm.q[i4], j, p, c.id, stage, rrank);
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const uint32_t key = getu(kq, u);
+        const bool part = (j + u < L) && ((key & pmask) == prefix);
+        const uint32_t dig = part ? ((key >> shift) & 255u) : (0x100u | (uint32_t)lane);
+        const uint32_t peers = __match_any_sync(0xffffffffu, dig);
+        if (part && (__ffs(peers) - 1) == lane) atomicAdd(&h[dig], (uint32_t)__popc(peers));
+      }
+    }
+    cluster_sync_all();
+    if (threadIdx.x < 256) {
+      uint32_t s = 0;
+      for (uint32_t r = 0; r < cs; r++) s += dsmem(h, r)[threadIdx.x];
+      sm.tot[threadIdx.x] = s;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t c8[8], S = 0;
+#pragma unroll
+      for (int i = 0; i < 8; i++) {
+        c8[i] = sm.tot[255 - 8 * lane - i];
+        S += c8[i];
+      }
+      uint32_t incl = S;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const uint32_t excl = incl - S;
+      if (excl < kk && kk <= incl) {
+        uint32_t above = excl;
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+          if (above + c8[i] >= kk) {
+            sm.info[0] = 255 - 8 * lane - i;
+            sm.info[1] = above;
+            break;
+          }
+          above += c8[i];
+        }
+      }
+    }
+    __syncthreads();
+    prefix |= sm.info[0] << shift;
+    pmask |= 0xFFu << shift;
+    kk -= sm.info[1];
+    __syncthreads();
+  }
+  const uint32_t T = prefix;   // the k-th largest key; take kk of the keys equal to T (lowest index)
+  // ---- per-slice counts -> cluster prefix
+  if (threadIdx.x < 2) sm.cnt[threadIdx.x] = 0;
+  __syncthreads();
+  {
+    uint32_t ngt = 0, neq = 0;
+    for (int it = 0; it < IT; it++) {
+      const uint32_t i4 = it * NT + threadIdx.x;
+      const uint32_t j = s0 + 4 * i4;
+      if (j >= L) continue;
+      const uint4 kq = keys4<KIND>(sm.q[i4], j, p, c.id, stage, rrank);
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        if (j + u < L) {
+          const uint32_t key = getu(kq, u);
+          ngt += key > T;
+          neq += key == T;
+        }
+      }
+    }
+    ngt = __reduce_add_sync(0xffffffffu, ngt);
+    neq = __reduce_add_sync(0xffffffffu, neq);
+    if (lane == 0) {
+      atomicAdd(&sm.cnt[0], ngt);
+      atomicAdd(&sm.cnt[1], neq);
+    }
+  }
+  cluster_sync_all();
+  if (threadIdx.x == 0) {
+    uint32_t eqb = 0, selb = 0;
+    for (uint32_t r = 0; r < crank; r++) {
+      const uint32_t* cr = dsmem(sm.cnt, r);
+      const uint32_t g = cr[0], e = cr[1];
+      selb += g + min(e, kk > eqb ? kk - eqb : 0u);
+      eqb += e;
+    }
+    sm.info[2] = selb;
+    sm.info[3] = min(sm.cnt[1], kk > eqb ? kk - eqb : 0u);
+  }
+  __syncthreads();
+  const uint32_t take_eq = sm.info[3];
+  uint32_t sel_run = sm.info[2], eq_run = 0;
+  uint32_t* idx_out = reinterpret_cast<uint32_t*>(pay + 8);
+  float* val_out = reinterpret_cast<float*>(pay + 8 + 4ull * k);
+  const bool scaled = KIND == K_RANDK && p.randk_scaled;
+  const float scale = (float)((double)L / (double)k);
+  // ---- ordered compaction (index ascending) + error write
+  for (int it = 0; it < IT; it++) {
+    const uint32_t i4 = it * NT + threadIdx.x;
+    const uint32_t j = s0 + 4 * i4;
+    const float4 q = sm.q[i4];
+    uint32_t gtm = 0, eqm = 0;
+    if (j < L) {
+      const uint4 kq = keys4<KIND>(q, j, p, c.id, stage, rrank);
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const uint32_t key = getu(kq, u);
+        if (j + u < L) {
+          gtm |= (uint32_t)(key > T) << u;
+          eqm |= (uint32_t)(key == T) << u;
+        }
+      }
+    }
+    float4 ev = q;
+    if (__syncthreads_or((int)(gtm | eqm))) {
+      uint32_t te, ts;
+      const uint32_t ee = block_excl_scan(__popc(eqm), sm.scan, te);
+      uint32_t selm = gtm, rr = eq_run + ee;
+#pragma unroll
+      for (int u = 0; u < 4; u++)
+        if ((eqm >> u) & 1u) {
+          if (rr < take_eq) selm |= 1u << u;
+          rr++;
+        }
+      uint32_t pos = sel_run + block_excl_scan(__popc(selm), sm.scan, ts);
+#pragma unroll
+      for (int u = 0; u < 4; u++)
+        if ((selm >> u) & 1u) {
+          const float qu = get(q, u);
+          const float val = scaled ? fmul(qu, scale) : qu;
+          idx_out[pos] = j + u;
+          val_out[pos] = val;
+          set(ev, u, fsub(qu, val));
+          pos++;
+        }
+      eq_run += te;
+      sel_run += ts;
+    }
+    if (errp && j < L) store4_masked(errp, j, L, ev);
+  }
+  if (crank == 0 && threadIdx.x == 0) *reinterpret_cast<uint64_t*>(pay) = (uint64_t)k;
+}
+
+// ---------------------------------------------------------------- raw tiles
+template <bool SERVER>
+__device__ __forceinline__ void raw_tile(const CompressParams& p, const Tile& tl) {
+  const DevChunk c = p.chunks[tl.chunk];
+  float* out = reinterpret_cast<float*>(p.out + c.pay);
+  const uint32_t L = c.len;
+  bool bad = false;
+  for (uint32_t i = threadIdx.x; 4 * i < tl.len; i += NT) {
+    const uint32_t j = tl.start + 4 * i;
+    float4 v;
+    if (!SERVER) {
+      v = load4_masked(p.grad + c.off, j, L);   // raw units: delta = g, no EF (R3)
+      if (p.check_finite) bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
+    } else {
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      for (uint32_t r = 0; r < p.n; r++) {
+        const float4 d = load4_masked(reinterpret_cast<const float*>(p.recv + r * p.slot_bytes + c.recv), j, L);
+        a0 += (double)d.x; a1 += (double)d.y; a2 += (double)d.z; a3 += (double)d.w;
+      }
+      v = make_float4(mean_plus(a0, p.inv_n, 0.0), mean_plus(a1, p.inv_n, 0.0),
+                      mean_plus(a2, p.inv_n, 0.0), mean_plus(a3, p.inv_n, 0.0));
+    }
+    store4_masked(out, j, L, v);
+  }
+  if (bad) atomicOr(p.flag, 1u);
+}
+
+// ---------------------------------------------------------------- the kernel
+template <int KIND, bool SERVER>
+__global__ void __launch_bounds__(NT, 2) compress_kernel(const __grid_constant__ CompressParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+  const uint32_t cid = blockIdx.x / p.cs;
+  const uint32_t crank = cta_rank_in_cluster();
+  if (cid >= p.n_items) {   // cluster-uniform: raw tiles, no cluster barriers
+    const uint32_t ti = (cid - p.n_items) * p.cs + crank;
+    if (ti < p.n_raw_tiles) raw_tile<SERVER>(p, p.raw_tiles[ti]);
+    return;
+  }
+  if constexpr (KIND != K_NONE) {
+    const DevChunk c = p.chunks[p.items[cid]];
+    const uint32_t s0 = crank * SLICE;
+    uint8_t* pay = p.out + c.pay;
+    float* errp = p.use_ef ? (SERVER ? p.etl + c.etl : p.err + c.off) : nullptr;
+    const uint32_t stage = SERVER ? 1u : 0u;
+    const uint32_t rrank = SERVER ? 0u : p.rank;
+    double lv[IT];
+    if constexpr (KIND == K_SIGN || KIND == K_LDITHER || KIND == K_NDITHER) {
+      constexpr bool L2 = KIND != K_SIGN;
+      if (SERVER) produce_server_dense<KIND>(p, c, sm, s0, lv);
+      else produce_worker<L2, true>(p, c, sm, s0, lv);
+      const double total = cluster_tree_total(sm, lv, p.cs);
+      if (KIND == K_SIGN) emit_sign(c, sm, s0, crank, total, pay, errp);
+      else emit_dither<KIND>(p, c, sm, s0, crank, total, pay, errp, stage, rrank);
+    } else {
+      if (SERVER) produce_server_sparse(p, c, sm, s0);
+      else produce_worker<false, false>(p, c, sm, s0, lv);
+      __syncthreads();
+      emit_sparse<KIND>(p, c, sm, s0, crank, pay, errp, stage, rrank);
+    }
+    cluster_sync_all();   // no CTA exits while a peer may still read its shared memory
+  }
+}
+
+template <int KIND, bool SERVER>
+static cudaError_t launch_t(const CompressParams& p, cudaStream_t s) {
+  const uint32_t nclusters = p.n_items + (p.n_raw_tiles + p.cs - 1) / p.cs;
+  if (nclusters == 0) return cudaSuccess;
+  auto fn = compress_kernel<KIND, SERVER>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nclusters * p.cs);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = sizeof(Smem);
+  cfg.stream = s;
+  cudaLaunchAttribute a[1];
+  a[0].id = cudaLaunchAttributeClusterDimension;
+  a[0].val.clusterDim.x = p.cs;
+  a[0].val.clusterDim.y = 1;
+  a[0].val.clusterDim.z = 1;
+  cfg.attrs = a;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, fn, p);
+}
+
+template <int KIND, bool SERVER>
+static cudaError_t max_clusters_t(uint32_t cs, int* out) {
+  auto fn = compress_kernel<KIND, SERVER>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cs * 64);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = sizeof(Smem);
+  cudaLaunchAttribute a[1];
+  a[0].id = cudaLaunchAttributeClusterDimension;
+  a[0].val.clusterDim.x = cs;
+  a[0].val.clusterDim.y = 1;
+  a[0].val.clusterDim.z = 1;
+  cfg.attrs = a;
+  cfg.numAttrs = 1;
+  return cudaOccupancyMaxActiveClusters(out, fn, &cfg);
+}
+
+#define BPC_DISPATCH(KIND_, SERVER_, CALL)                                   \
+  switch (KIND_) {                                                           \
+    case K_NONE: return SERVER_ ? CALL(K_NONE, true) : CALL(K_NONE, false);  \
+    case K_SIGN: return SERVER_ ? CALL(K_SIGN, true) : CALL(K_SIGN, false);  \
+    case K_TOPK: return SERVER_ ? CALL(K_TOPK, true) : CALL(K_TOPK, false);  \
+    case K_RANDK: return SERVER_ ? CALL(K_RANDK, true) : CALL(K_RANDK, false); \
+    case K_LDITHER: return SERVER_ ? CALL(K_LDITHER, true) : CALL(K_LDITHER, false); \
+    case K_NDITHER: return SERVER_ ? CALL(K_NDITHER, true) : CALL(K_NDITHER, false); \
+  }                                                                          \
+  return cudaErrorInvalidValue;
+
+cudaError_t launch_compress(int kind, bool server, const CompressParams& p, cudaStream_t s) {
+#define CALL_LAUNCH(K, S) launch_t<K, S>(p, s)
+  BPC_DISPATCH(kind, server, CALL_LAUNCH)
+#undef CALL_LAUNCH
+}
+
+cudaError_t compress_max_active_clusters(int kind, bool server, uint32_t cs, int* out) {
+#define CALL_MAX(K, S) max_clusters_t<K, S>(cs, out)
+  BPC_DISPATCH(kind, server, CALL_MAX)
+#undef CALL_MAX
+}
+
+}  // namespace bpc
