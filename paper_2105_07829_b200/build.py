@@ -55,6 +55,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
               "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc]
     if verbose:
         common += ["-Xptxas", "-v"]
+    common += os.environ.get("BPC_NVCC_EXTRA", "").split()
     procs, objs = [], []
     for s in SOURCES:
         o = os.path.join(objdir, s.replace(".cu", ".o"))

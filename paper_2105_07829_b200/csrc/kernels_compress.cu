@@ -35,14 +35,10 @@ struct __align__(16) Smem {
 size_t compress_smem_bytes() { return sizeof(Smem); }
 
 // ---------------------------------------------------------------- reductions
-__device__ __forceinline__ double cluster_tree_total(Smem& sm, const double (&lv)[IT],
-                                                     uint32_t cs) {
+// The producers left in sm.red[m] the subtree sum of slice elements
+// [128 m, 128 m + 128) (m = it * NWARP + warp, see leaf_to_red).
+__device__ __forceinline__ double cluster_tree_total(Smem& sm, uint32_t cs) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#pragma unroll
-  for (int it = 0; it < IT; it++) {
-    const double a = warp_tree(lv[it]);
-    if (lane == 0) sm.red[it * NWARP + warp] = a;   // subtree of elements [128 m, 128 m + 128)
-  }
   __syncthreads();
   if (warp == 0) {
     double r = (sm.red[4 * lane] + sm.red[4 * lane + 1]) + (sm.red[4 * lane + 2] + sm.red[4 * lane + 3]);
@@ -51,10 +47,14 @@ __device__ __forceinline__ double cluster_tree_total(Smem& sm, const double (&lv
   }
   cluster_sync_all();   // publish every slice's sum to the cluster
   if (threadIdx.x == 0) {
+    // tree over the cs slices, zero-padded to 16 (padding leaves the value unchanged)
     double v[16];
-    for (uint32_t r = 0; r < cs; r++) v[r] = *dsmem(&sm.part, r);
-    for (uint32_t w = 1; w < cs; w <<= 1)
-      for (uint32_t r = 0; r + w < cs; r += 2 * w) v[r] = v[r] + v[r + w];
+#pragma unroll
+    for (uint32_t r = 0; r < 16; r++) v[r] = r < cs ? *dsmem(&sm.part, r) : 0.0;
+#pragma unroll
+    for (uint32_t w = 1; w < 16; w <<= 1)
+#pragma unroll
+      for (uint32_t r = 0; r < 16; r += 2 * w) v[r] = v[r] + v[r + w];
     sm.total = v[0];
   }
   __syncthreads();
@@ -89,34 +89,51 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* scan, 
   return r;
 }
 
+// warp subtree of this iteration's 128 elements -> sm.red (all lanes call it)
+__device__ __forceinline__ void leaf_to_red(Smem& sm, int it, double leaf) {
+  const double a = warp_tree(leaf);
+  if ((threadIdx.x & 31) == 0) sm.red[it * NWARP + (threadIdx.x >> 5)] = a;
+}
+
 // ---------------------------------------------------------------- producers
 // worker: q = g + e (use_ef) or q = g; slice -> sm.q; leaf sums -> lv
 template <bool L2, bool LEAF>
 __device__ __forceinline__ void produce_worker(const CompressParams& p, const DevChunk& c, Smem& sm,
-                                               uint32_t s0, double (&lv)[IT]) {
+                                               uint32_t s0) {
   const float* g = p.grad + c.off;
   const float* e = p.err + c.off;
   const uint32_t L = c.len;
   bool bad = false;
+  auto finish = [&](int it, float4 g4, float4 e4) {
+    if (p.check_finite) bad |= !(isfinite(g4.x) && isfinite(g4.y) && isfinite(g4.z) && isfinite(g4.w));
+    // padding lanes are 0 + 0 = +0
+    const float4 q = p.use_ef ? make_float4(fadd(g4.x, e4.x), fadd(g4.y, e4.y), fadd(g4.z, e4.z), fadd(g4.w, e4.w))
+                              : g4;
+    sm.q[it * NT + threadIdx.x] = q;
+    if (LEAF) leaf_to_red(sm, it, L2 ? leaf4_sq(q) : leaf4_abs(q));
+  };
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (s0 + SLICE <= L) {
+    // whole slice valid: batches of B iterations keep 2B 16-byte loads in flight per thread
+    constexpr int B = 4;
 #pragma unroll
-  for (int it = 0; it < IT; it++) {
-    const uint32_t i4 = it * NT + threadIdx.x;
-    const uint32_t j = s0 + 4 * i4;
-    float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (j < L) {
-      const float4 g4 = load4_masked(g, j, L);
-      if (p.check_finite)
-        bad |= !(isfinite(g4.x) && isfinite(g4.y) && isfinite(g4.z) && isfinite(g4.w));
-      if (p.use_ef) {
-        const float4 e4 = load4_masked(e, j, L);
-        q = make_float4(fadd(g4.x, e4.x), fadd(g4.y, e4.y), fadd(g4.z, e4.z), fadd(g4.w, e4.w));
-        // masked lanes: 0 + 0 = +0 (padding)
-      } else {
-        q = g4;
-      }
+    for (int it0 = 0; it0 < IT; it0 += B) {
+      float4 g4[B], e4[B];
+#pragma unroll
+      for (int b = 0; b < B; b++) g4[b] = ldg4_stream(g + s0 + 4 * ((it0 + b) * NT + threadIdx.x));
+#pragma unroll
+      for (int b = 0; b < B; b++) e4[b] = p.use_ef ? ld4(e + s0 + 4 * ((it0 + b) * NT + threadIdx.x)) : z;
+#pragma unroll
+      for (int b = 0; b < B; b++) finish(it0 + b, g4[b], e4[b]);
     }
-    sm.q[i4] = q;
-    if (LEAF) lv[it] = L2 ? leaf4_sq(q) : leaf4_abs(q);
+  } else {
+#pragma unroll 2
+    for (int it = 0; it < IT; it++) {
+      const uint32_t j = s0 + 4 * (it * NT + threadIdx.x);
+      const float4 g4 = j < L ? load4_masked(g, j, L) : z;
+      const float4 e4 = (p.use_ef && j < L) ? load4_masked(e, j, L) : z;
+      finish(it, g4, e4);
+    }
   }
   if (bad) atomicOr(p.flag, 1u);
 }
@@ -124,7 +141,7 @@ __device__ __forceinline__ void produce_worker(const CompressParams& p, const De
 // server, dense kinds: Delta_j = (float)(sum_i dec(delta_i)_j * (1/n) + e~_j)
 template <int KIND>
 __device__ __forceinline__ void produce_server_dense(const CompressParams& p, const DevChunk& c,
-                                                     Smem& sm, uint32_t s0, double (&lv)[IT]) {
+                                                     Smem& sm, uint32_t s0) {
   const uint32_t L = c.len;
   const int b = (int)p.bits;
   const float sl = (float)((1u << (b - 1)) - 1u);
@@ -172,7 +189,7 @@ __device__ __forceinline__ void produce_server_dense(const CompressParams& p, co
       d.w = j + 3 < L ? mean_plus(acc[3], p.inv_n, (double)e4.w) : 0.f;
     }
     sm.q[i4] = d;
-    lv[it] = (KIND == K_SIGN) ? leaf4_abs(d) : leaf4_sq(d);
+    leaf_to_red(sm, it, (KIND == K_SIGN) ? leaf4_abs(d) : leaf4_sq(d));
   }
 }
 
@@ -574,17 +591,16 @@ __global__ void __launch_bounds__(NT, 2) compress_kernel(const __grid_constant__
     float* errp = p.use_ef ? (SERVER ? p.etl + c.etl : p.err + c.off) : nullptr;
     const uint32_t stage = SERVER ? 1u : 0u;
     const uint32_t rrank = SERVER ? 0u : p.rank;
-    double lv[IT];
     if constexpr (KIND == K_SIGN || KIND == K_LDITHER || KIND == K_NDITHER) {
       constexpr bool L2 = KIND != K_SIGN;
-      if (SERVER) produce_server_dense<KIND>(p, c, sm, s0, lv);
-      else produce_worker<L2, true>(p, c, sm, s0, lv);
-      const double total = cluster_tree_total(sm, lv, p.cs);
+      if (SERVER) produce_server_dense<KIND>(p, c, sm, s0);
+      else produce_worker<L2, true>(p, c, sm, s0);
+      const double total = cluster_tree_total(sm, p.cs);
       if (KIND == K_SIGN) emit_sign(c, sm, s0, crank, total, pay, errp);
       else emit_dither<KIND>(p, c, sm, s0, crank, total, pay, errp, stage, rrank);
     } else {
       if (SERVER) produce_server_sparse(p, c, sm, s0);
-      else produce_worker<false, false>(p, c, sm, s0, lv);
+      else produce_worker<false, false>(p, c, sm, s0);
       __syncthreads();
       emit_sparse<KIND>(p, c, sm, s0, crank, pay, errp, stage, rrank);
     }
