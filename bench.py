@@ -39,7 +39,7 @@ DESCR = {
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="C2")
@@ -60,7 +60,7 @@ def dist_env():
 class Clocks:
     """nvidia-smi sampler running around the timed region (B200_PROFILING.md)."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+    Q = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
@@ -71,30 +71,37 @@ class Clocks:
         except OSError:
             self.p = None
 
-    def stop(self):
+    def stop(self, t0=None, t1=None):
+        """Median SM clock and throttle reasons over the samples inside [t0, t1]
+        (host wall clock of the timed region); all samples if none fall inside."""
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
         self.p.terminate()
         self.p.wait()
         self.f.seek(0)
-        sm, mx, reasons = [], [], set()
+        import datetime
+        rows = []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in self.f.read().splitlines():
             parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 6:
+            if len(parts) < 7:
                 continue
             try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
+                ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                rows.append((ts, float(parts[1]), float(parts[2]),
+                             [nm for nm, v in zip(names, parts[3:7]) if v.lower() == "active"]))
             except ValueError:
                 continue
-            for nm, v in zip(names, parts[2:6]):
-                if v.lower() == "active":
-                    reasons.add(nm)
         os.unlink(self.f.name)
-        sm.sort()
-        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        win = [r for r in rows if t0 is not None and t0 - 0.06 <= r[0] <= t1 + 0.06]
+        scope = "timed region"
+        if not win:
+            win, scope = rows, "whole run (no sample fell inside the timed region)"
+        sm = sorted(r[1] for r in win)
+        reasons = sorted({x for r in win for x in r[3]})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max((r[2] for r in win), default=None),
+                "reasons": reasons, "samples": len(win), "window": scope}
 
 
 # ---------------------------------------------------------------- byte models
@@ -154,19 +161,47 @@ def run_reference(args):
     world, rank, local = dist_env()
     if rank != 0:
         return
-    from workloads import config
-    w = config(args.config, n=args.gpus)
-    d = sum(w.tensor_numels())
-    # each "step" is one full oracle round of the workload (n = --gpus workers simulated)
-    val, steps, busy = oracle_sample(w, args.gpus, max(1.0, min(args.cpu_seconds, 20.0)))
+    import numpy as np
+
+    import oracle
+    from workloads import config, gen_grad, gen_params, layout
+    n = args.gpus
+    full = config(args.config, n=n)
+    d_full = sum(full.tensor_numels())
+    # Each step is one oracle round (n simulated workers) over a miniature of the
+    # workload: every tensor, the size threshold and the unit size divided by s,
+    # so the tensor count and the raw / compressed mix are kept; s is chosen so
+    # the whole --warmup + --steps run takes about a minute on one core.
+    rate = 15e6                                    # oracle elements / s / core (measured)
+    budget = max(4096.0, 60.0 * rate / max(1, args.steps + args.warmup) / n)
+    s = max(1, int(np.ceil(d_full / budget)))
+    w = config(args.config, n=n, scale=s, threshold_bytes=full.threshold_bytes // s,
+               chunk_elems=max(1, full.chunk_elems // s))
+    oracle.build()
+    numels = w.tensor_numels()
+    offs, D = layout(numels)
+    d = sum(numels)
+    cfg = oracle.Cfg.from_workload(w, n=n)
+    st = oracle.State(n, D, gen_params(w))
+    grads = [np.stack([gen_grad(w, i, k) for i in range(n)]) for k in (1, 2)]
+    for i in range(args.warmup):
+        oracle.round_(cfg, st, grads[i % 2], w.lr, want_payloads=False)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        oracle.round_(cfg, st, grads[i % 2], w.lr, want_payloads=False)
+    busy = time.perf_counter() - t0
+    steps = args.steps
     ms = busy / steps * 1e3
+    val = n * 4 * d * steps / busy / 1e9
     line = {
         "impl": "reference", "metric": METRIC, "value": round(val, 6), "unit": "GB/s", "n_gpus": args.gpus,
-        "steps": steps, "warmup": 0, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{args.config}: {DESCR[args.config]}", "ranks_simulated": args.gpus, "d": d},
+        "steps": steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {DESCR[args.config]}", "ranks_simulated": n, "d": d_full,
+                   "sample_scale": s, "sample_d": d},
         "cpu_baseline": {"value": round(val, 6), "unit": "GB/s", "cores": 1, "kind": "oracle",
-                         "sample": f"{steps} full oracle rounds of {args.config} with {args.gpus} simulated workers"},
+                         "sample": f"each step: one oracle round of {args.config} with every tensor, the threshold "
+                                   f"and the unit size divided by {s} ({d} elements), {n} simulated workers"},
         "e2e": {"value": round(val, 6), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -181,6 +216,7 @@ def run_ours(args):
     world, rank, local = dist_env()
     if world != args.gpus and world > 1:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
+    clocks = Clocks(local)   # started early: nvidia-smi needs ~0.5 s before its first sample
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -226,20 +262,21 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    clocks = Clocks(local)
     for i in range(args.warmup):
         step(i)
     launches0 = ctx.launch_count()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    wt0 = time.time()
     e0.record(stream)
     for i in range(args.steps):
         step(i)
     e1.record(stream)
     barrier()
+    wt1 = time.time()
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     launches = ctx.launch_count() - launches0
-    clk = clocks.stop()
+    clk = clocks.stop(wt0, wt1)
     ctx.sync()
 
     # per-kernel device timing (events recorded by libbpc around each launch, same stream)

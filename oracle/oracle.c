@@ -363,17 +363,19 @@ void orc_adam(uint64_t L, const float* gt, float* m, float* v, float* x, uint32_
               float lr, float beta1, float beta2, float eps, float wd) {
   /* Alg. 5 lines 12-16 and the x update with the
    * direction r + lambda x (PAPER.md:292-295 with the LANS normalisation
-   * left to NEXT #1): reading R15. Bias corrections in fp64 (R16). */
+   * left to NEXT #1): reading R15. The bias corrections 1/(1 - beta^t) are
+   * formed once per step in fp64 and rounded to fp32 (R16); lines 14-15 then
+   * multiply by them (R21: same real-number formula as the division). */
   float omb1 = (float)(1.0 - (double)beta1);
   float omb2 = (float)(1.0 - (double)beta2);
-  float bc1 = (float)(1.0 - pow((double)beta1, (double)t));
-  float bc2 = (float)(1.0 - pow((double)beta2, (double)t));
+  float ibc1 = (float)(1.0 / (1.0 - pow((double)beta1, (double)t)));
+  float ibc2 = (float)(1.0 / (1.0 - pow((double)beta2, (double)t)));
   for (uint64_t j = 0; j < L; j++) {
     float g = gt[j];
     m[j] = beta1 * m[j] + omb1 * g;                 /* line 12 */
     v[j] = beta2 * v[j] + omb2 * (g * g);           /* line 13 */
-    float mh = m[j] / bc1;                          /* line 14 */
-    float vh = v[j] / bc2;                          /* line 15 */
+    float mh = m[j] * ibc1;                         /* line 14: m / (1 - beta1^t) */
+    float vh = v[j] * ibc2;                         /* line 15: v / (1 - beta2^t) */
     float r = mh / (sqrtf(vh) + eps);               /* line 16 */
     x[j] = x[j] - lr * (r + wd * x[j]);             /* line 18 (Adam core) */
   }

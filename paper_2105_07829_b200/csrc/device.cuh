@@ -13,9 +13,9 @@ namespace bpc {
 namespace cg = cooperative_groups;
 
 constexpr int SLICE = 16384;           // elements per CTA of a compression unit
-constexpr int NT = 512;                // threads per compress CTA
-constexpr int NWARP = NT / 32;         // 16
-constexpr int IT = SLICE / 4 / NT;     // float4 per thread per slice = 8
+constexpr int NT = 256;                // threads per compress CTA (3 CTAs / SM)
+constexpr int NWARP = NT / 32;         // 8
+constexpr int IT = SLICE / 4 / NT;     // float4 per thread per slice = 16
 static_assert(IT * NWARP == 128, "slice reduction expects 128 warp subtrees");
 constexpr int UNT = 256;               // threads per update CTA
 constexpr int UTILE = 4096;            // elements per update tile
@@ -37,6 +37,10 @@ __device__ __forceinline__ void cluster_arrive() {
 }
 __device__ __forceinline__ void cluster_wait() {
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// arrive without memory ordering: "my reads of peers' shared memory are done"
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void cluster_sync_all() {
   cluster_arrive();

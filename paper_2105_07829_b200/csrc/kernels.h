@@ -56,7 +56,7 @@ struct UpdateParams {
   float* m;
   float* v;
   float* x;
-  float beta1, beta2, omb1, omb2, bc1, bc2, eps, lr, wd;
+  float beta1, beta2, omb1, omb2, bc1, bc2, eps, lr, wd;   // bc = 1 / (1 - beta^t), R21
   uint32_t bits;
 };
 

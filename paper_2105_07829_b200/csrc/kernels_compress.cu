@@ -58,6 +58,7 @@ __device__ __forceinline__ double cluster_tree_total(Smem& sm, uint32_t cs) {
     sm.total = v[0];
   }
   __syncthreads();
+  cluster_arrive_relaxed();   // done with peers' smem; the matching wait is at kernel exit
   return sm.total;
 }
 
@@ -139,6 +140,7 @@ __device__ __forceinline__ void produce_worker(const CompressParams& p, const De
 }
 
 // server, dense kinds: Delta_j = (float)(sum_i dec(delta_i)_j * (1/n) + e~_j)
+// Batches of B iterations: the e~ loads and each rank's code words are issued together.
 template <int KIND>
 __device__ __forceinline__ void produce_server_dense(const CompressParams& p, const DevChunk& c,
                                                      Smem& sm, uint32_t s0) {
@@ -146,50 +148,71 @@ __device__ __forceinline__ void produce_server_dense(const CompressParams& p, co
   const int b = (int)p.bits;
   const float sl = (float)((1u << (b - 1)) - 1u);
   const int cmax = (1 << (b - 1)) - 1;
+  const uint32_t cmask = (1u << b) - 1u;
   const float* et = p.etl + c.etl;
-#pragma unroll 2
-  for (int it = 0; it < IT; it++) {
-    const uint32_t i4 = it * NT + threadIdx.x;
-    const uint32_t j = s0 + 4 * i4;
-    float4 d = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (j < L) {
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      for (uint32_t r = 0; r < p.n; r++) {
-        const uint8_t* pl = p.recv + r * p.slot_bytes + c.recv;
-        const uint32_t* words = reinterpret_cast<const uint32_t*>(pl + 4);
-        const float hdr = *reinterpret_cast<const float*>(pl);
-        if (KIND == K_SIGN) {
-          const uint32_t nib = (words[j >> 5] >> (j & 31)) & 15u;
+  const bool full = s0 + SLICE <= L;
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  constexpr int B = 4;
+#pragma unroll 1
+  for (int it0 = 0; it0 < IT; it0 += B) {
+    uint32_t jj[B];
+    float4 e4[B];
+    double acc[B][4];
 #pragma unroll
-          for (int u = 0; u < 4; u++)
-            if (j + u < L) acc[u] += (double)(((nib >> u) & 1u) ? hdr : -hdr);
-        } else {
-          const uint32_t field = load_field(words, (uint64_t)b * j, 4 * b);
-          const float unit = fdiv(hdr, sl);
+    for (int q = 0; q < B; q++) {
+      jj[q] = s0 + 4 * ((it0 + q) * NT + threadIdx.x);
+      e4[q] = z;
+      if (p.use_ef) e4[q] = full ? ld4(et + jj[q]) : (jj[q] < L ? load4_masked(et, jj[q], L) : z);
 #pragma unroll
-          for (int u = 0; u < 4; u++) {
-            const uint32_t code = (field >> (b * u)) & ((1u << b) - 1u);
+      for (int u = 0; u < 4; u++) acc[q][u] = 0.0;
+    }
+#pragma unroll 1
+    for (uint32_t r = 0; r < p.n; r++) {
+      const uint8_t* pl = p.recv + r * p.slot_bytes + c.recv;
+      const uint32_t* words = reinterpret_cast<const uint32_t*>(pl + 4);
+      const float hdr = *reinterpret_cast<const float*>(pl);
+      uint32_t f[B];
+#pragma unroll
+      for (int q = 0; q < B; q++) {
+        f[q] = 0;
+        if (jj[q] < L)
+          f[q] = KIND == K_SIGN ? ((words[jj[q] >> 5] >> (jj[q] & 31)) & 15u)
+                                : load_field(words, (uint64_t)b * jj[q], 4 * b);
+      }
+      const float unit = fdiv(hdr, sl);
+#pragma unroll
+      for (int q = 0; q < B; q++) {
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          float dec;
+          if (KIND == K_SIGN) {
+            dec = ((f[q] >> u) & 1u) ? hdr : -hdr;
+          } else {
+            const uint32_t code = (f[q] >> (b * u)) & cmask;
             float mag;
             if (KIND == K_LDITHER) {
               mag = fmul((float)(code >> 1), unit);
             } else {
               const uint32_t cl = code >> 1;
-              const float level = cl == 0 ? 0.f : __uint_as_float((uint32_t)(127 - (cmax - (int)cl)) << 23);
-              mag = fmul(level, hdr);
+              mag = fmul(cl == 0 ? 0.f : __uint_as_float((uint32_t)(127 - (cmax - (int)cl)) << 23), hdr);
             }
-            if (j + u < L) acc[u] += (double)((code & 1u) ? mag : -mag);
+            dec = (code & 1u) ? mag : -mag;
           }
+          if (jj[q] + u < L) acc[q][u] += (double)dec;
         }
       }
-      float4 e4 = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (p.use_ef) e4 = load4_masked(et, j, L);
-      d.x = mean_plus(acc[0], p.inv_n, (double)e4.x);
-      d.y = j + 1 < L ? mean_plus(acc[1], p.inv_n, (double)e4.y) : 0.f;
-      d.z = j + 2 < L ? mean_plus(acc[2], p.inv_n, (double)e4.z) : 0.f;
-      d.w = j + 3 < L ? mean_plus(acc[3], p.inv_n, (double)e4.w) : 0.f;
     }
-    sm.q[i4] = d;
-    leaf_to_red(sm, it, (KIND == K_SIGN) ? leaf4_abs(d) : leaf4_sq(d));
+#pragma unroll
+    for (int q = 0; q < B; q++) {
+      const uint32_t j = jj[q];
+      float4 d = z;
+      if (j < L) d.x = mean_plus(acc[q][0], p.inv_n, (double)e4[q].x);
+      if (j + 1 < L) d.y = mean_plus(acc[q][1], p.inv_n, (double)e4[q].y);
+      if (j + 2 < L) d.z = mean_plus(acc[q][2], p.inv_n, (double)e4[q].z);
+      if (j + 3 < L) d.w = mean_plus(acc[q][3], p.inv_n, (double)e4[q].w);
+      sm.q[(it0 + q) * NT + threadIdx.x] = d;
+      leaf_to_red(sm, it0 + q, (KIND == K_SIGN) ? leaf4_abs(d) : leaf4_sq(d));
+    }
   }
 }
 
@@ -492,6 +515,7 @@ __device__ void emit_sparse(const CompressParams& p, const DevChunk& c, Smem& sm
     sm.info[3] = min(sm.cnt[1], kk > eqb ? kk - eqb : 0u);
   }
   __syncthreads();
+  cluster_arrive_relaxed();   // done with peers' smem; the matching wait is at kernel exit
   const uint32_t take_eq = sm.info[3];
   uint32_t sel_run = sm.info[2], eq_run = 0;
   uint32_t* idx_out = reinterpret_cast<uint32_t*>(pay + 8);
@@ -574,7 +598,7 @@ __device__ __forceinline__ void raw_tile(const CompressParams& p, const Tile& tl
 
 // ---------------------------------------------------------------- the kernel
 template <int KIND, bool SERVER>
-__global__ void __launch_bounds__(NT, 2) compress_kernel(const __grid_constant__ CompressParams p) {
+__global__ void __launch_bounds__(NT, 3) compress_kernel(const __grid_constant__ CompressParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   const uint32_t cid = blockIdx.x / p.cs;
@@ -604,7 +628,7 @@ __global__ void __launch_bounds__(NT, 2) compress_kernel(const __grid_constant__
       __syncthreads();
       emit_sparse<KIND>(p, c, sm, s0, crank, pay, errp, stage, rrank);
     }
-    cluster_sync_all();   // no CTA exits while a peer may still read its shared memory
+    cluster_wait();   // no CTA exits while a peer may still read its shared memory
   }
 }
 
@@ -616,6 +640,8 @@ static cudaError_t launch_t(const CompressParams& p, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nclusters * p.cs);
@@ -638,6 +664,8 @@ static cudaError_t max_clusters_t(uint32_t cs, int* out) {
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cs * 64);

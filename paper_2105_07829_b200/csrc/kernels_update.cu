@@ -11,8 +11,8 @@ enum { U_NONE = 0, U_SIGN = 2, U_TOPK = 3, U_RANDK = 4, U_LDITHER = 5, U_NDITHER
 __device__ __forceinline__ void adam1(float g, float& m, float& v, float& x, const UpdateParams& p) {
   m = fadd(fmul(p.beta1, m), fmul(p.omb1, g));                 // line 12
   v = fadd(fmul(p.beta2, v), fmul(p.omb2, fmul(g, g)));        // line 13
-  const float mh = fdiv(m, p.bc1);                             // line 14
-  const float vh = fdiv(v, p.bc2);                             // line 15
+  const float mh = fmul(m, p.bc1);                             // line 14 (bc1 = fl32(1/(1-b1^t)), R21)
+  const float vh = fmul(v, p.bc2);                             // line 15
   const float r = fdiv(mh, fadd(__fsqrt_rn(vh), p.eps));       // line 16
   x = fsub(x, fmul(p.lr, fadd(r, fmul(p.wd, x))));             // x update (Adam core)
 }
@@ -50,12 +50,18 @@ __global__ void __launch_bounds__(UNT) update_kernel(const __grid_constant__ Upd
       __syncthreads();
     }
   }
+  // full tiles (the common case): unconditional 16-byte loads, 3 * UIT in flight per thread
+  const bool full = tl.len == UTILE;
   float4 m4[UIT], v4[UIT], x4[UIT];
 #pragma unroll
   for (int it = 0; it < UIT; it++) {
     const uint32_t i4 = it * UNT + threadIdx.x;
     const uint32_t j = tl.start + 4 * i4;
-    if (4 * i4 < tl.len) {
+    if (full) {
+      m4[it] = ld4(m + j);
+      v4[it] = ld4(v + j);
+      x4[it] = ld4(x + j);
+    } else if (4 * i4 < tl.len) {
       m4[it] = load4_masked(m, j, L);
       v4[it] = load4_masked(v, j, L);
       x4[it] = load4_masked(x, j, L);
@@ -69,10 +75,10 @@ __global__ void __launch_bounds__(UNT) update_kernel(const __grid_constant__ Upd
   for (int it = 0; it < UIT; it++) {
     const uint32_t i4 = it * UNT + threadIdx.x;
     const uint32_t j = tl.start + 4 * i4;
-    if (4 * i4 >= tl.len) continue;
+    if (!full && 4 * i4 >= tl.len) continue;
     float4 g4;
     if (raw || KIND == U_NONE) {
-      g4 = load4_masked(reinterpret_cast<const float*>(pay), j, L);
+      g4 = full ? ld4(reinterpret_cast<const float*>(pay) + j) : load4_masked(reinterpret_cast<const float*>(pay), j, L);
     } else if (KIND == U_SIGN) {
       const uint32_t nib = (reinterpret_cast<const uint32_t*>(pay + 4)[j >> 5] >> (j & 31)) & 15u;
       g4 = make_float4(nib & 1u ? hdr : -hdr, nib & 2u ? hdr : -hdr, nib & 4u ? hdr : -hdr,
@@ -98,9 +104,15 @@ __global__ void __launch_bounds__(UNT) update_kernel(const __grid_constant__ Upd
     adam1(g4.y, m4[it].y, v4[it].y, x4[it].y, p);
     adam1(g4.z, m4[it].z, v4[it].z, x4[it].z, p);
     adam1(g4.w, m4[it].w, v4[it].w, x4[it].w, p);
-    store4_masked(m, j, L, m4[it]);
-    store4_masked(v, j, L, v4[it]);
-    store4_masked(x, j, L, x4[it]);
+    if (full) {
+      st4(m + j, m4[it]);
+      st4(v + j, v4[it]);
+      st4(x + j, x4[it]);
+    } else {
+      store4_masked(m, j, L, m4[it]);
+      store4_masked(v, j, L, v4[it]);
+      store4_masked(x, j, L, x4[it]);
+    }
   }
 }
 
