@@ -17,7 +17,13 @@
 namespace {
 using namespace bpc;
 
-constexpr uint64_t kSlice = 16384;   // == SLICE of the kernels
+constexpr uint64_t kSlice = 16384;   // == SLICE of the cluster kernels
+constexpr uint32_t kStreamSlice = 8192;   // == CSL of the streaming kernels
+
+// compressors whose worker step runs in the streaming kernel (unit norm, no selection)
+bool stream_worker(int kind) {
+  return kind == BPC_NONE || kind == BPC_SCALED_SIGN || kind == BPC_LINEAR_DITHER || kind == BPC_NATURAL_DITHER;
+}
 
 uint64_t round_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
@@ -194,6 +200,19 @@ struct bpc_ctx {
   Tile *d_wraw = nullptr, *d_sraw = nullptr, *d_utiles = nullptr;
   uint32_t n_witems = 0, n_sitems = 0, n_wraw = 0, n_sraw = 0, n_utiles = 0;
   unsigned int* d_flag = nullptr;
+  // streaming worker (norm-based compressors): slices, partials, unit counters
+  Slice* d_wslices = nullptr;
+  uint32_t n_wslices = 0;
+  double* d_wpartials = nullptr;
+  unsigned long long* d_wcounters = nullptr;
+  uint32_t wepoch = 0;
+  // streaming server (owned units)
+  Slice* d_sslices = nullptr;
+  uint32_t n_sslices = 0;
+  double* d_spartials = nullptr;
+  unsigned long long* d_scounters = nullptr;
+  uint32_t sepoch = 0;
+  int num_sms = 148;
   ncclComm_t comm = nullptr;
   uint32_t t = 1;
   int phase = 0;   // 0 compress, 1 push, 2 server, 3 pull, 4 step
@@ -250,7 +269,9 @@ void free_ctx(bpc_ctx* ctx) {
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   for (void* p : {(void*)ctx->e, (void*)ctx->etl, (void*)ctx->m, (void*)ctx->v, (void*)ctx->send,
                   (void*)ctx->pbuf, (void*)ctx->d_chunks, (void*)ctx->d_witems, (void*)ctx->d_sitems,
-                  (void*)ctx->d_wraw, (void*)ctx->d_sraw, (void*)ctx->d_utiles, (void*)ctx->d_flag})
+                  (void*)ctx->d_wraw, (void*)ctx->d_sraw, (void*)ctx->d_utiles, (void*)ctx->d_flag,
+                  (void*)ctx->d_wslices, (void*)ctx->d_wpartials, (void*)ctx->d_wcounters,
+                  (void*)ctx->d_sslices, (void*)ctx->d_spartials, (void*)ctx->d_scounters})
     if (p) cudaFree(p);
   if (ctx->recv && ctx->recv != ctx->send) cudaFree(ctx->recv);
   for (auto& ev : ctx->events) {
@@ -414,6 +435,35 @@ bpc_status bpc_init(const bpc_config* cfg, bpc_ctx** out) {
   ctx->n_wraw = (uint32_t)wraw.size();
   ctx->n_sraw = (uint32_t)sraw.size();
   ctx->n_utiles = (uint32_t)utiles.size();
+  // streaming-worker slices: compressed units in 2^13-element slices (multi-slice
+  // units combine partials through global memory), raw units as plain tiles
+  // (the server's: only the units this rank owns)
+  for (int side = 0; side < 2; side++) {
+    std::vector<Slice> sl;
+    uint32_t units = 0, parts = 0;
+    for (uint32_t c = 0; c < P.chunks.size(); c++) {
+      const auto& ci = P.chunks[c];
+      if (side == 1 && ci.owner != rank) continue;
+      const uint32_t L = (uint32_t)ci.len;
+      const uint32_t ns = (L + kStreamSlice - 1) / kStreamSlice;
+      for (uint32_t s0 = 0, k = 0; s0 < L; s0 += kStreamSlice, k++) {
+        Slice x = {c, s0, std::min<uint32_t>(kStreamSlice, L - s0), ci.raw ? 0u : ns, k, units, parts, 0};
+        sl.push_back(x);
+      }
+      if (!ci.raw && ns > 1) {
+        units++;
+        parts += ns;
+      }
+    }
+    Slice** dsl = side ? &ctx->d_sslices : &ctx->d_wslices;
+    double** dp = side ? &ctx->d_spartials : &ctx->d_wpartials;
+    unsigned long long** dc = side ? &ctx->d_scounters : &ctx->d_wcounters;
+    if ((s = upload(ctx, dsl, sl)) != BPC_OK) return bail(s);
+    (side ? ctx->n_sslices : ctx->n_wslices) = (uint32_t)sl.size();
+    if ((ce = alloc((void**)dp, 8ull * parts)) != cudaSuccess) return bail(cuda_fail(ctx, ce, "alloc partials"));
+    if ((ce = alloc((void**)dc, 8ull * units)) != cudaSuccess) return bail(cuda_fail(ctx, ce, "alloc counters"));
+  }
+  cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cfg->device);
   // the cluster shape must be schedulable
   int maxc = 0;
   ce = compress_max_active_clusters(cfg->comp.kind, false, P.cs, &maxc);
@@ -439,18 +489,42 @@ bpc_status bpc_init(const bpc_config* cfg, bpc_ctx** out) {
 bpc_status bpc_compress(bpc_ctx* ctx, const float* d_grad) {
   if (!ctx || !d_grad) return BPC_ERR_INVALID_ARGUMENT;
   if (ctx->phase != 0) return BPC_ERR_BAD_STATE;
-  CompressParams p = base_params(ctx);
-  p.grad = d_grad;
-  p.err = ctx->e;
-  p.out = ctx->send;
-  p.items = ctx->d_witems;
-  p.n_items = ctx->n_witems;
-  p.raw_tiles = ctx->d_wraw;
-  p.n_raw_tiles = ctx->n_wraw;
-  p.stage = 0;
   cudaEvent_t b = nullptr;
   timer_begin(ctx, BPC_TIMER_COMPRESS, &b);
-  CK(launch_compress(ctx->cfg.comp.kind, false, p, ctx->stream), "worker compress launch");
+  if (stream_worker(ctx->cfg.comp.kind)) {
+    StreamParams q = {};
+    q.grad = d_grad;
+    q.err = ctx->e;
+    q.out = ctx->send;
+    q.chunks = ctx->d_chunks;
+    q.slices = ctx->d_wslices;
+    q.n_slices = ctx->n_wslices;
+    q.partials = ctx->d_wpartials;
+    q.counters = ctx->d_wcounters;
+    q.epoch = ++ctx->wepoch;
+    q.n = (uint32_t)ctx->cfg.world_size;
+    q.inv_n = 1.0 / (double)ctx->cfg.world_size;
+    q.t = ctx->t;
+    q.rank = (uint32_t)ctx->cfg.rank;
+    q.stage = 0;
+    q.seed = ctx->cfg.seed;
+    q.bits = ctx->cfg.comp.bits;
+    q.use_ef = ctx->cfg.comp.use_ef;
+    q.check_finite = ctx->cfg.check_finite;
+    q.flag = ctx->d_flag;
+    CK(launch_worker_stream(ctx->cfg.comp.kind, q, ctx->num_sms, ctx->stream), "worker stream launch");
+  } else {
+    CompressParams p = base_params(ctx);
+    p.grad = d_grad;
+    p.err = ctx->e;
+    p.out = ctx->send;
+    p.items = ctx->d_witems;
+    p.n_items = ctx->n_witems;
+    p.raw_tiles = ctx->d_wraw;
+    p.n_raw_tiles = ctx->n_wraw;
+    p.stage = 0;
+    CK(launch_compress(ctx->cfg.comp.kind, false, p, ctx->stream), "worker compress launch");
+  }
   timer_end(ctx, BPC_TIMER_COMPRESS, b);
   ctx->launches++;
   ctx->phase = 1;
@@ -486,22 +560,50 @@ bpc_status bpc_exchange_push(bpc_ctx* ctx) {
 bpc_status bpc_server(bpc_ctx* ctx) {
   if (!ctx) return BPC_ERR_INVALID_ARGUMENT;
   if (ctx->phase != 2) return BPC_ERR_BAD_STATE;
-  CompressParams p = base_params(ctx);
-  p.recv = ctx->recv;
-  p.slot_bytes = ctx->cfg.world_size == 1 ? 0 : ctx->plan.seg_bytes[ctx->cfg.rank];
-  p.etl = ctx->etl;
-  p.out = ctx->pbuf;
-  p.items = ctx->d_sitems;
-  p.n_items = ctx->n_sitems;
-  p.raw_tiles = ctx->d_sraw;
-  p.n_raw_tiles = ctx->n_sraw;
-  p.stage = 1;
-  if (ctx->cfg.world_size == 1) {
-    // RECV aliases SEND: recv offsets equal payload offsets (one segment)
-  }
+  // n == 1: RECV aliases SEND, recv offsets equal payload offsets (one segment)
+  const uint64_t slot = ctx->cfg.world_size == 1 ? 0 : ctx->plan.seg_bytes[ctx->cfg.rank];
   cudaEvent_t b = nullptr;
   timer_begin(ctx, BPC_TIMER_SERVER, &b);
-  CK(launch_compress(ctx->cfg.comp.kind, true, p, ctx->stream), "server launch");
+  if (stream_worker(ctx->cfg.comp.kind)) {
+    StreamParams q = {};
+    q.err = ctx->etl;
+    q.out = ctx->pbuf;
+    q.recv = ctx->recv;
+    q.slot_bytes = slot;
+    q.chunks = ctx->d_chunks;
+    q.slices = ctx->d_sslices;
+    q.n_slices = ctx->n_sslices;
+    q.partials = ctx->d_spartials;
+    q.counters = ctx->d_scounters;
+    q.epoch = ++ctx->sepoch;
+    q.n = (uint32_t)ctx->cfg.world_size;
+    q.inv_n = 1.0 / (double)ctx->cfg.world_size;
+    q.t = ctx->t;
+    q.rank = 0;
+    q.stage = 1;
+    q.seed = ctx->cfg.seed;
+    q.bits = ctx->cfg.comp.bits;
+    q.use_ef = ctx->cfg.comp.use_ef;
+    q.flag = ctx->d_flag;
+    // stage the ranks' payload bytes of a slice in shared memory when a 3+-deep
+    // ring still fits (<= 48 KB of pieces per stage)
+    const uint32_t bb = ctx->cfg.comp.kind == BPC_SCALED_SIGN ? 1u : ctx->cfg.comp.bits;
+    q.piece_stride = (uint32_t)round_up((uint64_t)kStreamSlice * bb / 8 + 32, 16);
+    q.stage_payload = (uint64_t)q.piece_stride * q.n <= 49152 && ctx->cfg.world_size <= 32;
+    CK(launch_server_stream(ctx->cfg.comp.kind, q, ctx->num_sms, ctx->stream), "server stream launch");
+  } else {
+    CompressParams p = base_params(ctx);
+    p.recv = ctx->recv;
+    p.slot_bytes = slot;
+    p.etl = ctx->etl;
+    p.out = ctx->pbuf;
+    p.items = ctx->d_sitems;
+    p.n_items = ctx->n_sitems;
+    p.raw_tiles = ctx->d_sraw;
+    p.n_raw_tiles = ctx->n_sraw;
+    p.stage = 1;
+    CK(launch_compress(ctx->cfg.comp.kind, true, p, ctx->stream), "server launch");
+  }
   timer_end(ctx, BPC_TIMER_SERVER, b);
   ctx->launches++;
   ctx->phase = 3;
@@ -563,7 +665,10 @@ bpc_status bpc_step(bpc_ctx* ctx, float* d_params, float lr) {
   p.bits = c.comp.bits;
   cudaEvent_t b = nullptr;
   timer_begin(ctx, BPC_TIMER_UPDATE, &b);
-  CK(launch_update(c.comp.kind, p, ctx->stream), "update launch");
+  if (c.comp.kind == BPC_TOP_K || c.comp.kind == BPC_RANDOM_K)
+    CK(launch_update(c.comp.kind, p, ctx->stream), "update launch");   // sparse decode: per-tile scatter
+  else
+    CK(launch_update_stream(c.comp.kind, p, ctx->num_sms, ctx->stream), "update launch");
   timer_end(ctx, BPC_TIMER_UPDATE, b);
   ctx->launches++;
   ctx->t++;

@@ -6,6 +6,7 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 #include "kernels.h"
 
@@ -50,6 +51,87 @@ __device__ __forceinline__ void cluster_sync_all() {
 template <class T>
 __device__ __forceinline__ T* dsmem(T* p, uint32_t rank) {
   return cg::this_cluster().map_shared_rank(p, rank);
+}
+
+// ---------------------------------------------------------------- mbarrier + 1-D TMA
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+// bulk global -> shared copy (UBLKCP); bytes and both addresses multiples of 16
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// Watchdog: a wait longer than ~4 s of SM clock reports who was waiting on what
+// and traps (the launch fails with an error instead of hanging the device).
+#ifndef BPC_WATCHDOG_CYCLES
+#define BPC_WATCHDOG_CYCLES 8000000000ll
+#endif
+static __device__ __noinline__ void watchdog_fire(const char* what, uint32_t a, uint32_t b,
+                                                  unsigned long long c, unsigned long long d) {
+  printf("BPC WATCHDOG block %d thread %d: %s tag=%x parity=%u c=%llu d=%llu\n", (int)blockIdx.x,
+         (int)threadIdx.x, what, a, b, c, d);
+  __trap();
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, uint32_t tag = 0) {
+  if (mbar_try(bar, parity)) return;
+  const long long t0 = clock64();
+  while (!mbar_try(bar, parity)) {
+    if (clock64() - t0 > BPC_WATCHDOG_CYCLES)
+      watchdog_fire("mbarrier", tag, parity, (unsigned long long)smem_u32(bar), 0);
+  }
+}
+// gpu-scope release add / acquire load on unit counters (cross-CTA unit reductions)
+__device__ __forceinline__ void red_release_add(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+// spin with relaxed loads (no L1 invalidation per poll), then one acquire
+__device__ __forceinline__ void wait_counter(const unsigned long long* p, unsigned long long target,
+                                             uint32_t tag = 0) {
+  const long long t0 = clock64();
+  unsigned long long v;
+  while ((v = ld_relaxed(p)) < target) {
+    if (clock64() - t0 > BPC_WATCHDOG_CYCLES) watchdog_fire("counter", tag, 0, v, target);
+  }
+  (void)ld_acquire(p);
 }
 
 // ---------------------------------------------------------------- exact fp32 ops

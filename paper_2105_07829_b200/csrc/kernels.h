@@ -60,7 +60,48 @@ struct UpdateParams {
   uint32_t bits;
 };
 
+// a 2^13-element slice of a unit for the streaming worker / server kernels
+struct Slice {
+  uint32_t chunk;       // index into the chunk table
+  uint32_t start;       // first element, relative to the chunk
+  uint32_t len;
+  uint32_t nslices;     // slices in this unit (0 = raw tile: no reduction)
+  uint32_t sidx;        // index of this slice inside its unit
+  uint32_t unit;        // unit counter index (multi-slice units)
+  uint32_t unit_first;  // first partial of the unit
+  uint32_t pad;
+};
+
+struct StreamParams {
+  const float* grad;      // worker: g
+  float* err;             // worker: e; server: e~ (compact)
+  uint8_t* out;           // worker: SEND; server: P
+  const uint8_t* recv;    // server: RECV
+  uint64_t slot_bytes;
+  const DevChunk* chunks;
+  const Slice* slices;
+  uint32_t n_slices;
+  double* partials;       // per-slice tree partials of multi-slice units
+  unsigned long long* counters;   // per-unit published-slice counters (monotonic)
+  uint32_t epoch;         // launch number: a unit is complete at epoch * nslices
+  uint32_t n;
+  double inv_n;
+  uint32_t t, rank, stage;
+  uint64_t seed;
+  uint32_t bits;
+  int32_t use_ef, check_finite;
+  unsigned int* flag;
+  uint32_t stage_payload;   // server: stage the n ranks' payload pieces in smem
+  uint32_t piece_stride;    // server: bytes per staged piece
+  uint32_t nstages, stage_a, stage_b;   // ring geometry (set by the launcher)
+};
+
 // host launchers (return the launch error)
+cudaError_t launch_worker_stream(int kind, const StreamParams& p, int grid, cudaStream_t s);
+cudaError_t launch_server_stream(int kind, const StreamParams& p, int grid, cudaStream_t s);
+cudaError_t launch_update_stream(int kind, const UpdateParams& p, int grid, cudaStream_t s);
+size_t cstream_smem();
+size_t update_stream_smem();
 cudaError_t launch_compress(int kind, bool server, const CompressParams& p, cudaStream_t s);
 cudaError_t launch_update(int kind, const UpdateParams& p, cudaStream_t s);
 size_t compress_smem_bytes();

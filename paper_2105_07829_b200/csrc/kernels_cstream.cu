@@ -1,0 +1,477 @@
+// kernels_cstream.cu — persistent, warp-specialised worker and server kernels
+// for the norm-based compressors (scaled sign, linear / natural dithering) and
+// raw units (sm_100a).
+//
+//   worker: q = g + e (Alg. 4 l.5),
+//           delta = C(q) (l.6), e = q - dec(delta) (l.7)
+//   server  (A5-A7): Delta = (1/n) sum_i dec(delta_i) + e~ (l.10),
+//           p = C(Delta) (l.11), e~ = Delta - dec(p) (l.13)
+//
+// One CTA per SM walks 2^13-element slices of its units through a ring of
+// NS (<= 8) shared-memory stages sized at launch.  Warps:
+//   PRODUCER  reads the slice descriptors and issues the 1-D bulk copies
+//             (cp.async.bulk, mbarrier complete_tx): worker g, e; server e~ and
+//             the n ranks' payload bytes of the slice;
+//   4 REDUCERS (slice i -> reducer i % 4) complete each unit's fp64
+//             pairwise-tree total (R6):
+//             single-slice units take the local partial; for multi-slice units
+//             the reducer publishes the slice's partial, bumps the unit counter
+//             (release) and waits (relaxed spin + one acquire) for the others;
+//   16 CONSUMERS  produce slice i (q or Delta in place, slice partial) and
+//             then emit slice i-1 (codes + error) once its total is ready.
+// All CTAs are co-resident (cooperative launch) and every CTA publishes slice i
+// before it waits on slice i-1's unit, so the waits cannot deadlock.
+#include "device.cuh"
+
+namespace bpc {
+
+enum { C_NONE = 0, C_SIGN = 2, C_LDITHER = 5, C_NDITHER = 6 };
+
+constexpr int CCW = 16;                  // consumer warps
+constexpr int CCNT = 32 * CCW;           // consumer threads
+constexpr int CPROD = CCW;               // producer warp index
+constexpr int CRED = CCW + 1;            // first reducer warp index
+constexpr int CRW = 4;                   // reducer warps (slice i -> reducer i % CRW)
+constexpr int CSNT = CCNT + 32 + 32 * CRW;   // + producer + reducers
+constexpr int CDEF = 1;                  // emit of slice i - CDEF follows the produce of slice i
+constexpr int CMAXST = 8;                // max stages
+constexpr int CSL = 8192;                // elements per slice
+constexpr int CK = CSL / 4 / CCNT;       // float4 per consumer thread per slice
+constexpr int CNRED = CK * CCW;          // 128-element warp subtrees per slice (32 or 64)
+constexpr int CUNITSL = (1 << 18) / CSL; // max slices per unit (32 or 64)
+constexpr int CMAXN = 32;                // ranks whose headers are staged (server)
+static_assert(CNRED == 32 || CNRED == 64, "slice tree expects 32 or 64 warp subtrees");
+
+struct CDesc {
+  uint64_t off;        // worker: flat element offset of the chunk
+  uint64_t pay;        // payload byte offset (SEND / P)
+  uint64_t recv;       // server: offset inside each RECV slot
+  uint64_t etl;        // server: e~ element offset
+  uint32_t start, len, L, id;
+  uint32_t nslices, sidx, unit, unit_first;
+  uint32_t pofs;       // server: byte offset of the slice's first field inside a staged piece
+  uint32_t staged;     // server: payload pieces staged in smem
+};
+
+struct __align__(128) CHead {
+  uint64_t full[CMAXST], empty[CMAXST], tready[CMAXST];
+  uint32_t produced;   // slices produced so far (monotonic; reducers wait on it out of order)
+  CDesc desc[CMAXST];
+  double red[2][CNRED];
+  double part[CMAXST];
+  double total[CMAXST];
+  float hdr[CMAXST][CMAXN];
+};
+
+__device__ __forceinline__ void mbar_arrive1(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void cons_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(CCNT) : "memory");
+}
+
+__device__ __forceinline__ uint32_t lin_code_c(float q, float N, float sl, float inv, uint32_t w) {
+  const uint32_t sign = !(q < 0.f);
+  uint32_t level = 0;
+  if (N != 0.f) {
+    const float r = fminf(fmul(fabsf(q), inv), sl);
+    const float l = floorf(r);
+    const float f = fsub(r, l);
+    const float u = (float)(w >> 8) * 0x1p-24f;
+    level = (uint32_t)l + (u < f ? 1u : 0u);
+  }
+  return sign | (level << 1);
+}
+__device__ __forceinline__ uint32_t nat_code_c(float q, float N, int cmax, float lmin, uint32_t w) {
+  const uint32_t sign = !(q < 0.f);
+  uint32_t code = 0;
+  if (N != 0.f) {
+    const float r = fminf(fdiv(fabsf(q), N), 1.0f);
+    const float u = (float)(w >> 8) * 0x1p-24f;
+    if (r >= lmin) {
+      const int eb = (int)(__float_as_uint(r) >> 23);
+      const float lo = __uint_as_float((uint32_t)eb << 23);
+      const float pup = fsub(fdiv(r, lo), 1.0f);
+      const int e_lev = (u < pup) ? eb - 127 + 1 : eb - 127;
+      code = (uint32_t)(cmax + e_lev);
+    } else {
+      code = (u < fdiv(r, lmin)) ? 1u : 0u;
+    }
+  }
+  return sign | (code << 1);
+}
+// |dec| of a dithering code
+template <int KIND>
+__device__ __forceinline__ float dither_mag(uint32_t code, float hdr, float unit, int cmax) {
+  if (KIND == C_LDITHER) return fmul((float)(code >> 1), unit);
+  const uint32_t cl = code >> 1;
+  return fmul(cl == 0 ? 0.f : __uint_as_float((uint32_t)(127 - (cmax - (int)cl)) << 23), hdr);
+}
+
+template <int KIND, bool SERVER>
+__global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant__ StreamParams p) {
+  extern __shared__ __align__(128) unsigned char sraw[];
+  CHead& hd = *reinterpret_cast<CHead*>(sraw);
+  unsigned char* ring = sraw + sizeof(CHead);
+  const uint32_t NS = p.nstages;
+  const uint32_t SA = p.stage_a, SB = p.stage_b;   // bytes of the two regions of a stage
+  auto regA = [&](uint32_t s) { return reinterpret_cast<float4*>(ring + s * (SA + SB)); };
+  auto regB = [&](uint32_t s) { return reinterpret_cast<float4*>(ring + s * (SA + SB) + SA); };
+  const uint32_t G = gridDim.x;
+  const uint32_t mine = p.n_slices > blockIdx.x ? (p.n_slices - blockIdx.x + G - 1) / G : 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = KIND == C_SIGN ? 1 : (int)p.bits;       // bits per element in the payload stream
+  if (threadIdx.x == 0) {
+    for (uint32_t s = 0; s < NS; s++) {
+      mbar_init(&hd.full[s], 1);
+      mbar_init(&hd.empty[s], CCW);
+      mbar_init(&hd.tready[s], 1);
+    }
+    hd.produced = 0;
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  // ===================================================== producer
+  if (warp == CPROD) {
+    if (lane == 0) {
+      for (uint32_t i = 0; i < mine; i++) {
+        const uint32_t s = i % NS;
+        if (i >= NS) mbar_wait(&hd.empty[s], ((i / NS) - 1) & 1, 0x1000000u | i);
+        const Slice sl = p.slices[blockIdx.x + i * G];
+        const DevChunk c = p.chunks[sl.chunk];
+        CDesc d;
+        d.off = c.off;
+        d.pay = c.pay;
+        d.recv = c.recv;
+        d.etl = c.etl;
+        d.start = sl.start;
+        d.len = sl.len;
+        d.L = c.len;
+        d.id = c.id;
+        d.nslices = sl.nslices;
+        d.sidx = sl.sidx;
+        d.unit = sl.unit;
+        d.unit_first = sl.unit_first;
+        d.pofs = 0;
+        d.staged = 0;
+        const uint32_t nvb = (sl.len & ~3u) * 4u;
+        const bool comp = sl.nslices > 0;
+        uint32_t tx = 0;
+        uint64_t a0 = 0, a1 = 0;
+        if (!SERVER) {
+          tx = (p.use_ef && comp) ? 2 * nvb : nvb;
+        } else if (comp) {
+          const uint64_t s0 = 4 + (uint64_t)sl.start * b / 8;
+          const uint64_t e0 = 4 + ((uint64_t)(sl.start + sl.len) * b + 7) / 8;
+          a0 = s0 & ~15ull;
+          a1 = (e0 + 15) & ~15ull;
+          d.pofs = (uint32_t)(s0 - a0);
+          d.staged = p.stage_payload;
+          if (p.use_ef) tx += nvb;
+          if (d.staged) tx += p.n * (uint32_t)(a1 - a0);
+          for (uint32_t r = 0; r < p.n && r < (uint32_t)CMAXN; r++)
+            hd.hdr[s][r] = *reinterpret_cast<const float*>(p.recv + r * p.slot_bytes + c.recv);
+        }
+        hd.desc[s] = d;
+        mbar_arrive_expect_tx(&hd.full[s], tx);
+        if (!SERVER) {
+          if (nvb) {
+            tma_load_1d(regA(s), p.grad + c.off + sl.start, nvb, &hd.full[s]);
+            if (p.use_ef && comp) tma_load_1d(regB(s), p.err + c.off + sl.start, nvb, &hd.full[s]);
+          }
+        } else if (comp) {
+          if (p.use_ef && nvb) tma_load_1d(regB(s), p.err + c.etl + sl.start, nvb, &hd.full[s]);
+          if (d.staged)
+            for (uint32_t r = 0; r < p.n; r++)
+              tma_load_1d(reinterpret_cast<uint8_t*>(regA(s)) + r * p.piece_stride,
+                          p.recv + r * p.slot_bytes + c.recv + a0, (uint32_t)(a1 - a0), &hd.full[s]);
+        }
+      }
+    }
+    return;
+  }
+
+  // ===================================================== reducers
+  if (warp >= CRED) {
+    for (uint32_t i = warp - CRED; i < mine; i += CRW) {
+      const uint32_t s = i % NS;
+      {   // wait until the consumers have produced slice i (monotonic counter: no parity aliasing)
+        const long long t0 = clock64();
+        while (*reinterpret_cast<volatile uint32_t*>(&hd.produced) < i + 1)
+          if (clock64() - t0 > BPC_WATCHDOG_CYCLES) watchdog_fire("produced", 0x2000000u | i, 0, 0, 0);
+        __threadfence_block();
+      }
+      const uint32_t ns = hd.desc[s].nslices;
+      if (ns > 1) {
+        if (lane == 0) {
+          // publish this slice's partial, then wait for the unit's other slices
+          const CDesc& d = hd.desc[s];
+          p.partials[d.unit_first + d.sidx] = hd.part[s];
+          red_release_add(p.counters + d.unit, 1ull);
+          wait_counter(p.counters + d.unit, (unsigned long long)p.epoch * ns, 0x3000000u | i);
+        }
+        __syncwarp();
+        // unit total: pairwise tree over its slices, zero-padded to CUNITSL (R6)
+        const double* P = p.partials + hd.desc[s].unit_first;
+        double v;
+        if (CUNITSL == 64) {   // lane l holds the 2-slice subtree (2l, 2l+1)
+          const uint32_t l0 = 2 * lane, l1 = 2 * lane + 1;
+          v = (l0 < ns ? __ldcg(P + l0) : 0.0) + (l1 < ns ? __ldcg(P + l1) : 0.0);
+        } else {
+          v = (uint32_t)lane < ns ? __ldcg(P + lane) : 0.0;
+        }
+        v = warp_tree(v);
+        if (lane == 0) hd.total[s] = v;
+      } else if (ns == 1 && lane == 0) {
+        hd.total[s] = hd.part[s];
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive1(&hd.tready[s]);
+    }
+    return;
+  }
+
+  // ===================================================== consumers
+  const int nb = 4 * b;
+  const float slv = (float)((1u << (p.bits - 1)) - 1u);
+  const int cmax = (1 << (p.bits - 1)) - 1;
+  const float lmin = __uint_as_float((uint32_t)(127 - (cmax - 1)) << 23);
+  const uint32_t cmask = (1u << b) - 1u;
+  const uint32_t stage_id = SERVER ? 1u : 0u;
+  const uint32_t rng_rank = SERVER ? 0u : p.rank;
+  bool bad = false;
+
+  for (uint32_t i = 0; i < mine + CDEF; i++) {
+    // ---------------- produce slice i
+    if (i < mine) {
+      const uint32_t s = i % NS;
+      mbar_wait(&hd.full[s], (i / NS) & 1, 0x4000000u | i);
+      const CDesc d = hd.desc[s];
+      const uint32_t nvec = d.len >> 2;
+      const bool comp = d.nslices > 0;
+      float4* val = SERVER ? regB(s) : regA(s);
+#pragma unroll
+      for (int k = 0; k < CK; k++) {
+        const uint32_t f = threadIdx.x + k * CCNT;
+        const uint32_t j = d.start + 4 * f;
+        float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (!SERVER) {
+          const bool ef = p.use_ef && comp;
+          float4 g4 = q, e4 = q;
+          if (f < nvec) {
+            g4 = regA(s)[f];
+            if (ef) e4 = regB(s)[f];
+          } else if (4 * f < d.len) {   // ragged tail (not in the 16-byte bulk copy)
+            g4 = load4_masked(p.grad + d.off, j, d.L);
+            if (ef) e4 = load4_masked(p.err + d.off, j, d.L);
+          }
+          if (p.check_finite) bad |= !(isfinite(g4.x) && isfinite(g4.y) && isfinite(g4.z) && isfinite(g4.w));
+          q = ef ? make_float4(fadd(g4.x, e4.x), fadd(g4.y, e4.y), fadd(g4.z, e4.z), fadd(g4.w, e4.w)) : g4;
+        } else if (4 * f < d.len) {
+          double acc[4] = {0.0, 0.0, 0.0, 0.0};
+          if (!comp) {   // raw unit: mean of the ranks' fp32 values
+            for (uint32_t r = 0; r < p.n; r++) {
+              const float4 x4 = load4_masked(reinterpret_cast<const float*>(p.recv + r * p.slot_bytes + d.recv), j, d.L);
+              acc[0] += (double)x4.x;
+              acc[1] += (double)x4.y;
+              acc[2] += (double)x4.z;
+              acc[3] += (double)x4.w;
+            }
+          } else {
+            for (uint32_t r = 0; r < p.n; r++) {
+              const float h = r < (uint32_t)CMAXN ? hd.hdr[s][r]
+                                                  : *reinterpret_cast<const float*>(p.recv + r * p.slot_bytes + d.recv);
+              const uint32_t* words =
+                  d.staged ? reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(regA(s)) +
+                                                               r * p.piece_stride + d.pofs)
+                           : reinterpret_cast<const uint32_t*>(p.recv + r * p.slot_bytes + d.recv + 4 +
+                                                               (uint64_t)d.start * b / 8);
+              const uint32_t field = KIND == C_SIGN ? ((words[f >> 3] >> ((f & 7) * 4)) & 15u)
+                                                    : load_field(words, (uint64_t)b * 4 * f, nb);
+              const float unit = fdiv(h, slv);
+#pragma unroll
+              for (int u = 0; u < 4; u++) {
+                float dec;
+                if (KIND == C_SIGN) {
+                  dec = ((field >> u) & 1u) ? h : -h;
+                } else {
+                  const uint32_t code = (field >> (b * u)) & cmask;
+                  const float mag = dither_mag<KIND>(code, h, unit, cmax);
+                  dec = (code & 1u) ? mag : -mag;
+                }
+                if (j + u < d.L) acc[u] += (double)dec;
+              }
+            }
+          }
+          float4 e4 = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (comp && p.use_ef) e4 = f < nvec ? regB(s)[f] : load4_masked(p.err + d.etl, j, d.L);
+          if (j < d.L) q.x = mean_plus(acc[0], p.inv_n, (double)e4.x);
+          if (j + 1 < d.L) q.y = mean_plus(acc[1], p.inv_n, (double)e4.y);
+          if (j + 2 < d.L) q.z = mean_plus(acc[2], p.inv_n, (double)e4.z);
+          if (j + 3 < d.L) q.w = mean_plus(acc[3], p.inv_n, (double)e4.w);
+        }
+        val[f] = q;
+        if (comp) {
+          const double a = warp_tree(KIND == C_SIGN ? leaf4_abs(q) : leaf4_sq(q));
+          if (lane == 0) hd.red[i & 1][k * CCW + warp] = a;   // subtree of slice elements [128 m, 128 m + 128)
+        }
+      }
+      if (comp) cons_sync();
+      if (warp == 0) {
+        if (comp) {
+          const double r = warp_tree(CNRED == 64 ? hd.red[i & 1][2 * lane] + hd.red[i & 1][2 * lane + 1]
+                                                 : hd.red[i & 1][lane]);
+          if (lane == 0) hd.part[s] = r;   // the slice's reducer publishes it
+        }
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence_block();
+          *reinterpret_cast<volatile uint32_t*>(&hd.produced) = i + 1;
+        }
+      }
+    }
+    // ---------------- emit slice i - CDEF
+    if (i >= (uint32_t)CDEF) {
+      const uint32_t ie = i - CDEF;
+      const uint32_t s = ie % NS;
+      const CDesc d = hd.desc[s];
+      const uint32_t L = d.L;
+      uint8_t* pay = p.out + d.pay;
+      const float4* val = SERVER ? regB(s) : regA(s);
+      // every slice (raw included) waits for its reducer before the stage is
+      // recycled: keeps each mbarrier at most one phase ahead of its waiters
+      mbar_wait(&hd.tready[s], (ie / NS) & 1, 0x5000000u | ie);
+      if (d.nslices == 0) {   // raw unit: fp32 payload (worker: g, no EF; server: the mean)
+        float* out = reinterpret_cast<float*>(pay);
+#pragma unroll
+        for (int k = 0; k < CK; k++) {
+          const uint32_t f = threadIdx.x + k * CCNT;
+          if (4 * f < d.len) store4_masked(out, d.start + 4 * f, L, val[f]);
+        }
+      } else {
+        const double total = hd.total[s];
+        float* errp = p.use_ef ? (SERVER ? p.err + d.etl : p.err + d.off) : nullptr;
+        if (KIND == C_SIGN) {
+          const float sc = __double2float_rn(total / (double)L);
+          uint32_t* words = reinterpret_cast<uint32_t*>(pay + 4);
+#pragma unroll
+          for (int k = 0; k < CK; k++) {
+            const uint32_t f = threadIdx.x + k * CCNT;
+            const uint32_t j = d.start + 4 * f;
+            const float4 q = val[f];
+            uint32_t nib = 0;
+            float4 ev;
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+              const float qu = get(q, u);
+              const bool bit = !(qu < 0.f);
+              if (bit && j + u < L) nib |= 1u << u;
+              set(ev, u, bit ? fsub(qu, sc) : fadd(qu, sc));
+            }
+            if (errp && j < L) store4_masked(errp, j, L, ev);
+            uint32_t w = nib << (4 * (lane & 7));
+            w |= __shfl_xor_sync(0xffffffffu, w, 1);
+            w |= __shfl_xor_sync(0xffffffffu, w, 2);
+            w |= __shfl_xor_sync(0xffffffffu, w, 4);
+            if ((lane & 7) == 0 && j < L) words[j >> 5] = w;
+          }
+          if (d.sidx == 0 && threadIdx.x == 0) *reinterpret_cast<float*>(pay) = sc;
+        } else if (KIND == C_LDITHER || KIND == C_NDITHER) {
+          const float N = __double2float_rn(sqrt(total));
+          const float inv = N != 0.f ? fdiv(slv, N) : 0.f;
+          const float unit = fdiv(N, slv);
+          uint32_t* words = reinterpret_cast<uint32_t*>(pay + 4);
+          const uint64_t nwords = ((uint64_t)b * L + 31) / 32;
+#pragma unroll
+          for (int k = 0; k < CK; k++) {
+            const uint32_t f = threadIdx.x + k * CCNT;
+            const uint32_t j = d.start + 4 * f;
+            const float4 q = val[f];
+            uint32_t field = 0;
+            if (j < L) {
+              const uint4 w4 = rng4(p.seed, j >> 2, d.id, p.t, stage_id, rng_rank);
+              float4 ev;
+#pragma unroll
+              for (int u = 0; u < 4; u++) {
+                const uint32_t w = u == 0 ? w4.x : (u == 1 ? w4.y : (u == 2 ? w4.z : w4.w));
+                const float qu = get(q, u);
+                const uint32_t code = KIND == C_LDITHER ? lin_code_c(qu, N, slv, inv, w)
+                                                        : nat_code_c(qu, N, cmax, lmin, w);
+                if (j + u < L) field |= (code & cmask) << (b * u);
+                const float mag = dither_mag<KIND>(code, N, unit, cmax);
+                set(ev, u, fsub(qu, (code & 1u) ? mag : -mag));
+              }
+              if (errp) store4_masked(errp, j, L, ev);
+            }
+            const uint32_t wd = warp_pack(field, nb);
+            const uint64_t wbase = (uint64_t)(d.start + 4 * (k * CCNT + 32 * warp)) / 32 * b;
+            if (lane < nb && wbase + lane < nwords) words[wbase + lane] = wd;
+          }
+          if (d.sidx == 0 && threadIdx.x == 0) *reinterpret_cast<float*>(pay) = N;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive1(&hd.empty[s]);   // this warp is done with stage ie % NS
+    }
+  }
+  if (bad) atomicOr(p.flag, 1u);
+}
+
+// stage geometry for a launch: regions A / B per stage, stage count, smem bytes
+static void cstream_geometry(bool server, const StreamParams& p, uint32_t* sa, uint32_t* sb, uint32_t* ns,
+                             size_t* smem) {
+  const uint32_t slice_bytes = CSL * 4;
+  if (!server) {
+    *sa = slice_bytes;                       // g -> q
+    *sb = p.use_ef ? slice_bytes : 0;        // e
+  } else {
+    *sa = p.stage_payload ? (uint32_t)((p.n * p.piece_stride + 127) / 128 * 128) : 0;   // payload pieces
+    *sb = slice_bytes;                       // e~ -> Delta
+  }
+  const size_t budget = 227 * 1024 - sizeof(CHead) - 1024;
+  uint32_t n = (uint32_t)(budget / (*sa + *sb));
+  *ns = n > (uint32_t)CMAXST ? (uint32_t)CMAXST : n;
+  *smem = sizeof(CHead) + (size_t)(*ns) * (*sa + *sb);
+}
+
+template <bool SERVER>
+static cudaError_t launch_cstream_t(int kind, StreamParams p, int grid, cudaStream_t st) {
+  if (p.n_slices == 0) return cudaSuccess;
+  size_t smem;
+  cstream_geometry(SERVER, p, &p.stage_a, &p.stage_b, &p.nstages, &smem);
+  if (p.nstages < CDEF + 2) return cudaErrorInvalidConfiguration;   // held stages + one in flight
+  auto go = [&](auto fn) -> cudaError_t {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)std::min<uint32_t>((uint32_t)grid, p.n_slices));
+    cfg.blockDim = dim3(CSNT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute a[1];
+    a[0].id = cudaLaunchAttributeCooperative;   // all CTAs co-resident: the unit waits need it
+    a[0].val.cooperative = 1;
+    cfg.attrs = a;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, fn, p);
+  };
+  switch (kind) {
+    case C_NONE: return go(cstream_kernel<C_NONE, SERVER>);
+    case C_SIGN: return go(cstream_kernel<C_SIGN, SERVER>);
+    case C_LDITHER: return go(cstream_kernel<C_LDITHER, SERVER>);
+    case C_NDITHER: return go(cstream_kernel<C_NDITHER, SERVER>);
+  }
+  return cudaErrorInvalidValue;
+}
+
+size_t cstream_smem() { return sizeof(CHead); }
+
+cudaError_t launch_worker_stream(int kind, const StreamParams& p, int grid, cudaStream_t st) {
+  return launch_cstream_t<false>(kind, p, grid, st);
+}
+cudaError_t launch_server_stream(int kind, const StreamParams& p, int grid, cudaStream_t st) {
+  return launch_cstream_t<true>(kind, p, grid, st);
+}
+
+}  // namespace bpc

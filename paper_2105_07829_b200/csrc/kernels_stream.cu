@@ -1,0 +1,222 @@
+// kernels_stream.cu — persistent, warp-specialised, TMA-pipelined streaming
+// kernels (sm_100a).  One CTA per SM; the last warp is the PRODUCER: it reads
+// the work descriptors, stages them in shared memory and issues 1-D bulk
+// copies (cp.async.bulk -> UBLKCP, mbarrier complete_tx) up to ST stages ahead;
+// 16 CONSUMER warps wait on full[s], compute, and release empty[s].  Descriptor
+// latency never reaches the consumers and the copy engine keeps ~130 KB of
+// reads in flight per SM.
+//
+// update_stream: g~ = dec(p) from the staged payload bytes,
+// then Alg. 5 lines 12-16 + x update (R15/R21)
+// on the staged m, v, x tile; results stored straight to HBM.
+//
+// worker_stream (A1-A3 for the norm-based compressors: scaled sign, linear /
+// natural dithering, raw units): per 2^13-element slice q = g + e in shared
+// memory (Alg. 4 l.5) and the slice's pairwise-tree partial
+// (R6); a unit spanning several slices combines its partials through global
+// memory (release add on a per-unit counter, acquire spin).  The emit of slice
+// i-1 (sign bits / codes + e = q - dec, l.6-7) is deferred behind the produce
+// of slice i so the wait overlaps useful work.  All CTAs are co-resident
+// (cooperative launch) and every CTA publishes a slice before it waits on an
+// earlier one, so the waits cannot deadlock.
+#include "device.cuh"
+
+namespace bpc {
+
+enum { S_NONE = 0, S_SIGN = 2, S_TOPK = 3, S_RANDK = 4, S_LDITHER = 5, S_NDITHER = 6 };
+
+constexpr int CW = 16;                 // consumer warps
+constexpr int CNT = 32 * CW;           // consumer threads
+constexpr int SNT = CNT + 32;          // + 1 producer warp
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void consumers_sync() {   // named barrier over the consumer warps
+  asm volatile("bar.sync 1, %0;" ::"n"(CNT) : "memory");
+}
+
+// ============================================================== update_stream
+constexpr int UST = 3;                      // stages
+constexpr int UK = UTILE / 4 / CNT;         // float4 per consumer thread per tile = 2
+
+struct UDesc {
+  uint64_t off;    // flat element offset of the chunk
+  uint64_t pay;    // payload byte offset of the chunk
+  uint32_t start;  // tile start (chunk-relative)
+  uint32_t len;
+  uint32_t L;
+  uint32_t raw;
+  uint32_t pofs;   // byte offset of the tile's first payload field inside the staged piece
+  float hdr;       // scale (sign) / norm (dither)
+};
+
+struct __align__(128) USmem {
+  float4 m[UST][UTILE / 4];
+  float4 v[UST][UTILE / 4];
+  float4 x[UST][UTILE / 4];
+  float4 pay[UST][UTILE / 4];     // payload piece: raw fp32 tile, or sign / code bits
+  UDesc desc[UST];
+  uint64_t full[UST], empty[UST];
+};
+
+__device__ __forceinline__ void adam1s(float g, float& m, float& v, float& x, const UpdateParams& p) {
+  m = fadd(fmul(p.beta1, m), fmul(p.omb1, g));                 // line 12
+  v = fadd(fmul(p.beta2, v), fmul(p.omb2, fmul(g, g)));        // line 13
+  const float mh = fmul(m, p.bc1);                             // line 14 (R21)
+  const float vh = fmul(v, p.bc2);                             // line 15
+  const float r = fdiv(mh, fadd(__fsqrt_rn(vh), p.eps));       // line 16
+  x = fsub(x, fmul(p.lr, fadd(r, fmul(p.wd, x))));             // x update (Adam core)
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(SNT, 1) update_stream(const __grid_constant__ UpdateParams p) {
+  extern __shared__ __align__(128) unsigned char sraw[];
+  USmem& sm = *reinterpret_cast<USmem*>(sraw);
+  const uint32_t G = gridDim.x;
+  const uint32_t mine = p.n_tiles > blockIdx.x ? (p.n_tiles - blockIdx.x + G - 1) / G : 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = KIND == S_SIGN ? 1 : (int)p.bits;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < UST; s++) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], CW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == CW) {   // ---------------- producer
+    if (lane == 0) {
+      for (uint32_t i = 0; i < mine; i++) {
+        const int s = i % UST;
+        if (i >= (uint32_t)UST) mbar_wait(&sm.empty[s], ((i / UST) - 1) & 1);
+        const Tile tl = p.tiles[blockIdx.x + i * G];
+        const DevChunk c = p.chunks[tl.chunk];
+        const uint8_t* pay = p.pbuf + c.pay;
+        const uint32_t nvb = (tl.len & ~3u) * 4u;
+        UDesc d;
+        d.off = c.off;
+        d.pay = c.pay;
+        d.start = tl.start;
+        d.len = tl.len;
+        d.L = c.len;
+        d.raw = c.raw;
+        const uint8_t* psrc;
+        uint32_t pbytes;
+        if (c.raw || KIND == S_NONE) {
+          psrc = pay + 4ull * tl.start;
+          pbytes = nvb;
+          d.pofs = 0;
+          d.hdr = 0.f;
+        } else {
+          const uint64_t s0 = 4 + (uint64_t)tl.start * b / 8;                  // first field byte
+          const uint64_t e0 = 4 + ((uint64_t)(tl.start + tl.len) * b + 7) / 8;  // end byte
+          const uint64_t a0 = s0 & ~15ull, a1 = (e0 + 15) & ~15ull;           // inside the 16-B slot
+          psrc = pay + a0;
+          pbytes = (uint32_t)(a1 - a0);
+          d.pofs = (uint32_t)(s0 - a0);
+          d.hdr = *reinterpret_cast<const float*>(pay);
+        }
+        sm.desc[s] = d;
+        mbar_arrive_expect_tx(&sm.full[s], 3 * nvb + pbytes);
+        if (nvb) {
+          tma_load_1d(sm.m[s], p.m + c.off + tl.start, nvb, &sm.full[s]);
+          tma_load_1d(sm.v[s], p.v + c.off + tl.start, nvb, &sm.full[s]);
+          tma_load_1d(sm.x[s], p.x + c.off + tl.start, nvb, &sm.full[s]);
+        }
+        if (pbytes) tma_load_1d(sm.pay[s], psrc, pbytes, &sm.full[s]);
+      }
+    }
+    return;
+  }
+  // ---------------- consumers
+  const float sl = (float)((1u << (p.bits - 1)) - 1u);
+  const int cmax = (1 << (p.bits - 1)) - 1;
+  for (uint32_t i = 0; i < mine; i++) {
+    const int s = i % UST;
+    mbar_wait(&sm.full[s], (i / UST) & 1);
+    const UDesc d = sm.desc[s];
+    const uint32_t nvec = d.len >> 2;
+    float* m = p.m + d.off;
+    float* v = p.v + d.off;
+    float* x = p.x + d.off;
+    const uint32_t* words = reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(sm.pay[s]) + d.pofs);
+    const float unit = fdiv(d.hdr, sl);
+#pragma unroll
+    for (int k = 0; k < UK; k++) {
+      const uint32_t f = threadIdx.x + k * CNT;   // float4 index inside the tile
+      if (4 * f >= d.len) continue;
+      const uint32_t j = d.start + 4 * f;
+      float4 g4;
+      if (d.raw || KIND == S_NONE) {
+        g4 = f < nvec ? sm.pay[s][f] : load4_masked(reinterpret_cast<const float*>(p.pbuf + d.pay), j, d.L);
+      } else if (KIND == S_SIGN) {
+        const float h = d.hdr;
+        const uint32_t nib = (words[f >> 3] >> ((f & 7) * 4)) & 15u;
+        g4 = make_float4(nib & 1u ? h : -h, nib & 2u ? h : -h, nib & 4u ? h : -h, nib & 8u ? h : -h);
+      } else {
+        const uint32_t field = load_field(words, (uint64_t)b * 4 * f, 4 * b);
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const uint32_t code = (field >> (b * u)) & ((1u << b) - 1u);
+          float mag;
+          if (KIND == S_LDITHER) {
+            mag = fmul((float)(code >> 1), unit);
+          } else {
+            const uint32_t cl = code >> 1;
+            mag = fmul(cl == 0 ? 0.f : __uint_as_float((uint32_t)(127 - (cmax - (int)cl)) << 23), d.hdr);
+          }
+          set(g4, u, (code & 1u) ? mag : -mag);
+        }
+      }
+      float4 m4, v4, x4;
+      if (f < nvec) {
+        m4 = sm.m[s][f];
+        v4 = sm.v[s][f];
+        x4 = sm.x[s][f];
+      } else {   // ragged tail of a unit: not covered by the 16-byte bulk copies
+        m4 = load4_masked(m, j, d.L);
+        v4 = load4_masked(v, j, d.L);
+        x4 = load4_masked(x, j, d.L);
+      }
+      adam1s(g4.x, m4.x, v4.x, x4.x, p);
+      adam1s(g4.y, m4.y, v4.y, x4.y, p);
+      adam1s(g4.z, m4.z, v4.z, x4.z, p);
+      adam1s(g4.w, m4.w, v4.w, x4.w, p);
+      if (f < nvec) {
+        st4(m + j, m4);
+        st4(v + j, v4);
+        st4(x + j, x4);
+      } else {
+        store4_masked(m, j, d.L, m4);
+        store4_masked(v, j, d.L, v4);
+        store4_masked(x, j, d.L, x4);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[s]);   // this warp is done with stage s
+  }
+}
+
+size_t update_stream_smem() { return sizeof(USmem); }
+
+cudaError_t launch_update_stream(int kind, const UpdateParams& p, int grid, cudaStream_t st) {
+  if (p.n_tiles == 0) return cudaSuccess;
+  auto go = [&](auto fn) -> cudaError_t {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(USmem));
+    if (e != cudaSuccess) return e;
+    const int g = (int)std::min<uint32_t>((uint32_t)grid, p.n_tiles);
+    fn<<<g, SNT, sizeof(USmem), st>>>(p);
+    return cudaGetLastError();
+  };
+  switch (kind) {
+    case S_NONE: return go(update_stream<S_NONE>);
+    case S_SIGN: return go(update_stream<S_SIGN>);
+    case S_LDITHER: return go(update_stream<S_LDITHER>);
+    case S_NDITHER: return go(update_stream<S_NDITHER>);
+  }
+  return cudaErrorInvalidValue;
+}
+
+
+}  // namespace bpc

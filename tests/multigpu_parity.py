@@ -1,0 +1,86 @@
+"""Real multi-GPU parity: one process per GPU (torchrun), libbpc's NCCL exchange
+(bpc_aggregate), every rank checked against the CPU oracle on the same seeded
+inputs.  Launched by tests/test_gpu_multi.py; prints "RANK <r> OK" per rank."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+import oracle
+import paper_2105_07829_b200 as bpc
+from workloads import (LINEAR_DITHER, RANDOM_K, SCALED_SIGN, TOP_K, Comp, Config, gen_grad, gen_params,
+                       layout)
+
+CASES = {
+    "onebit": Comp(SCALED_SIGN, use_ef=1),
+    "topk": Comp(TOP_K, 1, 1000, use_ef=1),
+    "randk": Comp(RANDOM_K, 1, 32, use_ef=1),
+    "ldither": Comp(LINEAR_DITHER, bits=7, use_ef=0),
+}
+SHAPES = (1000, 300000, 70000, 262147, 5, 600000)
+
+
+def f32(a):
+    return np.frombuffer(a.tobytes(), dtype=np.float32)
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    names = sys.argv[1].split(",") if len(sys.argv) > 1 else list(CASES)
+    for name in names:
+        w = Config("mg", "custom", CASES[name], numels=SHAPES, n=world)
+        offs, D = layout(w.tensor_numels())
+        obj = [bpc.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctx = bpc.context_for(w, rank=rank, world_size=world, device=local, nccl_id=obj[0], check_finite=1)
+        x = torch.tensor(gen_params(w), device=dev)
+        ocfg = oracle.Cfg.from_workload(w, n=world)
+        ost = oracle.State(world, D, gen_params(w))
+        lay = ocfg.payload_layout()
+        plan = ocfg.plan()
+        for step in (1, 2, 3):
+            gs = [gen_grad(w, i, step) for i in range(world)]
+            delta, p, _ = oracle.round_(ocfg, ost, np.stack(gs), w.lr)
+            ctx.compress(torch.tensor(gs[rank], device=dev))
+            ctx.aggregate()
+            ctx.step(x, w.lr)
+            ctx.sync()
+            send = ctx.copy_state(bpc.BUF_SEND)
+            pb = ctx.copy_state(bpc.BUF_P)
+            e = f32(ctx.copy_state(bpc.BUF_WORKER_ERR))
+            etl = f32(ctx.copy_state(bpc.BUF_SERVER_ERR))
+            xs = x.cpu().numpy()
+            for ci, (ti, off, L, raw) in enumerate(plan):
+                gc = ctx.chunk(ci)
+                po, nb = lay[ci]
+                assert send[gc.payload_offset:gc.payload_offset + nb].tobytes() == delta[rank, po:po + nb].tobytes(), \
+                    f"{name} rank {rank} step {step}: worker payload of chunk {ci} differs"
+                assert pb[gc.payload_offset:gc.payload_offset + nb].tobytes() == p[po:po + nb].tobytes(), \
+                    f"{name} rank {rank} step {step}: server payload of chunk {ci} differs (owner {gc.owner})"
+                assert e[off:off + L].tobytes() == ost.e[rank, off:off + L].tobytes(), \
+                    f"{name} rank {rank} step {step}: worker error of chunk {ci} differs"
+                if gc.owner == rank and not raw and w.comp.use_ef:
+                    s0 = gc.server_err_offset
+                    assert etl[s0:s0 + L].tobytes() == ost.et[off:off + L].tobytes(), \
+                        f"{name} rank {rank} step {step}: server error of chunk {ci} differs"
+                a, bref = xs[off:off + L], ost.x[off:off + L]
+                rel = np.max(np.abs(a.astype(np.float64) - bref) / np.maximum(np.abs(bref), 1e-30))
+                assert rel <= 1e-6, f"{name} rank {rank}: x rel diff {rel}"
+        ctx.finalize()
+        dist.barrier()
+        print(f"RANK {rank} {name} OK", flush=True)
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
