@@ -104,9 +104,18 @@ static __device__ __noinline__ void watchdog_fire(const char* what, uint32_t a, 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, uint32_t tag = 0) {
   if (mbar_try(bar, parity)) return;
   const long long t0 = clock64();
-  while (!mbar_try(bar, parity)) {
-    if (clock64() - t0 > BPC_WATCHDOG_CYCLES)
+  for (uint32_t it = 1; !mbar_try(bar, parity); it++) {
+    if ((it & 63) == 0 && clock64() - t0 > BPC_WATCHDOG_CYCLES)
       watchdog_fire("mbarrier", tag, parity, (unsigned long long)smem_u32(bar), 0);
+  }
+}
+// spin (with backoff) until *flag >= target; flag is a shared-memory counter
+__device__ __forceinline__ void smem_wait_geq(const uint32_t* flag, uint32_t target, uint32_t tag) {
+  if (*reinterpret_cast<const volatile uint32_t*>(flag) >= target) return;
+  const long long t0 = clock64();
+  for (uint32_t it = 1; *reinterpret_cast<const volatile uint32_t*>(flag) < target; it++) {
+    __nanosleep(64);
+    if ((it & 63) == 0 && clock64() - t0 > BPC_WATCHDOG_CYCLES) watchdog_fire("smem flag", tag, 0, 0, target);
   }
 }
 // gpu-scope release add / acquire load on unit counters (cross-CTA unit reductions)
@@ -128,8 +137,9 @@ __device__ __forceinline__ void wait_counter(const unsigned long long* p, unsign
                                              uint32_t tag = 0) {
   const long long t0 = clock64();
   unsigned long long v;
-  while ((v = ld_relaxed(p)) < target) {
-    if (clock64() - t0 > BPC_WATCHDOG_CYCLES) watchdog_fire("counter", tag, 0, v, target);
+  for (uint32_t it = 1; (v = ld_relaxed(p)) < target; it++) {
+    __nanosleep(128);
+    if ((it & 63) == 0 && clock64() - t0 > BPC_WATCHDOG_CYCLES) watchdog_fire("counter", tag, 0, v, target);
   }
   (void)ld_acquire(p);
 }

@@ -7,20 +7,26 @@
 //   server  (A5-A7): Delta = (1/n) sum_i dec(delta_i) + e~ (l.10),
 //           p = C(Delta) (l.11), e~ = Delta - dec(p) (l.13)
 //
-// One CTA per SM walks 2^13-element slices of its units through a ring of
-// NS (<= 8) shared-memory stages sized at launch.  Warps:
-//   PRODUCER  reads the slice descriptors and issues the 1-D bulk copies
-//             (cp.async.bulk, mbarrier complete_tx): worker g, e; server e~ and
-//             the n ranks' payload bytes of the slice;
-//   4 REDUCERS (slice i -> reducer i % 4) complete each unit's fp64
-//             pairwise-tree total (R6):
-//             single-slice units take the local partial; for multi-slice units
-//             the reducer publishes the slice's partial, bumps the unit counter
-//             (release) and waits (relaxed spin + one acquire) for the others;
-//   16 CONSUMERS  produce slice i (q or Delta in place, slice partial) and
-//             then emit slice i-1 (codes + error) once its total is ready.
-// All CTAs are co-resident (cooperative launch) and every CTA publishes slice i
-// before it waits on slice i-1's unit, so the waits cannot deadlock.
+// One CTA per SM walks 2^13-element slices of its units.  Shared memory holds
+// two rings sized at launch:
+//   HELD ring  (NH x 32 KB)  q (worker: g lands here by TMA, q = g + e in place)
+//                            or Delta (server), kept until the slice is emitted;
+//   INPUT ring (NI x SI)     e (worker) or e~ and the n ranks' payload bytes
+//                            (server), released as soon as the slice is produced.
+// Warps:
+//   PRODUCER   reads the slice descriptors and issues the 1-D bulk copies
+//              (cp.async.bulk -> UBLKCP, one mbarrier complete_tx per slice);
+//   4 REDUCERS (slice i -> reducer i % 4) complete each unit's fp64 pairwise-tree
+//              total (R6): a multi-slice unit publishes one partial per
+//              slice (release add on a per-unit counter) and each slice's reducer
+//              waits (relaxed spin + one acquire) for the unit, then reduces it;
+//   16 CONSUMERS produce slice i (q or Delta, slice partial) and then emit slice
+//              i - D (codes + error) once its total is ready, D = NH - 2 <= 3, so
+//              the cross-CTA wait overlaps the produce of D later slices.
+// All CTAs are co-resident (cooperative launch) and every slice's partial is
+// published before its CTA waits on an earlier unit, so the waits cannot
+// deadlock.  Each mbarrier has a single in-order waiter group; the reducers,
+// which run out of order, wait on a monotonic shared-memory counter instead.
 #include "device.cuh"
 
 namespace bpc {
@@ -33,12 +39,13 @@ constexpr int CPROD = CCW;               // producer warp index
 constexpr int CRED = CCW + 1;            // first reducer warp index
 constexpr int CRW = 4;                   // reducer warps (slice i -> reducer i % CRW)
 constexpr int CSNT = CCNT + 32 + 32 * CRW;   // + producer + reducers
-constexpr int CDEF = 1;                  // emit of slice i - CDEF follows the produce of slice i
-constexpr int CMAXST = 8;                // max stages
+constexpr int CMAXH = 8;                 // max held stages
+constexpr int CNI = 2;                   // input stages
+constexpr int CMAXD = 3;                 // max emit deferral
 constexpr int CSL = 8192;                // elements per slice
 constexpr int CK = CSL / 4 / CCNT;       // float4 per consumer thread per slice
-constexpr int CNRED = CK * CCW;          // 128-element warp subtrees per slice (32 or 64)
-constexpr int CUNITSL = (1 << 18) / CSL; // max slices per unit (32 or 64)
+constexpr int CNRED = CK * CCW;          // 128-element warp subtrees per slice (64)
+constexpr int CUNITSL = (1 << 18) / CSL; // max slices per unit (32)
 constexpr int CMAXN = 32;                // ranks whose headers are staged (server)
 static_assert(CNRED == 32 || CNRED == 64, "slice tree expects 32 or 64 warp subtrees");
 
@@ -54,13 +61,13 @@ struct CDesc {
 };
 
 struct __align__(128) CHead {
-  uint64_t full[CMAXST], empty[CMAXST], tready[CMAXST];
-  uint32_t produced;   // slices produced so far (monotonic; reducers wait on it out of order)
-  CDesc desc[CMAXST];
+  uint64_t fullI[CNI], emptyI[CNI], emptyH[CMAXH], tready[CMAXH];
+  uint32_t produced;   // slices produced so far (monotonic; the reducers wait on it out of order)
+  CDesc desc[CMAXH];
   double red[2][CNRED];
-  double part[CMAXST];
-  double total[CMAXST];
-  float hdr[CMAXST][CMAXN];
+  double part[CMAXH];
+  double total[CMAXH];
+  float hdr[CMAXH][CMAXN];
 };
 
 __device__ __forceinline__ void mbar_arrive1(uint64_t* bar) {
@@ -112,20 +119,27 @@ template <int KIND, bool SERVER>
 __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant__ StreamParams p) {
   extern __shared__ __align__(128) unsigned char sraw[];
   CHead& hd = *reinterpret_cast<CHead*>(sraw);
-  unsigned char* ring = sraw + sizeof(CHead);
-  const uint32_t NS = p.nstages;
-  const uint32_t SA = p.stage_a, SB = p.stage_b;   // bytes of the two regions of a stage
-  auto regA = [&](uint32_t s) { return reinterpret_cast<float4*>(ring + s * (SA + SB)); };
-  auto regB = [&](uint32_t s) { return reinterpret_cast<float4*>(ring + s * (SA + SB) + SA); };
+  const uint32_t NH = p.nstages;          // held stages
+  const uint32_t D = NH - 2 < (uint32_t)CMAXD ? NH - 2 : (uint32_t)CMAXD;   // emit deferral
+  const uint32_t SI = p.stage_b;          // bytes per input stage
+  const uint32_t SIE = p.stage_a;         // byte offset of the e / e~ region inside an input stage
+  unsigned char* held = sraw + sizeof(CHead);
+  unsigned char* input = held + (size_t)NH * CSL * 4;
+  auto H = [&](uint32_t s) { return reinterpret_cast<float4*>(held + (size_t)s * CSL * 4); };
+  auto I = [&](uint32_t t) { return input + (size_t)t * SI; };               // payload pieces at 0
+  auto IE = [&](uint32_t t) { return reinterpret_cast<float4*>(input + (size_t)t * SI + SIE); };
   const uint32_t G = gridDim.x;
   const uint32_t mine = p.n_slices > blockIdx.x ? (p.n_slices - blockIdx.x + G - 1) / G : 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = KIND == C_SIGN ? 1 : (int)p.bits;       // bits per element in the payload stream
   if (threadIdx.x == 0) {
-    for (uint32_t s = 0; s < NS; s++) {
-      mbar_init(&hd.full[s], 1);
-      mbar_init(&hd.empty[s], CCW);
+    for (uint32_t s = 0; s < NH; s++) {
+      mbar_init(&hd.emptyH[s], CCW);
       mbar_init(&hd.tready[s], 1);
+    }
+    for (uint32_t t = 0; t < (uint32_t)CNI; t++) {
+      mbar_init(&hd.fullI[t], 1);
+      mbar_init(&hd.emptyI[t], CCW);
     }
     hd.produced = 0;
     fence_mbar_init();
@@ -136,8 +150,9 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
   if (warp == CPROD) {
     if (lane == 0) {
       for (uint32_t i = 0; i < mine; i++) {
-        const uint32_t s = i % NS;
-        if (i >= NS) mbar_wait(&hd.empty[s], ((i / NS) - 1) & 1, 0x1000000u | i);
+        const uint32_t hs = i % NH, t = i % CNI;
+        if (i >= NH) mbar_wait(&hd.emptyH[hs], ((i / NH) - 1) & 1, 0x1000000u | i);
+        if (i >= (uint32_t)CNI) mbar_wait(&hd.emptyI[t], ((i / CNI) - 1) & 1, 0x1100000u | i);
         const Slice sl = p.slices[blockIdx.x + i * G];
         const DevChunk c = p.chunks[sl.chunk];
         CDesc d;
@@ -171,21 +186,21 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
           if (p.use_ef) tx += nvb;
           if (d.staged) tx += p.n * (uint32_t)(a1 - a0);
           for (uint32_t r = 0; r < p.n && r < (uint32_t)CMAXN; r++)
-            hd.hdr[s][r] = *reinterpret_cast<const float*>(p.recv + r * p.slot_bytes + c.recv);
+            hd.hdr[hs][r] = *reinterpret_cast<const float*>(p.recv + r * p.slot_bytes + c.recv);
         }
-        hd.desc[s] = d;
-        mbar_arrive_expect_tx(&hd.full[s], tx);
+        hd.desc[hs] = d;
+        mbar_arrive_expect_tx(&hd.fullI[t], tx);
         if (!SERVER) {
           if (nvb) {
-            tma_load_1d(regA(s), p.grad + c.off + sl.start, nvb, &hd.full[s]);
-            if (p.use_ef && comp) tma_load_1d(regB(s), p.err + c.off + sl.start, nvb, &hd.full[s]);
+            tma_load_1d(H(hs), p.grad + c.off + sl.start, nvb, &hd.fullI[t]);
+            if (p.use_ef && comp) tma_load_1d(IE(t), p.err + c.off + sl.start, nvb, &hd.fullI[t]);
           }
         } else if (comp) {
-          if (p.use_ef && nvb) tma_load_1d(regB(s), p.err + c.etl + sl.start, nvb, &hd.full[s]);
+          if (p.use_ef && nvb) tma_load_1d(IE(t), p.err + c.etl + sl.start, nvb, &hd.fullI[t]);
           if (d.staged)
             for (uint32_t r = 0; r < p.n; r++)
-              tma_load_1d(reinterpret_cast<uint8_t*>(regA(s)) + r * p.piece_stride,
-                          p.recv + r * p.slot_bytes + c.recv + a0, (uint32_t)(a1 - a0), &hd.full[s]);
+              tma_load_1d(I(t) + r * p.piece_stride, p.recv + r * p.slot_bytes + c.recv + a0,
+                          (uint32_t)(a1 - a0), &hd.fullI[t]);
         }
       }
     }
@@ -195,25 +210,21 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
   // ===================================================== reducers
   if (warp >= CRED) {
     for (uint32_t i = warp - CRED; i < mine; i += CRW) {
-      const uint32_t s = i % NS;
-      {   // wait until the consumers have produced slice i (monotonic counter: no parity aliasing)
-        const long long t0 = clock64();
-        while (*reinterpret_cast<volatile uint32_t*>(&hd.produced) < i + 1)
-          if (clock64() - t0 > BPC_WATCHDOG_CYCLES) watchdog_fire("produced", 0x2000000u | i, 0, 0, 0);
-        __threadfence_block();
-      }
-      const uint32_t ns = hd.desc[s].nslices;
+      const uint32_t hs = i % NH;
+      smem_wait_geq(&hd.produced, i + 1, 0x2000000u | i);   // slice i produced
+      __threadfence_block();
+      const uint32_t ns = hd.desc[hs].nslices;
       if (ns > 1) {
         if (lane == 0) {
           // publish this slice's partial, then wait for the unit's other slices
-          const CDesc& d = hd.desc[s];
-          p.partials[d.unit_first + d.sidx] = hd.part[s];
+          const CDesc& d = hd.desc[hs];
+          p.partials[d.unit_first + d.sidx] = hd.part[hs];
           red_release_add(p.counters + d.unit, 1ull);
           wait_counter(p.counters + d.unit, (unsigned long long)p.epoch * ns, 0x3000000u | i);
         }
         __syncwarp();
         // unit total: pairwise tree over its slices, zero-padded to CUNITSL (R6)
-        const double* P = p.partials + hd.desc[s].unit_first;
+        const double* P = p.partials + hd.desc[hs].unit_first;
         double v;
         if (CUNITSL == 64) {   // lane l holds the 2-slice subtree (2l, 2l+1)
           const uint32_t l0 = 2 * lane, l1 = 2 * lane + 1;
@@ -222,12 +233,12 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
           v = (uint32_t)lane < ns ? __ldcg(P + lane) : 0.0;
         }
         v = warp_tree(v);
-        if (lane == 0) hd.total[s] = v;
+        if (lane == 0) hd.total[hs] = v;
       } else if (ns == 1 && lane == 0) {
-        hd.total[s] = hd.part[s];
+        hd.total[hs] = hd.part[hs];
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive1(&hd.tready[s]);
+      if (lane == 0) mbar_arrive1(&hd.tready[hs]);
     }
     return;
   }
@@ -242,15 +253,15 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
   const uint32_t rng_rank = SERVER ? 0u : p.rank;
   bool bad = false;
 
-  for (uint32_t i = 0; i < mine + CDEF; i++) {
+  for (uint32_t i = 0; i < mine + D; i++) {
     // ---------------- produce slice i
     if (i < mine) {
-      const uint32_t s = i % NS;
-      mbar_wait(&hd.full[s], (i / NS) & 1, 0x4000000u | i);
-      const CDesc d = hd.desc[s];
+      const uint32_t hs = i % NH, t = i % CNI;
+      mbar_wait(&hd.fullI[t], (i / CNI) & 1, 0x4000000u | i);
+      const CDesc d = hd.desc[hs];
       const uint32_t nvec = d.len >> 2;
       const bool comp = d.nslices > 0;
-      float4* val = SERVER ? regB(s) : regA(s);
+      float4* val = H(hs);
 #pragma unroll
       for (int k = 0; k < CK; k++) {
         const uint32_t f = threadIdx.x + k * CCNT;
@@ -260,8 +271,8 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
           const bool ef = p.use_ef && comp;
           float4 g4 = q, e4 = q;
           if (f < nvec) {
-            g4 = regA(s)[f];
-            if (ef) e4 = regB(s)[f];
+            g4 = val[f];
+            if (ef) e4 = IE(t)[f];
           } else if (4 * f < d.len) {   // ragged tail (not in the 16-byte bulk copy)
             g4 = load4_masked(p.grad + d.off, j, d.L);
             if (ef) e4 = load4_masked(p.err + d.off, j, d.L);
@@ -278,38 +289,67 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
               acc[2] += (double)x4.z;
               acc[3] += (double)x4.w;
             }
+          } else if (p.n == 1) {
+            // n = 1: Delta = fl32(fl64(dec * 1.0) + fl64(e~)) equals the fp32 sum
+            // fl32(dec + e~): the fp64 sum of two fp32 values is exact unless their
+            // exponents differ by more than 29, and then both roundings return the
+            // larger operand.  One fp32 add instead of four conversions.
+            const float h = hd.hdr[hs][0];
+            const uint32_t* words =
+                d.staged ? reinterpret_cast<const uint32_t*>(I(t) + d.pofs)
+                         : reinterpret_cast<const uint32_t*>(p.recv + d.recv + 4 + (uint64_t)d.start * b / 8);
+            const uint32_t field = KIND == C_SIGN ? ((words[f >> 3] >> ((f & 7) * 4)) & 15u)
+                                                  : load_field(words, (uint64_t)b * 4 * f, nb);
+            const float unit = fdiv(h, slv);
+            float4 e4 = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (p.use_ef) e4 = f < nvec ? IE(t)[f] : load4_masked(p.err + d.etl, j, d.L);
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+              float dec;
+              if (KIND == C_SIGN) {
+                dec = ((field >> u) & 1u) ? h : -h;
+              } else {
+                const uint32_t code = (field >> (b * u)) & cmask;
+                const float mag = dither_mag<KIND>(code, h, unit, cmax);
+                dec = (code & 1u) ? mag : -mag;
+              }
+              // acc = +0.0 + dec (turns -0 into +0, as the fp64 sum does), then + e~
+              if (j + u < d.L) set(q, u, fadd(fadd(0.f, dec), get(e4, u)));
+            }
           } else {
             for (uint32_t r = 0; r < p.n; r++) {
-              const float h = r < (uint32_t)CMAXN ? hd.hdr[s][r]
+              const float h = r < (uint32_t)CMAXN ? hd.hdr[hs][r]
                                                   : *reinterpret_cast<const float*>(p.recv + r * p.slot_bytes + d.recv);
               const uint32_t* words =
-                  d.staged ? reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(regA(s)) +
-                                                               r * p.piece_stride + d.pofs)
+                  d.staged ? reinterpret_cast<const uint32_t*>(I(t) + r * p.piece_stride + d.pofs)
                            : reinterpret_cast<const uint32_t*>(p.recv + r * p.slot_bytes + d.recv + 4 +
                                                                (uint64_t)d.start * b / 8);
               const uint32_t field = KIND == C_SIGN ? ((words[f >> 3] >> ((f & 7) * 4)) & 15u)
                                                     : load_field(words, (uint64_t)b * 4 * f, nb);
               const float unit = fdiv(h, slv);
+              const double hd64 = (double)h;   // sign: one conversion per rank, not per element
 #pragma unroll
               for (int u = 0; u < 4; u++) {
-                float dec;
+                double dec;
                 if (KIND == C_SIGN) {
-                  dec = ((field >> u) & 1u) ? h : -h;
+                  dec = ((field >> u) & 1u) ? hd64 : -hd64;
                 } else {
                   const uint32_t code = (field >> (b * u)) & cmask;
                   const float mag = dither_mag<KIND>(code, h, unit, cmax);
-                  dec = (code & 1u) ? mag : -mag;
+                  dec = (double)((code & 1u) ? mag : -mag);
                 }
-                if (j + u < d.L) acc[u] += (double)dec;
+                if (j + u < d.L) acc[u] += dec;
               }
             }
           }
-          float4 e4 = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (comp && p.use_ef) e4 = f < nvec ? regB(s)[f] : load4_masked(p.err + d.etl, j, d.L);
-          if (j < d.L) q.x = mean_plus(acc[0], p.inv_n, (double)e4.x);
-          if (j + 1 < d.L) q.y = mean_plus(acc[1], p.inv_n, (double)e4.y);
-          if (j + 2 < d.L) q.z = mean_plus(acc[2], p.inv_n, (double)e4.z);
-          if (j + 3 < d.L) q.w = mean_plus(acc[3], p.inv_n, (double)e4.w);
+          if (!comp || p.n != 1) {
+            float4 e4 = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (comp && p.use_ef) e4 = f < nvec ? IE(t)[f] : load4_masked(p.err + d.etl, j, d.L);
+            if (j < d.L) q.x = mean_plus(acc[0], p.inv_n, (double)e4.x);
+            if (j + 1 < d.L) q.y = mean_plus(acc[1], p.inv_n, (double)e4.y);
+            if (j + 2 < d.L) q.z = mean_plus(acc[2], p.inv_n, (double)e4.z);
+            if (j + 3 < d.L) q.w = mean_plus(acc[3], p.inv_n, (double)e4.w);
+          }
         }
         val[f] = q;
         if (comp) {
@@ -317,31 +357,32 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
           if (lane == 0) hd.red[i & 1][k * CCW + warp] = a;   // subtree of slice elements [128 m, 128 m + 128)
         }
       }
-      if (comp) cons_sync();
+      __syncwarp();
+      if (lane == 0) mbar_arrive1(&hd.emptyI[t]);   // input stage consumed by this warp
+      cons_sync();                                    // all q written, red complete
       if (warp == 0) {
         if (comp) {
           const double r = warp_tree(CNRED == 64 ? hd.red[i & 1][2 * lane] + hd.red[i & 1][2 * lane + 1]
                                                  : hd.red[i & 1][lane]);
-          if (lane == 0) hd.part[s] = r;   // the slice's reducer publishes it
+          if (lane == 0) hd.part[hs] = r;   // the slice's reducer publishes it
         }
-        __syncwarp();
         if (lane == 0) {
           __threadfence_block();
           *reinterpret_cast<volatile uint32_t*>(&hd.produced) = i + 1;
         }
       }
     }
-    // ---------------- emit slice i - CDEF
-    if (i >= (uint32_t)CDEF) {
-      const uint32_t ie = i - CDEF;
-      const uint32_t s = ie % NS;
-      const CDesc d = hd.desc[s];
+    // ---------------- emit slice i - D
+    if (i >= D) {
+      const uint32_t ie = i - D;
+      const uint32_t hs = ie % NH;
+      const CDesc d = hd.desc[hs];
       const uint32_t L = d.L;
       uint8_t* pay = p.out + d.pay;
-      const float4* val = SERVER ? regB(s) : regA(s);
+      const float4* val = H(hs);
       // every slice (raw included) waits for its reducer before the stage is
       // recycled: keeps each mbarrier at most one phase ahead of its waiters
-      mbar_wait(&hd.tready[s], (ie / NS) & 1, 0x5000000u | ie);
+      mbar_wait(&hd.tready[hs], (ie / NH) & 1, 0x5000000u | ie);
       if (d.nslices == 0) {   // raw unit: fp32 payload (worker: g, no EF; server: the mean)
         float* out = reinterpret_cast<float*>(pay);
 #pragma unroll
@@ -350,7 +391,7 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
           if (4 * f < d.len) store4_masked(out, d.start + 4 * f, L, val[f]);
         }
       } else {
-        const double total = hd.total[s];
+        const double total = hd.total[hs];
         float* errp = p.use_ef ? (SERVER ? p.err + d.etl : p.err + d.off) : nullptr;
         if (KIND == C_SIGN) {
           const float sc = __double2float_rn(total / (double)L);
@@ -412,27 +453,29 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive1(&hd.empty[s]);   // this warp is done with stage ie % NS
+      if (lane == 0) mbar_arrive1(&hd.emptyH[hs]);   // this warp is done with held stage hs
     }
   }
   if (bad) atomicOr(p.flag, 1u);
 }
 
-// stage geometry for a launch: regions A / B per stage, stage count, smem bytes
-static void cstream_geometry(bool server, const StreamParams& p, uint32_t* sa, uint32_t* sb, uint32_t* ns,
+// ring geometry for a launch: input-stage size and layout, number of held stages
+static void cstream_geometry(bool server, const StreamParams& p, uint32_t* sie, uint32_t* si, uint32_t* nh,
                              size_t* smem) {
   const uint32_t slice_bytes = CSL * 4;
+  uint32_t pieces = 0, ebytes = 0;
   if (!server) {
-    *sa = slice_bytes;                       // g -> q
-    *sb = p.use_ef ? slice_bytes : 0;        // e
+    ebytes = p.use_ef ? slice_bytes : 0;                                              // e
   } else {
-    *sa = p.stage_payload ? (uint32_t)((p.n * p.piece_stride + 127) / 128 * 128) : 0;   // payload pieces
-    *sb = slice_bytes;                       // e~ -> Delta
+    pieces = p.stage_payload ? (uint32_t)((p.n * p.piece_stride + 127) / 128 * 128) : 0;   // payload pieces
+    ebytes = p.use_ef ? slice_bytes : 0;                                              // e~
   }
+  *sie = pieces;
+  *si = pieces + ebytes;
   const size_t budget = 227 * 1024 - sizeof(CHead) - 1024;
-  uint32_t n = (uint32_t)(budget / (*sa + *sb));
-  *ns = n > (uint32_t)CMAXST ? (uint32_t)CMAXST : n;
-  *smem = sizeof(CHead) + (size_t)(*ns) * (*sa + *sb);
+  uint32_t n = (uint32_t)((budget - (size_t)CNI * (*si)) / slice_bytes);
+  *nh = n > (uint32_t)CMAXH ? (uint32_t)CMAXH : n;
+  *smem = sizeof(CHead) + (size_t)(*nh) * slice_bytes + (size_t)CNI * (*si);
 }
 
 template <bool SERVER>
@@ -440,7 +483,7 @@ static cudaError_t launch_cstream_t(int kind, StreamParams p, int grid, cudaStre
   if (p.n_slices == 0) return cudaSuccess;
   size_t smem;
   cstream_geometry(SERVER, p, &p.stage_a, &p.stage_b, &p.nstages, &smem);
-  if (p.nstages < CDEF + 2) return cudaErrorInvalidConfiguration;   // held stages + one in flight
+  if (p.nstages < 3) return cudaErrorInvalidConfiguration;   // deferral >= 1 needs 3 held stages
   auto go = [&](auto fn) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
