@@ -46,7 +46,6 @@ constexpr int CSL = 8192;                // elements per slice
 constexpr int CK = CSL / 4 / CCNT;       // float4 per consumer thread per slice
 constexpr int CNRED = CK * CCW;          // 128-element warp subtrees per slice (64)
 constexpr int CUNITSL = (1 << 18) / CSL; // max slices per unit (32)
-constexpr int CMAXN = 32;                // ranks whose headers are staged (server)
 static_assert(CNRED == 32 || CNRED == 64, "slice tree expects 32 or 64 warp subtrees");
 
 struct CDesc {
@@ -67,7 +66,6 @@ struct __align__(128) CHead {
   double red[2][CNRED];
   double part[CMAXH];
   double total[CMAXH];
-  float hdr[CMAXH][CMAXN];
 };
 
 __device__ __forceinline__ void mbar_arrive1(uint64_t* bar) {
@@ -126,7 +124,10 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
   unsigned char* held = sraw + sizeof(CHead);
   unsigned char* input = held + (size_t)NH * CSL * 4;
   auto H = [&](uint32_t s) { return reinterpret_cast<float4*>(held + (size_t)s * CSL * 4); };
-  auto I = [&](uint32_t t) { return input + (size_t)t * SI; };               // payload pieces at 0
+  // server input stage: [n x 16-byte payload heads][n payload pieces][e~]
+  const uint32_t HB = SERVER ? (16 * p.n + 127) / 128 * 128 : 0;
+  auto IH = [&](uint32_t t) { return input + (size_t)t * SI; };               // payload heads
+  auto I = [&](uint32_t t) { return input + (size_t)t * SI + HB; };          // payload pieces
   auto IE = [&](uint32_t t) { return reinterpret_cast<float4*>(input + (size_t)t * SI + SIE); };
   const uint32_t G = gridDim.x;
   const uint32_t mine = p.n_slices > blockIdx.x ? (p.n_slices - blockIdx.x + G - 1) / G : 0;
@@ -149,12 +150,20 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
   // ===================================================== producer
   if (warp == CPROD) {
     if (lane == 0) {
+      // descriptors of the next slice are loaded before the stage waits, so their
+      // latency overlaps the wait instead of delaying the bulk copies
+      Slice sl_next = mine ? p.slices[blockIdx.x] : Slice{};
+      DevChunk c_next = mine ? p.chunks[sl_next.chunk] : DevChunk{};
       for (uint32_t i = 0; i < mine; i++) {
         const uint32_t hs = i % NH, t = i % CNI;
+        const Slice sl = sl_next;
+        const DevChunk c = c_next;
+        if (i + 1 < mine) {
+          sl_next = p.slices[blockIdx.x + (i + 1) * G];
+          c_next = p.chunks[sl_next.chunk];
+        }
         if (i >= NH) mbar_wait(&hd.emptyH[hs], ((i / NH) - 1) & 1, 0x1000000u | i);
         if (i >= (uint32_t)CNI) mbar_wait(&hd.emptyI[t], ((i / CNI) - 1) & 1, 0x1100000u | i);
-        const Slice sl = p.slices[blockIdx.x + i * G];
-        const DevChunk c = p.chunks[sl.chunk];
         CDesc d;
         d.off = c.off;
         d.pay = c.pay;
@@ -185,8 +194,7 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
           d.staged = p.stage_payload;
           if (p.use_ef) tx += nvb;
           if (d.staged) tx += p.n * (uint32_t)(a1 - a0);
-          for (uint32_t r = 0; r < p.n && r < (uint32_t)CMAXN; r++)
-            hd.hdr[hs][r] = *reinterpret_cast<const float*>(p.recv + r * p.slot_bytes + c.recv);
+          tx += 16 * p.n;   // each rank's payload head (scale / norm) by bulk copy
         }
         hd.desc[hs] = d;
         mbar_arrive_expect_tx(&hd.fullI[t], tx);
@@ -197,6 +205,8 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
           }
         } else if (comp) {
           if (p.use_ef && nvb) tma_load_1d(IE(t), p.err + c.etl + sl.start, nvb, &hd.fullI[t]);
+          for (uint32_t r = 0; r < p.n; r++)
+            tma_load_1d(IH(t) + 16 * r, p.recv + r * p.slot_bytes + c.recv, 16, &hd.fullI[t]);
           if (d.staged)
             for (uint32_t r = 0; r < p.n; r++)
               tma_load_1d(I(t) + r * p.piece_stride, p.recv + r * p.slot_bytes + c.recv + a0,
@@ -294,7 +304,7 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
             // fl32(dec + e~): the fp64 sum of two fp32 values is exact unless their
             // exponents differ by more than 29, and then both roundings return the
             // larger operand.  One fp32 add instead of four conversions.
-            const float h = hd.hdr[hs][0];
+            const float h = *reinterpret_cast<const float*>(IH(t));
             const uint32_t* words =
                 d.staged ? reinterpret_cast<const uint32_t*>(I(t) + d.pofs)
                          : reinterpret_cast<const uint32_t*>(p.recv + d.recv + 4 + (uint64_t)d.start * b / 8);
@@ -318,8 +328,7 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
             }
           } else {
             for (uint32_t r = 0; r < p.n; r++) {
-              const float h = r < (uint32_t)CMAXN ? hd.hdr[hs][r]
-                                                  : *reinterpret_cast<const float*>(p.recv + r * p.slot_bytes + d.recv);
+              const float h = *reinterpret_cast<const float*>(IH(t) + 16 * r);
               const uint32_t* words =
                   d.staged ? reinterpret_cast<const uint32_t*>(I(t) + r * p.piece_stride + d.pofs)
                            : reinterpret_cast<const uint32_t*>(p.recv + r * p.slot_bytes + d.recv + 4 +
@@ -470,8 +479,9 @@ static void cstream_geometry(bool server, const StreamParams& p, uint32_t* sie, 
     pieces = p.stage_payload ? (uint32_t)((p.n * p.piece_stride + 127) / 128 * 128) : 0;   // payload pieces
     ebytes = p.use_ef ? slice_bytes : 0;                                              // e~
   }
-  *sie = pieces;
-  *si = pieces + ebytes;
+  const uint32_t heads = server ? (16 * p.n + 127) / 128 * 128 : 0;   // payload heads
+  *sie = heads + pieces;
+  *si = heads + pieces + ebytes;
   const size_t budget = 227 * 1024 - sizeof(CHead) - 1024;
   uint32_t n = (uint32_t)((budget - (size_t)CNI * (*si)) / slice_bytes);
   *nh = n > (uint32_t)CMAXH ? (uint32_t)CMAXH : n;

@@ -43,11 +43,11 @@ def launches(path):
         names[r[idi]] = short(r[ki])
         v = float(r[vi].replace(",", ""))
         unit = r[ui]
-        if unit == "nsecond":
+        if unit in ("nsecond", "ns"):
             v /= 1e3
-        elif unit == "msecond":
+        elif unit in ("msecond", "ms"):
             v *= 1e3
-        elif unit == "usecond":
+        elif unit in ("usecond", "us"):
             pass
         elif unit in ("byte",):
             pass
