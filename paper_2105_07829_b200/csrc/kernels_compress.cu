@@ -20,16 +20,28 @@ namespace bpc {
 
 enum { K_NONE = 0, K_SIGN = 2, K_TOPK = 3, K_RANDK = 4, K_LDITHER = 5, K_NDITHER = 6 };
 
+constexpr int FNB = 1024;   // bins of the sparse kinds' 10-bit key histogram (= candidate capacity)
+
 struct __align__(16) Smem {
   float4 q[SLICE / 4];      // the slice of q (worker) or Delta (server)
-  double red[128];          // warp subtree sums
+  union {
+    double red[128];        // dense kinds: warp subtree sums
+    uint32_t fh[FNB];       // sparse kinds: 10-bit key histogram (DSMEM), then CTA 0's candidate keys
+  };
+  union {
+    uint32_t bsum[FNB];     // sparse: this CTA's share of the cluster-wide histogram (DSMEM)
+    struct {
+      uint32_t hist[2][256];   // sparse fallback: radix-select histograms (DSMEM)
+      uint32_t tot[256];
+    };
+  };
   double part;              // this slice's subtree sum (read through DSMEM)
   double total;             // unit total
-  uint32_t hist[2][256];    // radix-select histograms (read through DSMEM)
-  uint32_t tot[256];
   uint32_t cnt[2];          // (#key > T, #key == T) of this slice (DSMEM)
   uint32_t scan[NWARP + 1];
-  uint32_t info[4];
+  uint32_t info[8];
+  uint32_t btot;            // sum of bsum (DSMEM)
+  uint32_t ccount;          // candidates gathered into CTA 0 (DSMEM atomics)
 };
 
 size_t compress_smem_bytes() { return sizeof(Smem); }
@@ -414,8 +426,132 @@ __device__ void emit_sparse(const CompressParams& p, const DevChunk& c, Smem& sm
   const uint32_t L = c.len, k = c.k, cs = p.cs;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t prefix = 0, pmask = 0, kk = k;
-  // ---- radix select of the k-th largest key over the whole unit (cluster)
-  for (int pass = 0; pass < 4; pass++) {
+  bool selected = false;
+  // ---- fast exact select of the k-th largest key over the unit (cluster):
+  // (1) 10-bit histogram of the top key bits per slice (plain smem atomics);
+  // (2) CTA r sums bins [r B, r B + B) over the cluster (DSMEM), B = 1024 / cs;
+  // (3) every CTA scans the block totals and that block's bins from the top to
+  //     find the bin holding the k-th largest key and the count above it;
+  // (4) the bin's keys (a few hundred for gradients) are gathered into CTA 0
+  //     (DSMEM atomics), which ranks them exactly; T and the number of T-ties to
+  //     take are read back by every CTA.  A bin larger than the capacity (e.g. a
+  //     unit of equal values) falls back to the 4 x 8-bit radix select below.
+  {
+    constexpr int DSH = KIND == K_TOPK ? 21 : 22;   // |q| bits have bit 31 clear; Philox keys use all 32
+    if (threadIdx.x == 0) sm.ccount = 0;
+    // up to two 10-bit rounds: round 1 histograms only the keys of round 0's bin
+    uint32_t bin = 0, above = 0, cnt = 0, dsh = DSH;
+    for (int round = 0; round < 2; round++) {
+      dsh = DSH - 10 * round;
+      const uint32_t pbin = bin;   // round 1: keys with (key >> DSH) == pbin
+      for (uint32_t b = threadIdx.x; b < (uint32_t)FNB; b += NT) sm.fh[b] = 0;
+      __syncthreads();
+#pragma unroll 2
+      for (int it = 0; it < IT; it++) {
+        const uint32_t i4 = it * NT + threadIdx.x;
+        const uint32_t j = s0 + 4 * i4;
+        if (j >= L) continue;
+        const uint4 kq = keys4<KIND>(sm.q[i4], j, p, c.id, stage, rrank);
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const uint32_t key = getu(kq, u);
+          if (j + u < L && (round == 0 || (key >> DSH) == pbin))
+            atomicAdd(&sm.fh[(key >> dsh) & (FNB - 1)], 1u);
+        }
+      }
+      cluster_sync_all();   // histograms visible to the cluster
+      const uint32_t B = FNB / cs;
+      uint32_t bt = 0;
+      for (uint32_t b = threadIdx.x; b < B; b += NT) {
+        uint32_t s = 0;
+        for (uint32_t r = 0; r < cs; r++) s += dsmem(sm.fh, r)[crank * B + b];
+        sm.bsum[b] = s;
+        bt += s;
+      }
+      bt = __reduce_add_sync(0xffffffffu, bt);
+      if (threadIdx.x == 0) sm.btot = 0;
+      __syncthreads();
+      if (lane == 0) atomicAdd(&sm.btot, bt);
+      cluster_sync_all();   // block sums visible
+      if (threadIdx.x == 0) {
+        uint32_t ab = above, blk = 0, bn = 0, cn = 0;
+        for (int r = (int)cs - 1; r >= 0; r--) {
+          const uint32_t t = *dsmem(&sm.btot, (uint32_t)r);
+          if (ab + t >= k) {
+            blk = (uint32_t)r;
+            break;
+          }
+          ab += t;
+        }
+        const uint32_t* bs = dsmem(sm.bsum, blk);
+        for (int b = (int)B - 1; b >= 0; b--) {
+          const uint32_t v = bs[b];
+          if (ab + v >= k) {
+            bn = blk * B + (uint32_t)b;
+            cn = v;
+            break;
+          }
+          ab += v;
+        }
+        sm.info[4] = round == 0 ? bn : ((pbin << 10) | bn);
+        sm.info[5] = ab;
+        sm.info[6] = cn;
+      }
+      __syncthreads();
+      bin = sm.info[4];
+      above = sm.info[5];
+      cnt = sm.info[6];
+      __syncthreads();
+      if (cnt <= (uint32_t)FNB) break;   // cluster-uniform
+    }
+    // candidates: the keys with (key >> dsh) == bin
+    if (cnt <= (uint32_t)FNB) {   // cluster-uniform
+      uint32_t* cand = dsmem(sm.fh, 0u);
+      uint32_t* ccount = dsmem(&sm.ccount, 0u);
+#pragma unroll 2
+      for (int it = 0; it < IT; it++) {
+        const uint32_t i4 = it * NT + threadIdx.x;
+        const uint32_t j = s0 + 4 * i4;
+        if (j >= L) continue;
+        const uint4 kq = keys4<KIND>(sm.q[i4], j, p, c.id, stage, rrank);
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const uint32_t key = getu(kq, u);
+          if (j + u < L && (key >> dsh) == bin) cand[atomicAdd(ccount, 1u)] = key;
+        }
+      }
+      cluster_sync_all();   // candidates gathered in CTA 0
+      if (crank == 0) {
+        const uint32_t kk2 = k - above;   // rank of the k-th largest inside the bin
+        for (uint32_t a = threadIdx.x; a < cnt; a += NT) {
+          const uint32_t ka = sm.fh[a];
+          uint32_t gt = 0, eq = 0;
+          for (uint32_t b2 = 0; b2 < cnt; b2++) {
+            const uint32_t kb = sm.fh[b2];
+            gt += kb > ka;
+            eq += kb == ka;
+          }
+          if (gt < kk2 && kk2 <= gt + eq) {   // ka is the kk2-th largest (all such threads agree)
+            sm.info[2] = ka;
+            sm.info[3] = kk2 - gt;
+          }
+        }
+      }
+      cluster_sync_all();   // T published by CTA 0
+      if (threadIdx.x == 0) {
+        sm.info[0] = *dsmem(&sm.info[2], 0u);
+        sm.info[1] = *dsmem(&sm.info[3], 0u);
+      }
+      __syncthreads();
+      prefix = sm.info[0];
+      kk = sm.info[1];
+      selected = true;
+      __syncthreads();
+    }
+  }
+  // ---- fallback: radix select of the k-th largest key over the whole unit (cluster)
+  if (!selected) cluster_sync_all();   // peers may still read bsum, which hist / tot alias
+  for (int pass = 0; pass < 4 && !selected; pass++) {
     const int shift = 24 - 8 * pass;
     uint32_t* h = sm.hist[pass & 1];
     if (threadIdx.x < 256) h[threadIdx.x] = 0;
