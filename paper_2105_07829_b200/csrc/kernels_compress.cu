@@ -502,7 +502,8 @@ __device__ void emit_sparse(const CompressParams& p, const DevChunk& c, Smem& sm
       above = sm.info[5];
       cnt = sm.info[6];
       __syncthreads();
-      if (cnt <= (uint32_t)FNB) break;   // cluster-uniform
+      // refine while the bin is large: CTA 0 ranks the candidates in O(C^2 / NT)
+      if (cnt <= 256u) break;   // cluster-uniform
     }
     // candidates: the keys with (key >> dsh) == bin
     if (cnt <= (uint32_t)FNB) {   // cluster-uniform
