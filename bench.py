@@ -124,6 +124,21 @@ def kernel_bytes(chunks, comp, n, rank):
     return {"compress": w, "server": s, "update": u}
 
 
+def ncu_traffic(cfg_name, kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture
+    of the same workload (profiles/*/traffic.json), or None."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "traffic.json")), reverse=True):
+        try:
+            with open(path) as f:
+                v = json.load(f).get(cfg_name, {}).get(kernel)
+            if v:
+                return int(v), os.path.relpath(path, ROOT)
+        except Exception:
+            continue
+    return None, None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -291,6 +306,7 @@ def run_ours(args):
     dom = max(("compress", "server", "update"), key=lambda k: per[k][0])
     peak, peak_src = peaks()
     achieved = kb[dom] / (per[dom][0] * 1e-3) / 1e9
+    traffic, traffic_src = ncu_traffic(args.config, dom) if world == 1 else (None, None)
     kern = {k: {"ms": round(per[k][0], 5), "GB/s": round(kb[k] / max(per[k][0], 1e-9) / 1e6, 1) if k in kb else None,
                 "alg_bytes": kb.get(k)} for k in per if per[k][1]}
 
@@ -342,8 +358,9 @@ def run_ours(args):
                        "l2": "inputs larger than L2 (g, e, m, v, x = %.0f MB per rank)" % (20 * D / 1e6),
                        "parallelism": f"dp{world} (sharded server: all-to-all + all-gather)"},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
-                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
-                         "peak_source": peak_src, "alg_bytes_per_launch": kb[dom]},
+                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "traffic_source": traffic_src, "peak_source": peak_src,
+                         "alg_bytes_per_launch": kb[dom]},
             "kernels": kern,
             "cpu_baseline": cpu,
             "e2e": e2e,
