@@ -192,9 +192,11 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
           a1 = (e0 + 15) & ~15ull;
           d.pofs = (uint32_t)(s0 - a0);
           d.staged = p.stage_payload;
-          if (p.use_ef) tx += nvb;
+          if (p.use_ef) tx += nvb;   // e~ lands in the held stage; Delta is formed in place
           if (d.staged) tx += p.n * (uint32_t)(a1 - a0);
           tx += 16 * p.n;   // each rank's payload head (scale / norm) by bulk copy
+        } else {
+          tx = nvb;         // raw unit: rank 0's fp32 values land in the held stage
         }
         hd.desc[hs] = d;
         mbar_arrive_expect_tx(&hd.fullI[t], tx);
@@ -203,8 +205,10 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
             tma_load_1d(H(hs), p.grad + c.off + sl.start, nvb, &hd.fullI[t]);
             if (p.use_ef && comp) tma_load_1d(IE(t), p.err + c.off + sl.start, nvb, &hd.fullI[t]);
           }
-        } else if (comp) {
-          if (p.use_ef && nvb) tma_load_1d(IE(t), p.err + c.etl + sl.start, nvb, &hd.fullI[t]);
+        } else if (!comp) {
+          if (nvb) tma_load_1d(H(hs), p.recv + c.recv + 4ull * sl.start, nvb, &hd.fullI[t]);
+        } else {
+          if (p.use_ef && nvb) tma_load_1d(H(hs), p.err + c.etl + sl.start, nvb, &hd.fullI[t]);
           for (uint32_t r = 0; r < p.n; r++)
             tma_load_1d(IH(t) + 16 * r, p.recv + r * p.slot_bytes + c.recv, 16, &hd.fullI[t]);
           if (d.staged)
@@ -291,9 +295,11 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
           q = ef ? make_float4(fadd(g4.x, e4.x), fadd(g4.y, e4.y), fadd(g4.z, e4.z), fadd(g4.w, e4.w)) : g4;
         } else if (4 * f < d.len) {
           double acc[4] = {0.0, 0.0, 0.0, 0.0};
-          if (!comp) {   // raw unit: mean of the ranks' fp32 values
+          if (!comp) {   // raw unit: mean of the ranks' fp32 values (rank 0's staged in val)
             for (uint32_t r = 0; r < p.n; r++) {
-              const float4 x4 = load4_masked(reinterpret_cast<const float*>(p.recv + r * p.slot_bytes + d.recv), j, d.L);
+              const float4 x4 = (r == 0 && f < nvec)
+                                    ? val[f]
+                                    : load4_masked(reinterpret_cast<const float*>(p.recv + r * p.slot_bytes + d.recv), j, d.L);
               acc[0] += (double)x4.x;
               acc[1] += (double)x4.y;
               acc[2] += (double)x4.z;
@@ -310,9 +316,9 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
                          : reinterpret_cast<const uint32_t*>(p.recv + d.recv + 4 + (uint64_t)d.start * b / 8);
             const uint32_t field = KIND == C_SIGN ? ((words[f >> 3] >> ((f & 7) * 4)) & 15u)
                                                   : load_field(words, (uint64_t)b * 4 * f, nb);
-            const float unit = fdiv(h, slv);
+            const float unit = KIND == C_SIGN ? 0.f : fdiv(h, slv);
             float4 e4 = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (p.use_ef) e4 = f < nvec ? IE(t)[f] : load4_masked(p.err + d.etl, j, d.L);
+            if (p.use_ef) e4 = f < nvec ? val[f] : load4_masked(p.err + d.etl, j, d.L);
 #pragma unroll
             for (int u = 0; u < 4; u++) {
               float dec;
@@ -335,7 +341,7 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
                                                                (uint64_t)d.start * b / 8);
               const uint32_t field = KIND == C_SIGN ? ((words[f >> 3] >> ((f & 7) * 4)) & 15u)
                                                     : load_field(words, (uint64_t)b * 4 * f, nb);
-              const float unit = fdiv(h, slv);
+              const float unit = KIND == C_SIGN ? 0.f : fdiv(h, slv);
               const double hd64 = (double)h;   // sign: one conversion per rank, not per element
 #pragma unroll
               for (int u = 0; u < 4; u++) {
@@ -353,7 +359,7 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
           }
           if (!comp || p.n != 1) {
             float4 e4 = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (comp && p.use_ef) e4 = f < nvec ? IE(t)[f] : load4_masked(p.err + d.etl, j, d.L);
+            if (comp && p.use_ef) e4 = f < nvec ? val[f] : load4_masked(p.err + d.etl, j, d.L);
             if (j < d.L) q.x = mean_plus(acc[0], p.inv_n, (double)e4.x);
             if (j + 1 < d.L) q.y = mean_plus(acc[1], p.inv_n, (double)e4.y);
             if (j + 2 < d.L) q.z = mean_plus(acc[2], p.inv_n, (double)e4.z);
@@ -477,7 +483,7 @@ static void cstream_geometry(bool server, const StreamParams& p, uint32_t* sie, 
     ebytes = p.use_ef ? slice_bytes : 0;                                              // e
   } else {
     pieces = p.stage_payload ? (uint32_t)((p.n * p.piece_stride + 127) / 128 * 128) : 0;   // payload pieces
-    ebytes = p.use_ef ? slice_bytes : 0;                                              // e~
+    ebytes = 0;                                   // e~ (and raw rank-0 values) land in the held stage
   }
   const uint32_t heads = server ? (16 * p.n + 127) / 128 * 128 : 0;   // payload heads
   *sie = heads + pieces;
