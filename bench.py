@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="C2")
+    ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
+                    help="N>1 transport of the push/pull exchange: NVLink peer stores or NCCL send/recv")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -254,7 +256,8 @@ def run_ours(args):
         dist.broadcast_object_list(obj, src=0)
         nid = obj[0]
     stream = torch.cuda.current_stream(dev)
-    ctx = bpc.context_for(w, rank=rank, world_size=world, device=local, stream=stream.cuda_stream, nccl_id=nid)
+    ctx = bpc.context_for(w, rank=rank, world_size=world, device=local, stream=stream.cuda_stream, nccl_id=nid,
+                          exchange=args.exchange)
     chunks = ctx.chunks()
     grads = [gen_grad_torch(w, rank, s, dev) for s in (1, 2)]
     x = torch.tensor(gen_params(w), device=dev)
@@ -356,7 +359,8 @@ def run_ours(args):
                        "payload_bytes_per_rank": s.payload_total,
                        "compression_rate_vs_fp32": round(4 * d / s.payload_total, 2),
                        "l2": "inputs larger than L2 (g, e, m, v, x = %.0f MB per rank)" % (20 * D / 1e6),
-                       "parallelism": f"dp{world} (sharded server: all-to-all + all-gather)"},
+                       "parallelism": f"dp{world} (sharded server: all-to-all + all-gather)",
+                       "exchange": ctx.exchange if world > 1 else None},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                          "traffic_source": traffic_src, "peak_source": peak_src,

@@ -94,7 +94,19 @@ typedef struct {
   bpc_compressor comp;
   float beta1, beta2, eps, weight_decay;   /* Alg. 5 inputs; weight_decay = lambda (R15) */
   int32_t check_finite;          /* 1: flag non-finite gradients (reported by bpc_sync) */
+  int32_t exchange;              /* bpc_exchange_mode requested for A4/A8 when world_size > 1 */
 } bpc_config;
+
+/* Transport of the exchange steps A4 (push) and A8 (pull), world_size > 1.
+ * BPC_EXCHANGE_P2P: every rank maps its peers' RECV / P / flag buffers with CUDA
+ *   IPC (handles all-gathered over the NCCL communicator at init) and a copy
+ *   kernel stores the payload bytes straight into the peers' buffers over
+ *   NVLink, then releases a per-step epoch into each peer's flag array
+ *   (system scope); the consumer waits on its flags with acquire loads.  If the
+ *   peer mappings cannot be opened, init falls back to BPC_EXCHANGE_NCCL
+ *   (bpc_get_exchange reports what is in use).
+ * BPC_EXCHANGE_NCCL: grouped ncclSend/ncclRecv (all-to-all, all-gather). */
+typedef enum { BPC_EXCHANGE_P2P = 0, BPC_EXCHANGE_NCCL = 1 } bpc_exchange_mode;
 
 typedef struct bpc_ctx bpc_ctx;
 
@@ -161,6 +173,9 @@ bpc_status bpc_buffer(const bpc_ctx* ctx, int32_t which, void** d_ptr, uint64_t*
 /* Synchronous copies of a buffer to / from host memory (bytes must equal its size). */
 bpc_status bpc_copy_state(bpc_ctx* ctx, int32_t which, void* host_dst, uint64_t bytes);
 bpc_status bpc_load_state(bpc_ctx* ctx, int32_t which, const void* host_src, uint64_t bytes);
+/* Exchange transport in use (bpc_exchange_mode; BPC_EXCHANGE_NCCL also when
+ * world_size == 1 or for an external exchange, where no transport runs). */
+bpc_status bpc_get_exchange(const bpc_ctx* ctx, int32_t* mode);
 bpc_status bpc_get_step(const bpc_ctx* ctx, uint32_t* t);
 bpc_status bpc_set_step(bpc_ctx* ctx, uint32_t t);
 

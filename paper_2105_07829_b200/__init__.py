@@ -13,7 +13,8 @@ __all__ = ["Context", "make_config", "plan", "unique_id", "context_for", "BpcErr
            "ChunkInfo", "Config", "PlanSummary"]
 
 
-def context_for(wcfg, *, rank=0, world_size=None, device=0, stream=None, nccl_id=None, check_finite=0):
+def context_for(wcfg, *, rank=0, world_size=None, device=0, stream=None, nccl_id=None, check_finite=0,
+                exchange="p2p"):
     """Build a Context for a workloads.Config (shapes, compressor, hyper-parameters)."""
     from workloads import layout
     import torch
@@ -25,5 +26,5 @@ def context_for(wcfg, *, rank=0, world_size=None, device=0, stream=None, nccl_id
                       rank=rank, device=device, stream=stream, nccl_id=nccl_id, seed=wcfg.seed,
                       chunk_elems=wcfg.chunk_elems, threshold_bytes=wcfg.threshold_bytes, beta1=wcfg.beta1,
                       beta2=wcfg.beta2, eps=wcfg.eps, weight_decay=wcfg.weight_decay,
-                      check_finite=check_finite)
+                      check_finite=check_finite, exchange={"p2p": 0, "nccl": 1}[exchange])
     return Context(cfg)

@@ -20,6 +20,8 @@ STATUS = {0: "ok", 1: "invalid argument", 2: "size mismatch", 3: "empty block", 
           9: "NCCL error", 10: "out of memory"}
 BUF_SEND, BUF_RECV, BUF_P, BUF_WORKER_ERR, BUF_SERVER_ERR, BUF_M, BUF_V = range(7)
 TIMER_NAMES = ("compress", "server", "update", "push", "pull")
+EXCHANGE_P2P, EXCHANGE_NCCL = 0, 1
+EXCHANGE_NAMES = ("p2p", "nccl")
 
 
 class BpcError(RuntimeError):
@@ -40,7 +42,7 @@ class Config(C.Structure):
                 ("tensor_offset", C.POINTER(C.c_uint64)), ("chunk_elems", C.c_uint64),
                 ("size_threshold_bytes", C.c_uint64), ("comp", Compressor), ("beta1", C.c_float),
                 ("beta2", C.c_float), ("eps", C.c_float), ("weight_decay", C.c_float),
-                ("check_finite", C.c_int32)]
+                ("check_finite", C.c_int32), ("exchange", C.c_int32)]
 
 
 class ChunkInfo(C.Structure):
@@ -58,7 +60,7 @@ class PlanSummary(C.Structure):
 EXPORTS = ["bpc_get_unique_id", "bpc_init", "bpc_plan", "bpc_compress", "bpc_aggregate", "bpc_exchange_push",
            "bpc_server", "bpc_exchange_pull", "bpc_step", "bpc_sync", "bpc_finalize", "bpc_get_plan",
            "bpc_get_chunk", "bpc_peer_segment", "bpc_buffer", "bpc_copy_state", "bpc_load_state",
-           "bpc_get_step", "bpc_set_step", "bpc_set_timing", "bpc_get_timing", "bpc_launch_count",
+           "bpc_get_exchange", "bpc_get_step", "bpc_set_step", "bpc_set_timing", "bpc_get_timing", "bpc_launch_count",
            "bpc_status_string", "bpc_last_error"]
 
 _lib = None
@@ -80,7 +82,7 @@ def lib():
             "bpc_peer_segment": [P, C.c_int32, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)],
             "bpc_buffer": [P, C.c_int32, C.POINTER(C.c_void_p), C.POINTER(C.c_uint64)],
             "bpc_copy_state": [P, C.c_int32, P, C.c_uint64], "bpc_load_state": [P, C.c_int32, P, C.c_uint64],
-            "bpc_get_step": [P, C.POINTER(C.c_uint32)], "bpc_set_step": [P, C.c_uint32],
+            "bpc_get_exchange": [P, C.POINTER(C.c_int32)], "bpc_get_step": [P, C.POINTER(C.c_uint32)], "bpc_set_step": [P, C.c_uint32],
             "bpc_set_timing": [P, C.c_int32], "bpc_get_timing": [P, P, P], "bpc_launch_count": [P],
             "bpc_status_string": [C.c_int], "bpc_last_error": [P],
         }
@@ -109,7 +111,7 @@ def unique_id() -> bytes:
 
 def make_config(numels, offsets, comp, *, world_size=1, rank=0, device=0, stream=0, nccl_id=None,
                 seed=0, chunk_elems=1 << 18, threshold_bytes=1 << 20, beta1=0.9, beta2=0.999, eps=1e-6,
-                weight_decay=0.0, check_finite=0):
+                weight_decay=0.0, check_finite=0, exchange=0):
     numel = np.ascontiguousarray(numels, dtype=np.uint64)
     offset = np.ascontiguousarray(offsets, dtype=np.uint64)
     idbuf = (C.c_uint8 * 128).from_buffer_copy(nccl_id) if nccl_id is not None else None
@@ -117,7 +119,7 @@ def make_config(numels, offsets, comp, *, world_size=1, rank=0, device=0, stream
                  seed, len(numel), numel.ctypes.data_as(C.POINTER(C.c_uint64)),
                  offset.ctypes.data_as(C.POINTER(C.c_uint64)), chunk_elems, threshold_bytes,
                  Compressor(comp.kind, comp.k_num, comp.k_den, comp.bits, comp.randk_scaled, comp.use_ef),
-                 beta1, beta2, eps, weight_decay, check_finite)
+                 beta1, beta2, eps, weight_decay, check_finite, exchange)
     cfg._keep = (numel, offset, idbuf)   # keep the arrays alive with the struct
     return cfg
 
@@ -220,6 +222,13 @@ class Context:
     def load_state(self, which: int, data: np.ndarray):
         data = np.ascontiguousarray(data).view(np.uint8)
         _check(lib().bpc_load_state(self.h, which, data.ctypes.data_as(C.c_void_p), data.size), self.h)
+
+    @property
+    def exchange(self) -> str:
+        """Exchange transport in use: "p2p" (NVLink peer stores) or "nccl"."""
+        m = C.c_int32()
+        _check(lib().bpc_get_exchange(self.h, C.byref(m)), self.h)
+        return EXCHANGE_NAMES[m.value]
 
     @property
     def t(self) -> int:

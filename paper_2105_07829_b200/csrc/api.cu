@@ -85,6 +85,8 @@ bpc_status make_plan(const bpc_config* cfg, Plan* P, std::string* err) {
     return fail(BPC_ERR_INVALID_ARGUMENT, "betas must lie in (0, 1)");
   if (!(cfg->eps >= 0.f) || !(cfg->weight_decay >= 0.f))
     return fail(BPC_ERR_INVALID_ARGUMENT, "eps and weight_decay must be >= 0");
+  if (cfg->exchange != BPC_EXCHANGE_P2P && cfg->exchange != BPC_EXCHANGE_NCCL)
+    return fail(BPC_ERR_INVALID_ARGUMENT, "unknown exchange mode");
   uint64_t ce = cfg->chunk_elems ? cfg->chunk_elems : (1ull << 18);
   if (ce < kSlice || ce > 16 * kSlice || (ce & (ce - 1)))
     return fail(BPC_ERR_INVALID_ARGUMENT, "chunk_elems must be a power of two in [2^14, 2^18]");
@@ -214,6 +216,14 @@ struct bpc_ctx {
   uint32_t sepoch = 0;
   int num_sms = 148;
   ncclComm_t comm = nullptr;
+  // peer-memory exchange (BPC_EXCHANGE_P2P): peers' IPC-mapped RECV / P / flags
+  int32_t exchange = BPC_EXCHANGE_NCCL;
+  unsigned long long* d_xflags = nullptr;   // [2n]: push slots [0, n), pull slots [n, 2n)
+  unsigned long long* d_xdone = nullptr;    // [2]: CTA counters of the push / pull copy kernels
+  std::vector<uint8_t*> peer_recv, peer_p;
+  std::vector<unsigned long long*> peer_flags;
+  uint32_t push_epoch = 0, pull_epoch = 0;
+  int push_grid = 1, pull_grid = 1;
   uint32_t t = 1;
   int phase = 0;   // 0 compress, 1 push, 2 server, 3 pull, 4 step
   bool timing = false;
@@ -266,6 +276,13 @@ bpc_status upload(bpc_ctx* ctx, T** dst, const std::vector<T>& src) {
 
 void free_ctx(bpc_ctx* ctx) {
   if (!ctx) return;
+  for (auto* v : {&ctx->peer_recv, &ctx->peer_p})
+    for (int r = 0; r < (int)v->size(); r++)
+      if ((*v)[r] && r != ctx->cfg.rank) cudaIpcCloseMemHandle((*v)[r]);
+  for (int r = 0; r < (int)ctx->peer_flags.size(); r++)
+    if (ctx->peer_flags[r] && r != ctx->cfg.rank) cudaIpcCloseMemHandle(ctx->peer_flags[r]);
+  if (ctx->d_xflags) cudaFree(ctx->d_xflags);
+  if (ctx->d_xdone) cudaFree(ctx->d_xdone);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   for (void* p : {(void*)ctx->e, (void*)ctx->etl, (void*)ctx->m, (void*)ctx->v, (void*)ctx->send,
                   (void*)ctx->pbuf, (void*)ctx->d_chunks, (void*)ctx->d_witems, (void*)ctx->d_sitems,
@@ -279,6 +296,97 @@ void free_ctx(bpc_ctx* ctx) {
     cudaEventDestroy(ev.second.second);
   }
   delete ctx;
+}
+
+// BPC_EXCHANGE_P2P setup (collective over all ranks, after the communicator
+// exists): export RECV, P and the flag array as CUDA IPC handles, all-gather
+// them over NCCL, open the peers' handles, and agree (all-reduce min) that every
+// rank could open all of them.  Any failure leaves the context on NCCL.
+bpc_status setup_p2p(bpc_ctx* ctx) {
+  const int n = ctx->cfg.world_size, rank = ctx->cfg.rank;
+  const Plan& P = ctx->plan;
+  cudaError_t ce;
+  CK(cudaMalloc((void**)&ctx->d_xflags, 16ull * n), "alloc exchange flags");
+  CK(cudaMemset(ctx->d_xflags, 0, 16ull * n), "zero exchange flags");
+  CK(cudaMalloc((void**)&ctx->d_xdone, 16), "alloc exchange counters");
+  CK(cudaMemset(ctx->d_xdone, 0, 16), "zero exchange counters");
+  struct Rec {
+    cudaIpcMemHandle_t h[3];
+    int32_t ok;
+    int32_t pad[3];
+  };
+  Rec mine = {};
+  mine.ok = n <= P2P_MAXJ;
+  void* bufs[3] = {ctx->recv, ctx->pbuf, ctx->d_xflags};
+  for (int i = 0; i < 3 && mine.ok; i++)
+    if (cudaIpcGetMemHandle(&mine.h[i], bufs[i]) != cudaSuccess) mine.ok = 0;
+  (void)cudaGetLastError();
+  uint8_t* d_all = nullptr;
+  int32_t* d_ok = nullptr;
+  CK(cudaMalloc((void**)&d_all, sizeof(Rec) * n), "alloc handle exchange");
+  CK(cudaMalloc((void**)&d_ok, 4), "alloc handle exchange");
+  std::vector<Rec> all(n);
+  bpc_status st = BPC_OK;
+  int32_t ok = 0;
+  do {
+    if ((ce = cudaMemcpy(d_all + sizeof(Rec) * rank, &mine, sizeof(Rec), cudaMemcpyHostToDevice)) != cudaSuccess) {
+      st = cuda_fail(ctx, ce, "handle upload");
+      break;
+    }
+    ncclResult_t r = ncclAllGather(d_all + sizeof(Rec) * rank, d_all, sizeof(Rec), ncclUint8, ctx->comm, ctx->stream);
+    if (r != ncclSuccess || (ce = cudaStreamSynchronize(ctx->stream)) != cudaSuccess) {
+      ctx->err = "IPC handle all-gather failed";
+      st = BPC_ERR_NCCL;
+      break;
+    }
+    if ((ce = cudaMemcpy(all.data(), d_all, sizeof(Rec) * n, cudaMemcpyDeviceToHost)) != cudaSuccess) {
+      st = cuda_fail(ctx, ce, "handle download");
+      break;
+    }
+    ok = 1;
+    for (int q = 0; q < n; q++) ok &= all[q].ok;
+    ctx->peer_recv.assign(n, nullptr);
+    ctx->peer_p.assign(n, nullptr);
+    ctx->peer_flags.assign(n, nullptr);
+    for (int q = 0; q < n && ok; q++) {
+      if (q == rank) continue;
+      void* ptr[3] = {nullptr, nullptr, nullptr};
+      for (int i = 0; i < 3 && ok; i++)
+        if (cudaIpcOpenMemHandle(&ptr[i], all[q].h[i], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) ok = 0;
+      ctx->peer_recv[q] = (uint8_t*)ptr[0];
+      ctx->peer_p[q] = (uint8_t*)ptr[1];
+      ctx->peer_flags[q] = (unsigned long long*)ptr[2];
+    }
+    (void)cudaGetLastError();
+    // every rank must take the same transport
+    if ((ce = cudaMemcpy(d_ok, &ok, 4, cudaMemcpyHostToDevice)) != cudaSuccess) {
+      st = cuda_fail(ctx, ce, "agreement upload");
+      break;
+    }
+    r = ncclAllReduce(d_ok, d_ok, 1, ncclInt32, ncclMin, ctx->comm, ctx->stream);
+    if (r != ncclSuccess || cudaStreamSynchronize(ctx->stream) != cudaSuccess ||
+        cudaMemcpy(&ok, d_ok, 4, cudaMemcpyDeviceToHost) != cudaSuccess) {
+      ctx->err = "transport agreement failed";
+      st = BPC_ERR_NCCL;
+      break;
+    }
+  } while (0);
+  cudaFree(d_all);
+  cudaFree(d_ok);
+  if (st != BPC_OK) return st;
+  if (ok) {
+    ctx->exchange = BPC_EXCHANGE_P2P;
+    ctx->peer_recv[rank] = ctx->recv;
+    ctx->peer_p[rank] = ctx->pbuf;
+    ctx->peer_flags[rank] = ctx->d_xflags;
+    // copy grids: one 32 KB round (512 threads x 4 x 16 B) per CTA, <= 2 CTAs per SM
+    auto grid_for = [&](uint64_t bytes) {
+      return (int)std::max<uint64_t>(1, std::min<uint64_t>(2ull * ctx->num_sms, (bytes + 32767) / 32768));
+    };
+    ctx->push_grid = grid_for(P.send_bytes);
+    ctx->pull_grid = grid_for((uint64_t)(n - 1) * P.seg_bytes[rank]);
+  }
+  return BPC_OK;
 }
 
 CompressParams base_params(bpc_ctx* ctx) {
@@ -481,6 +589,7 @@ bpc_status bpc_init(const bpc_config* cfg, bpc_ctx** out) {
       ctx->comm = nullptr;
       return bail(BPC_ERR_NCCL);
     }
+    if (cfg->exchange == BPC_EXCHANGE_P2P && (s = setup_p2p(ctx)) != BPC_OK) return bail(s);
   }
   *out = ctx;
   return BPC_OK;
@@ -540,15 +649,39 @@ bpc_status bpc_exchange_push(bpc_ctx* ctx) {
     cudaEvent_t b = nullptr;
     timer_begin(ctx, BPC_TIMER_PUSH, &b);
     const uint64_t slot = P.seg_bytes[rank];
-    NK(ncclGroupStart(), "group start");
-    for (int r = 0; r < n; r++) {
-      if (r == rank) continue;
-      if (P.seg_bytes[r]) NK(ncclSend(ctx->send + P.seg_off[r], P.seg_bytes[r], ncclUint8, r, ctx->comm, ctx->stream), "send");
-      if (slot) NK(ncclRecv(ctx->recv + r * slot, slot, ncclUint8, r, ctx->comm, ctx->stream), "recv");
+    if (ctx->exchange == BPC_EXCHANGE_P2P) {
+      // segment r of SEND -> slot `rank` of owner r's RECV (the local one included)
+      P2PParams q = {};
+      for (int r = 0; r < n; r++) {
+        if (!P.seg_bytes[r]) continue;
+        q.src[q.njobs] = ctx->send + P.seg_off[r];
+        q.dst[q.njobs] = ctx->peer_recv[r] + (uint64_t)rank * P.seg_bytes[r];
+        q.len[q.njobs++] = P.seg_bytes[r];
+      }
+      P2PWait w = {};
+      for (int r = 0; r < n; r++) {
+        if (r == rank) continue;
+        q.peer_flag[q.npeers++] = ctx->peer_flags[r];
+        w.slots[w.nslots++] = r;
+      }
+      q.slot = rank;
+      q.epoch = w.epoch = ++ctx->push_epoch;
+      q.done = ctx->d_xdone;
+      w.flags = ctx->d_xflags;
+      CK(launch_p2p_copy(q, ctx->push_grid, ctx->stream), "push copy launch");
+      CK(launch_p2p_wait(w, ctx->stream), "push wait launch");
+      ctx->launches += 2;
+    } else {
+      NK(ncclGroupStart(), "group start");
+      for (int r = 0; r < n; r++) {
+        if (r == rank) continue;
+        if (P.seg_bytes[r]) NK(ncclSend(ctx->send + P.seg_off[r], P.seg_bytes[r], ncclUint8, r, ctx->comm, ctx->stream), "send");
+        if (slot) NK(ncclRecv(ctx->recv + r * slot, slot, ncclUint8, r, ctx->comm, ctx->stream), "recv");
+      }
+      NK(ncclGroupEnd(), "group end");
+      if (slot) CK(cudaMemcpyAsync(ctx->recv + rank * slot, ctx->send + P.seg_off[rank], slot,
+                                   cudaMemcpyDeviceToDevice, ctx->stream), "self copy");
     }
-    NK(ncclGroupEnd(), "group end");
-    if (slot) CK(cudaMemcpyAsync(ctx->recv + rank * slot, ctx->send + P.seg_off[rank], slot,
-                                 cudaMemcpyDeviceToDevice, ctx->stream), "self copy");
     timer_end(ctx, BPC_TIMER_PUSH, b);
   }
   // n == 1: RECV aliases SEND.  n > 1 without a communicator: the caller performed
@@ -618,13 +751,36 @@ bpc_status bpc_exchange_pull(bpc_ctx* ctx) {
     const Plan& P = ctx->plan;
     cudaEvent_t b = nullptr;
     timer_begin(ctx, BPC_TIMER_PULL, &b);
-    NK(ncclGroupStart(), "group start");
-    for (int r = 0; r < n; r++) {
-      if (r == rank) continue;
-      if (P.seg_bytes[rank]) NK(ncclSend(ctx->pbuf + P.seg_off[rank], P.seg_bytes[rank], ncclUint8, r, ctx->comm, ctx->stream), "send");
-      if (P.seg_bytes[r]) NK(ncclRecv(ctx->pbuf + P.seg_off[r], P.seg_bytes[r], ncclUint8, r, ctx->comm, ctx->stream), "recv");
+    if (ctx->exchange == BPC_EXCHANGE_P2P) {
+      // my segment of P -> the same offset of every peer's P
+      P2PParams q = {};
+      P2PWait w = {};
+      for (int r = 0; r < n; r++) {
+        if (r == rank) continue;
+        if (P.seg_bytes[rank]) {
+          q.src[q.njobs] = ctx->pbuf + P.seg_off[rank];
+          q.dst[q.njobs] = ctx->peer_p[r] + P.seg_off[rank];
+          q.len[q.njobs++] = P.seg_bytes[rank];
+        }
+        q.peer_flag[q.npeers++] = ctx->peer_flags[r];
+        w.slots[w.nslots++] = n + r;
+      }
+      q.slot = n + rank;
+      q.epoch = w.epoch = ++ctx->pull_epoch;
+      q.done = ctx->d_xdone + 1;
+      w.flags = ctx->d_xflags;
+      CK(launch_p2p_copy(q, ctx->pull_grid, ctx->stream), "pull copy launch");
+      CK(launch_p2p_wait(w, ctx->stream), "pull wait launch");
+      ctx->launches += 2;
+    } else {
+      NK(ncclGroupStart(), "group start");
+      for (int r = 0; r < n; r++) {
+        if (r == rank) continue;
+        if (P.seg_bytes[rank]) NK(ncclSend(ctx->pbuf + P.seg_off[rank], P.seg_bytes[rank], ncclUint8, r, ctx->comm, ctx->stream), "send");
+        if (P.seg_bytes[r]) NK(ncclRecv(ctx->pbuf + P.seg_off[r], P.seg_bytes[r], ncclUint8, r, ctx->comm, ctx->stream), "recv");
+      }
+      NK(ncclGroupEnd(), "group end");
     }
-    NK(ncclGroupEnd(), "group end");
     timer_end(ctx, BPC_TIMER_PULL, b);
   }
   ctx->phase = 4;
@@ -758,6 +914,12 @@ bpc_status bpc_load_state(bpc_ctx* ctx, int32_t which, const void* host_src, uin
   if (bytes != b) return BPC_ERR_SIZE_MISMATCH;
   CK(cudaStreamSynchronize(ctx->stream), "sync");
   if (b) CK(cudaMemcpy(p, host_src, b, cudaMemcpyHostToDevice), "load state");
+  return BPC_OK;
+}
+
+bpc_status bpc_get_exchange(const bpc_ctx* ctx, int32_t* mode) {
+  if (!ctx || !mode) return BPC_ERR_INVALID_ARGUMENT;
+  *mode = ctx->exchange;
   return BPC_OK;
 }
 

@@ -96,7 +96,29 @@ struct StreamParams {
   uint32_t nstages, stage_a, stage_b;   // ring geometry (set by the launcher)
 };
 
+// peer-memory exchange (kernels_p2p.cu)
+constexpr int P2P_MAXJ = 64;
+struct P2PParams {
+  const uint8_t* src[P2P_MAXJ];
+  uint8_t* dst[P2P_MAXJ];           // local or a peer's IPC-mapped buffer
+  uint64_t len[P2P_MAXJ];           // bytes, multiples of 16
+  int njobs;
+  unsigned long long* peer_flag[P2P_MAXJ];   // peers' flag arrays (IPC-mapped)
+  int npeers;
+  int slot;                         // flag slot this launch releases on every peer
+  uint32_t epoch;
+  unsigned long long* done;         // local CTA counter (monotonic: epoch * grid)
+};
+struct P2PWait {
+  const unsigned long long* flags;  // this rank's flag array
+  int slots[P2P_MAXJ];
+  int nslots;
+  uint32_t epoch;
+};
+
 // host launchers (return the launch error)
+cudaError_t launch_p2p_copy(const P2PParams& p, int grid, cudaStream_t s);
+cudaError_t launch_p2p_wait(const P2PWait& w, cudaStream_t s);
 cudaError_t launch_worker_stream(int kind, const StreamParams& p, int grid, cudaStream_t s);
 cudaError_t launch_server_stream(int kind, const StreamParams& p, int grid, cudaStream_t s);
 cudaError_t launch_update_stream(int kind, const UpdateParams& p, int grid, cudaStream_t s);

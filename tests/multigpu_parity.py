@@ -1,6 +1,7 @@
-"""Real multi-GPU parity: one process per GPU (torchrun), libbpc's NCCL exchange
-(bpc_aggregate), every rank checked against the CPU oracle on the same seeded
-inputs.  Launched by tests/test_gpu_multi.py; prints "RANK <r> OK" per rank."""
+"""Real multi-GPU parity: one process per GPU (torchrun), libbpc's exchange
+(bpc_aggregate; argv[2] = "p2p" NVLink peer stores or "nccl"), every rank
+checked against the CPU oracle on the same seeded inputs.  Launched by
+tests/test_gpu_multi.py; prints "RANK <r> <case> OK" per rank and case."""
 import os
 import sys
 
@@ -36,24 +37,34 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
-    names = sys.argv[1].split(",") if len(sys.argv) > 1 else list(CASES)
+    names = sys.argv[1].split(",") if len(sys.argv) > 1 and sys.argv[1] else list(CASES)
+    exchange = sys.argv[2] if len(sys.argv) > 2 else "p2p"
     for name in names:
         w = Config("mg", "custom", CASES[name], numels=SHAPES, n=world)
         offs, D = layout(w.tensor_numels())
         obj = [bpc.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        ctx = bpc.context_for(w, rank=rank, world_size=world, device=local, nccl_id=obj[0], check_finite=1)
+        ctx = bpc.context_for(w, rank=rank, world_size=world, device=local, nccl_id=obj[0], check_finite=1,
+                              exchange=exchange)
+        assert ctx.exchange == exchange, f"rank {rank}: asked for {exchange}, got {ctx.exchange}"
         x = torch.tensor(gen_params(w), device=dev)
         ocfg = oracle.Cfg.from_workload(w, n=world)
         ost = oracle.State(world, D, gen_params(w))
         lay = ocfg.payload_layout()
         plan = ocfg.plan()
-        for step in (1, 2, 3):
+        # steps 1-3 are checked one by one; steps 4-8 run back to back without a
+        # host sync (ranks drift apart: the exchange's cross-step ordering), then
+        # step 8 is checked
+        dgrads = {step: torch.tensor(gen_grad(w, rank, step), device=dev) for step in range(4, 9)}
+        torch.cuda.synchronize()
+        for step in range(1, 9):
             gs = [gen_grad(w, i, step) for i in range(world)]
             delta, p, _ = oracle.round_(ocfg, ost, np.stack(gs), w.lr)
-            ctx.compress(torch.tensor(gs[rank], device=dev))
+            ctx.compress(dgrads[step] if step in dgrads else torch.tensor(gs[rank], device=dev))
             ctx.aggregate()
             ctx.step(x, w.lr)
+            if step not in (1, 2, 3, 8):
+                continue
             ctx.sync()
             send = ctx.copy_state(bpc.BUF_SEND)
             pb = ctx.copy_state(bpc.BUF_P)

@@ -1,4 +1,4 @@
-"""Multi-GPU parity through NCCL (bpc_aggregate): torchrun one process per GPU
+"""Multi-GPU parity through the NVLink peer-store exchange and NCCL (bpc_aggregate): torchrun one process per GPU
 on 2 (and 4 when present) B200s; every rank's payloads, errors and parameters
 are checked against the CPU oracle (tests/multigpu_parity.py).  Skips when the
 box has a single GPU (the loopback tests cover n > 1 there)."""
@@ -17,8 +17,9 @@ def _ngpus():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
+@pytest.mark.parametrize("exchange", ["p2p", "nccl"])
 @pytest.mark.parametrize("n", [2, 4])
-def test_nccl_parity(n):
+def test_multi_parity(n, exchange):
     if _ngpus() < n:
         pytest.skip(f"needs {n} GPUs")
     import socket
@@ -28,7 +29,7 @@ def test_nccl_parity(n):
     s.close()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(port),
-           os.path.join(ROOT, "tests", "multigpu_parity.py")]
+           os.path.join(ROOT, "tests", "multigpu_parity.py"), "", exchange]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
