@@ -10,7 +10,8 @@
  *                  e~ = Delta - p, push p to each worker. Here every GPU is the server
  *                  of its own shard of chunks ("More Servers"):
  *                  an all-to-all of compressed payloads, the server kernel, then an
- *                  all-gather of the re-compressed p (NCCL over NVLink).
+ *                  all-gather of the re-compressed p, over NVLink peer memory fused
+ *                  into the kernels (default) or NCCL (bpc_exchange_mode).
  *   bpc_step       Alg. 5 lines 12-16 + x update, Adam core
  *                  (R15): g~ = dec(p) decoded inside the update kernel.
  * bpc_aggregate = bpc_exchange_push; bpc_server; bpc_exchange_pull.
@@ -99,12 +100,21 @@ typedef struct {
 
 /* Transport of the exchange steps A4 (push) and A8 (pull), world_size > 1.
  * BPC_EXCHANGE_P2P: every rank maps its peers' RECV / P / flag buffers with CUDA
- *   IPC (handles all-gathered over the NCCL communicator at init) and a copy
- *   kernel stores the payload bytes straight into the peers' buffers over
- *   NVLink, then releases a per-step epoch into each peer's flag array
- *   (system scope); the consumer waits on its flags with acquire loads.  If the
- *   peer mappings cannot be opened, init falls back to BPC_EXCHANGE_NCCL
- *   (bpc_get_exchange reports what is in use).
+ *   IPC (handles all-gathered over the NCCL communicator at init); flags are
+ *   per-step epochs released with system-scope stores and waited on with
+ *   acquire loads inside the kernels.
+ *   - norm-based kinds (NONE, SCALED_SIGN, dithering), fused into the kernels:
+ *     bpc_compress stores each payload straight into its owner's RECV slot
+ *     over NVLink (SEND is not written) and releases the push flags;
+ *     bpc_server waits for every rank's push, writes p into its own P segment
+ *     and releases the pull flags; bpc_step waits for them and bulk-copies
+ *     each chunk's p from its owner's P over NVLink.  bpc_exchange_push/pull
+ *     launch nothing; P holds valid bytes for the owned segment only.
+ *   - sparse kinds (top-k, random-k): bpc_exchange_push/pull run a copy
+ *     kernel that stores the segments into the peers' RECV / P over NVLink and
+ *     releases the flags, then a wait kernel (SEND and P fully valid).
+ *   If the peer mappings cannot be opened on every rank, init falls back to
+ *   BPC_EXCHANGE_NCCL (bpc_get_exchange reports what is in use).
  * BPC_EXCHANGE_NCCL: grouped ncclSend/ncclRecv (all-to-all, all-gather). */
 typedef enum { BPC_EXCHANGE_P2P = 0, BPC_EXCHANGE_NCCL = 1 } bpc_exchange_mode;
 
@@ -112,9 +122,11 @@ typedef struct bpc_ctx bpc_ctx;
 
 /* Buffers a caller may inspect (bpc_buffer / bpc_copy_state / bpc_load_state). */
 typedef enum {
-  BPC_BUF_SEND = 0,        /* worker payloads delta, grouped by owner rank (device) */
+  BPC_BUF_SEND = 0,        /* worker payloads delta, grouped by owner rank (device; not
+                              written by the fused P2P exchange: see RECV) */
   BPC_BUF_RECV = 1,        /* this owner's n received payload slots (device) */
-  BPC_BUF_P = 2,           /* server payloads p, same layout as SEND (device) */
+  BPC_BUF_P = 2,           /* server payloads p, same layout as SEND (device; fused P2P
+                              exchange: only this rank's owned segment) */
   BPC_BUF_WORKER_ERR = 3,  /* e, fp32, flat layout of the gradient */
   BPC_BUF_SERVER_ERR = 4,  /* e~ of the owned chunks, fp32, compact (chunk server_err_offset) */
   BPC_BUF_M = 5,           /* first moment m, flat */

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -389,6 +390,26 @@ bpc_status setup_p2p(bpc_ctx* ctx) {
   return BPC_OK;
 }
 
+// The exchange is fused into the streaming kernels (worker stores into the
+// owners' RECV, server into every rank's P) for the norm-based kinds; the
+// sparse kinds use the copy kernels in bpc_exchange_push / pull.
+bool fused_exchange(const bpc_ctx* ctx) {
+  return ctx->exchange == BPC_EXCHANGE_P2P && stream_worker(ctx->cfg.comp.kind);
+}
+PeerSync peer_sync(const bpc_ctx* ctx) {
+  PeerSync s = {};
+  s.n = (uint32_t)ctx->cfg.world_size;
+  s.self = (uint32_t)ctx->cfg.rank;
+  return s;
+}
+void set_signal(bpc_ctx* ctx, PeerSync* s, int which, uint32_t epoch) {
+  const int n = ctx->cfg.world_size, rank = ctx->cfg.rank;
+  s->done = ctx->d_xdone + which;
+  for (int r = 0; r < n; r++) s->sflag[r] = r == rank ? nullptr : ctx->peer_flags[r];
+  s->sslot = (uint32_t)(which * n + rank);
+  s->sepoch = epoch;
+}
+
 CompressParams base_params(bpc_ctx* ctx) {
   CompressParams p = {};
   p.chunks = ctx->d_chunks;
@@ -516,6 +537,7 @@ bpc_status bpc_init(const bpc_config* cfg, bpc_ctx** out) {
     d.k = ci.k;
     d.id = c;
     d.raw = ci.raw ? 1 : 0;
+    d.owner = ci.owner;
     const bool mine = ci.owner == rank;
     if (!ci.raw) {
       witems.push_back(c);
@@ -621,6 +643,14 @@ bpc_status bpc_compress(bpc_ctx* ctx, const float* d_grad) {
     q.use_ef = ctx->cfg.comp.use_ef;
     q.check_finite = ctx->cfg.check_finite;
     q.flag = ctx->d_flag;
+    q.sync = peer_sync(ctx);
+    if (fused_exchange(ctx)) {   // fused push: payloads go straight to the owners' RECV slots
+      const Plan& P = ctx->plan;
+      q.ndst = (uint32_t)ctx->cfg.world_size;
+      for (int r = 0; r < ctx->cfg.world_size; r++)
+        q.dst[r] = ctx->peer_recv[r] + (uint64_t)ctx->cfg.rank * P.seg_bytes[r];
+      set_signal(ctx, &q.sync, 0, ++ctx->push_epoch);
+    }
     CK(launch_worker_stream(ctx->cfg.comp.kind, q, ctx->num_sms, ctx->stream), "worker stream launch");
   } else {
     CompressParams p = base_params(ctx);
@@ -644,7 +674,7 @@ bpc_status bpc_exchange_push(bpc_ctx* ctx) {
   if (!ctx) return BPC_ERR_INVALID_ARGUMENT;
   if (ctx->phase != 1) return BPC_ERR_BAD_STATE;
   const int n = ctx->cfg.world_size, rank = ctx->cfg.rank;
-  if (n > 1 && ctx->comm) {
+  if (n > 1 && ctx->comm && !fused_exchange(ctx)) {
     const Plan& P = ctx->plan;
     cudaEvent_t b = nullptr;
     timer_begin(ctx, BPC_TIMER_PUSH, &b);
@@ -723,6 +753,22 @@ bpc_status bpc_server(bpc_ctx* ctx) {
     const uint32_t bb = ctx->cfg.comp.kind == BPC_SCALED_SIGN ? 1u : ctx->cfg.comp.bits;
     q.piece_stride = (uint32_t)round_up((uint64_t)kStreamSlice * bb / 8 + 32, 16);
     q.stage_payload = (uint64_t)q.piece_stride * q.n <= 49152 && ctx->cfg.world_size <= 32;
+    q.sync = peer_sync(ctx);
+    if (fused_exchange(ctx)) {   // wait for every rank's push; p stays in the local P; signal
+      q.sync.wflags = ctx->d_xflags;
+      q.sync.wslot0 = 0;
+      q.sync.wepoch = ctx->push_epoch;
+      set_signal(ctx, &q.sync, 1, ++ctx->pull_epoch);
+      if (ctx->n_sslices == 0) {   // owns no chunk: nothing to read or send, only the signal
+        P2PParams e = {};
+        for (int r = 0; r < ctx->cfg.world_size; r++)
+          if (r != ctx->cfg.rank) e.peer_flag[e.npeers++] = ctx->peer_flags[r];
+        e.slot = (int)q.sync.sslot;
+        e.epoch = q.sync.sepoch;
+        e.done = q.sync.done;
+        CK(launch_p2p_copy(e, 1, ctx->stream), "pull signal launch");
+      }
+    }
     CK(launch_server_stream(ctx->cfg.comp.kind, q, ctx->num_sms, ctx->stream), "server stream launch");
   } else {
     CompressParams p = base_params(ctx);
@@ -747,7 +793,7 @@ bpc_status bpc_exchange_pull(bpc_ctx* ctx) {
   if (!ctx) return BPC_ERR_INVALID_ARGUMENT;
   if (ctx->phase != 3) return BPC_ERR_BAD_STATE;
   const int n = ctx->cfg.world_size, rank = ctx->cfg.rank;
-  if (n > 1 && ctx->comm) {
+  if (n > 1 && ctx->comm && !fused_exchange(ctx)) {
     const Plan& P = ctx->plan;
     cudaEvent_t b = nullptr;
     timer_begin(ctx, BPC_TIMER_PULL, &b);
@@ -819,6 +865,13 @@ bpc_status bpc_step(bpc_ctx* ctx, float* d_params, float lr) {
   p.lr = lr;
   p.wd = c.weight_decay;
   p.bits = c.comp.bits;
+  p.sync = peer_sync(ctx);
+  if (fused_exchange(ctx)) {   // wait for every owner's p, then read it from the owner's P
+    p.sync.wflags = ctx->d_xflags;
+    p.sync.wslot0 = (uint32_t)c.world_size;
+    p.sync.wepoch = ctx->pull_epoch;
+    for (int r = 0; r < c.world_size; r++) p.psrc[r] = ctx->peer_p[r];
+  }
   cudaEvent_t b = nullptr;
   timer_begin(ctx, BPC_TIMER_UPDATE, &b);
   if (c.comp.kind == BPC_TOP_K || c.comp.kind == BPC_RANDOM_K)

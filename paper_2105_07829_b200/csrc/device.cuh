@@ -144,6 +144,50 @@ __device__ __forceinline__ void wait_counter(const unsigned long long* p, unsign
   (void)ld_acquire(p);
 }
 
+// ---------------------------------------------------------------- NVLink peer sync
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+// One thread: wait until every other rank released this step's epoch, then
+// order the later bulk (async-proxy) reads of the exchanged bytes after it.
+__device__ __forceinline__ void peer_wait(const PeerSync& s) {
+  if (!s.wflags) return;
+  for (uint32_t r = 0; r < s.n; r++) {
+    if (r == s.self) continue;
+    const unsigned long long* f = s.wflags + s.wslot0 + r;
+    const long long t0 = clock64();
+    for (uint32_t it = 1; ld_relaxed_sys(f) < (unsigned long long)s.wepoch; it++) {
+      __nanosleep(64);
+      if ((it & 63) == 0 && clock64() - t0 > BPC_WATCHDOG_CYCLES)
+        watchdog_fire("peer flag", s.wslot0 + r, 0, ld_relaxed_sys(f), s.wepoch);
+    }
+    (void)ld_acquire_sys(f);
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+// Every thread that stored exchanged bytes runs __threadfence_system(), then a
+// barrier over those threads, then this with `leader` = one of them: the last
+// CTA of the launch releases the epoch to every peer.
+__device__ __forceinline__ void peer_signal(const PeerSync& s, bool leader) {
+  if (!s.done || !leader) return;
+  const unsigned long long prev = atomicAdd(s.done, 1ull);
+  if (prev + 1 == (unsigned long long)s.sepoch * gridDim.x) {
+    __threadfence_system();
+    for (uint32_t r = 0; r < s.n; r++)
+      if (s.sflag[r]) st_release_sys(s.sflag[r] + s.sslot, (unsigned long long)s.sepoch);
+  }
+}
+
 // ---------------------------------------------------------------- exact fp32 ops
 // -fmad=false is also set, these keep every operation a single IEEE op.
 __device__ __forceinline__ float fadd(float a, float b) { return __fadd_rn(a, b); }

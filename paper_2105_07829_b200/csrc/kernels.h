@@ -5,6 +5,23 @@
 
 namespace bpc {
 
+constexpr int P2P_MAXJ = 64;   // max world size of the peer-memory exchange
+
+// Fused NVLink exchange inside a streaming kernel (BPC_EXCHANGE_P2P):
+//  wait   - before its first load of exchanged bytes, the kernel waits until
+//           wflags[wslot0 + r] >= wepoch for every rank r != self (system-scope
+//           acquire of the producers' release);
+//  signal - after its last store, the last CTA releases sepoch into slot sslot
+//           of every peer's flag array (sflag[r], IPC-mapped; null for self).
+struct PeerSync {
+  const unsigned long long* wflags;   // null: no wait
+  uint32_t wslot0, wepoch;
+  unsigned long long* done;           // CTA counter (monotonic: sepoch * grid); null: no signal
+  unsigned long long* sflag[P2P_MAXJ];
+  uint32_t sslot, sepoch;
+  uint32_t n, self;
+};
+
 // one compression unit (chunk) as the kernels see it
 struct DevChunk {
   uint64_t off;    // flat element offset
@@ -15,6 +32,8 @@ struct DevChunk {
   uint32_t k;      // sparse k
   uint32_t id;     // global chunk id (Philox counter word 1)
   uint32_t raw;    // 1 = NONE payload
+  uint32_t owner;  // server rank of the chunk
+  uint32_t pad;
 };
 
 // a piece of a chunk processed by one CTA (raw tiles, update tiles)
@@ -58,6 +77,8 @@ struct UpdateParams {
   float* x;
   float beta1, beta2, omb1, omb2, bc1, bc2, eps, lr, wd;   // bc = 1 / (1 - beta^t), R21
   uint32_t bits;
+  PeerSync sync;          // fused exchange: wait for the owners' p (pull) ...
+  const uint8_t* psrc[P2P_MAXJ];   // ... and read chunk payloads from psrc[owner] (P of each rank)
 };
 
 // a 2^13-element slice of a unit for the streaming worker / server kernels
@@ -94,10 +115,17 @@ struct StreamParams {
   uint32_t stage_payload;   // server: stage the n ranks' payload pieces in smem
   uint32_t piece_stride;    // server: bytes per staged piece
   uint32_t nstages, stage_a, stage_b;   // ring geometry (set by the launcher)
+  // fused exchange (BPC_EXCHANGE_P2P, n > 1):
+  //  worker: ndst = n, the payload of a chunk owned by r goes to dst[r] +
+  //          chunk.recv (slot `rank` of r's RECV, IPC-mapped), then signals push;
+  //  server: waits for every push, stores p to the local P, then signals pull
+  //          (the update kernels read it from there over NVLink).
+  uint8_t* dst[P2P_MAXJ];
+  uint32_t ndst;
+  PeerSync sync;
 };
 
 // peer-memory exchange (kernels_p2p.cu)
-constexpr int P2P_MAXJ = 64;
 struct P2PParams {
   const uint8_t* src[P2P_MAXJ];
   uint8_t* dst[P2P_MAXJ];           // local or a peer's IPC-mapped buffer

@@ -57,6 +57,7 @@ struct CDesc {
   uint32_t nslices, sidx, unit, unit_first;
   uint32_t pofs;       // server: byte offset of the slice's first field inside a staged piece
   uint32_t staged;     // server: payload pieces staged in smem
+  uint32_t owner;      // server rank of the chunk (worker: fused push destination)
 };
 
 struct __align__(128) CHead {
@@ -113,7 +114,11 @@ __device__ __forceinline__ float dither_mag(uint32_t code, float hdr, float unit
   return fmul(cl == 0 ? 0.f : __uint_as_float((uint32_t)(127 - (cmax - (int)cl)) << 23), hdr);
 }
 
-template <int KIND, bool SERVER>
+// FUSED (n > 1, BPC_EXCHANGE_P2P): the worker stores its payloads straight into
+// the owners' RECV slots over NVLink and releases the push flags; the server
+// waits for every rank's push before its first load and releases the pull
+// flags after its last store (the update kernels read p from the owners' P).
+template <int KIND, bool SERVER, bool FUSED>
 __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant__ StreamParams p) {
   extern __shared__ __align__(128) unsigned char sraw[];
   CHead& hd = *reinterpret_cast<CHead*>(sraw);
@@ -150,6 +155,7 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
   // ===================================================== producer
   if (warp == CPROD) {
     if (lane == 0) {
+      if (SERVER && FUSED) peer_wait(p.sync);   // fused exchange: every rank's delta has landed in RECV
       // descriptors of the next slice are loaded before the stage waits, so their
       // latency overlaps the wait instead of delaying the bulk copies
       Slice sl_next = mine ? p.slices[blockIdx.x] : Slice{};
@@ -179,6 +185,7 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
         d.unit_first = sl.unit_first;
         d.pofs = 0;
         d.staged = 0;
+        d.owner = c.owner;
         const uint32_t nvb = (sl.len & ~3u) * 4u;
         const bool comp = sl.nslices > 0;
         uint32_t tx = 0;
@@ -393,24 +400,24 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
       const uint32_t hs = ie % NH;
       const CDesc d = hd.desc[hs];
       const uint32_t L = d.L;
-      uint8_t* pay = p.out + d.pay;
+      // payload destination: worker -> the owner's RECV slot (fused push) or SEND;
+      // server -> the local P
+      uint8_t* const pay = (!SERVER && FUSED) ? p.dst[d.owner] + d.recv : p.out + d.pay;
       const float4* val = H(hs);
       // every slice (raw included) waits for its reducer before the stage is
       // recycled: keeps each mbarrier at most one phase ahead of its waiters
       mbar_wait(&hd.tready[hs], (ie / NH) & 1, 0x5000000u | ie);
       if (d.nslices == 0) {   // raw unit: fp32 payload (worker: g, no EF; server: the mean)
-        float* out = reinterpret_cast<float*>(pay);
 #pragma unroll
         for (int k = 0; k < CK; k++) {
           const uint32_t f = threadIdx.x + k * CCNT;
-          if (4 * f < d.len) store4_masked(out, d.start + 4 * f, L, val[f]);
+          if (4 * f < d.len) store4_masked(reinterpret_cast<float*>(pay), d.start + 4 * f, L, val[f]);
         }
       } else {
         const double total = hd.total[hs];
         float* errp = p.use_ef ? (SERVER ? p.err + d.etl : p.err + d.off) : nullptr;
         if (KIND == C_SIGN) {
           const float sc = __double2float_rn(total / (double)L);
-          uint32_t* words = reinterpret_cast<uint32_t*>(pay + 4);
 #pragma unroll
           for (int k = 0; k < CK; k++) {
             const uint32_t f = threadIdx.x + k * CCNT;
@@ -430,14 +437,13 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
             w |= __shfl_xor_sync(0xffffffffu, w, 1);
             w |= __shfl_xor_sync(0xffffffffu, w, 2);
             w |= __shfl_xor_sync(0xffffffffu, w, 4);
-            if ((lane & 7) == 0 && j < L) words[j >> 5] = w;
+            if ((lane & 7) == 0 && j < L) reinterpret_cast<uint32_t*>(pay + 4)[j >> 5] = w;
           }
           if (d.sidx == 0 && threadIdx.x == 0) *reinterpret_cast<float*>(pay) = sc;
         } else if (KIND == C_LDITHER || KIND == C_NDITHER) {
           const float N = __double2float_rn(sqrt(total));
           const float inv = N != 0.f ? fdiv(slv, N) : 0.f;
           const float unit = fdiv(N, slv);
-          uint32_t* words = reinterpret_cast<uint32_t*>(pay + 4);
           const uint64_t nwords = ((uint64_t)b * L + 31) / 32;
 #pragma unroll
           for (int k = 0; k < CK; k++) {
@@ -462,7 +468,7 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
             }
             const uint32_t wd = warp_pack(field, nb);
             const uint64_t wbase = (uint64_t)(d.start + 4 * (k * CCNT + 32 * warp)) / 32 * b;
-            if (lane < nb && wbase + lane < nwords) words[wbase + lane] = wd;
+            if (lane < nb && wbase + lane < nwords) reinterpret_cast<uint32_t*>(pay + 4)[wbase + lane] = wd;
           }
           if (d.sidx == 0 && threadIdx.x == 0) *reinterpret_cast<float*>(pay) = N;
         }
@@ -472,6 +478,11 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
     }
   }
   if (bad) atomicOr(p.flag, 1u);
+  if (FUSED) {   // fused exchange: release this step's payload bytes to the peers
+    __threadfence_system();
+    cons_sync();
+    peer_signal(p.sync, threadIdx.x == 0);
+  }
 }
 
 // ring geometry for a launch: input-stage size and layout, number of held stages
@@ -515,11 +526,14 @@ static cudaError_t launch_cstream_t(int kind, StreamParams p, int grid, cudaStre
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, fn, p);
   };
+  const bool fused = p.ndst > 0 || p.sync.wflags != nullptr;
   switch (kind) {
-    case C_NONE: return go(cstream_kernel<C_NONE, SERVER>);
-    case C_SIGN: return go(cstream_kernel<C_SIGN, SERVER>);
-    case C_LDITHER: return go(cstream_kernel<C_LDITHER, SERVER>);
-    case C_NDITHER: return go(cstream_kernel<C_NDITHER, SERVER>);
+    case C_NONE: return fused ? go(cstream_kernel<C_NONE, SERVER, true>) : go(cstream_kernel<C_NONE, SERVER, false>);
+    case C_SIGN: return fused ? go(cstream_kernel<C_SIGN, SERVER, true>) : go(cstream_kernel<C_SIGN, SERVER, false>);
+    case C_LDITHER:
+      return fused ? go(cstream_kernel<C_LDITHER, SERVER, true>) : go(cstream_kernel<C_LDITHER, SERVER, false>);
+    case C_NDITHER:
+      return fused ? go(cstream_kernel<C_NDITHER, SERVER, true>) : go(cstream_kernel<C_NDITHER, SERVER, false>);
   }
   return cudaErrorInvalidValue;
 }

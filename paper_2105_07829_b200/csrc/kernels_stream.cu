@@ -42,13 +42,12 @@ constexpr int UK = UTILE / 4 / CNT;         // float4 per consumer thread per ti
 
 struct UDesc {
   uint64_t off;    // flat element offset of the chunk
-  uint64_t pay;    // payload byte offset of the chunk
+  const uint8_t* pay;   // the chunk's payload (local P, or the owner's P over NVLink)
   uint32_t start;  // tile start (chunk-relative)
   uint32_t len;
   uint32_t L;
   uint32_t raw;
   uint32_t pofs;   // byte offset of the tile's first payload field inside the staged piece
-  float hdr;       // scale (sign) / norm (dither)
 };
 
 struct __align__(128) USmem {
@@ -56,6 +55,7 @@ struct __align__(128) USmem {
   float4 v[UST][UTILE / 4];
   float4 x[UST][UTILE / 4];
   float4 pay[UST][UTILE / 4];     // payload piece: raw fp32 tile, or sign / code bits
+  float4 head[UST];               // the payload's first 16 bytes: scale (sign) / norm (dither)
   UDesc desc[UST];
   uint64_t full[UST], empty[UST];
 };
@@ -69,7 +69,9 @@ __device__ __forceinline__ void adam1s(float g, float& m, float& v, float& x, co
   x = fsub(x, fmul(p.lr, fadd(r, fmul(p.wd, x))));             // x update (Adam core)
 }
 
-template <int KIND>
+// FUSED: wait for the owners' p (fused NVLink exchange), then bulk-copy each
+// chunk's payload straight from its owner's P (p.psrc[owner], IPC-mapped)
+template <int KIND, bool FUSED>
 __global__ void __launch_bounds__(SNT, 1) update_stream(const __grid_constant__ UpdateParams p) {
   extern __shared__ __align__(128) unsigned char sraw[];
   USmem& sm = *reinterpret_cast<USmem*>(sraw);
@@ -87,27 +89,27 @@ __global__ void __launch_bounds__(SNT, 1) update_stream(const __grid_constant__ 
   __syncthreads();
   if (warp == CW) {   // ---------------- producer
     if (lane == 0) {
+      if (FUSED) peer_wait(p.sync);   // fused exchange: every owner's p has landed in P
       for (uint32_t i = 0; i < mine; i++) {
         const int s = i % UST;
         if (i >= (uint32_t)UST) mbar_wait(&sm.empty[s], ((i / UST) - 1) & 1);
         const Tile tl = p.tiles[blockIdx.x + i * G];
         const DevChunk c = p.chunks[tl.chunk];
-        const uint8_t* pay = p.pbuf + c.pay;
+        const uint8_t* pay = (FUSED ? p.psrc[c.owner] : p.pbuf) + c.pay;
         const uint32_t nvb = (tl.len & ~3u) * 4u;
         UDesc d;
         d.off = c.off;
-        d.pay = c.pay;
+        d.pay = pay;
         d.start = tl.start;
         d.len = tl.len;
         d.L = c.len;
         d.raw = c.raw;
         const uint8_t* psrc;
-        uint32_t pbytes;
+        uint32_t pbytes, hbytes = 0;
         if (c.raw || KIND == S_NONE) {
           psrc = pay + 4ull * tl.start;
           pbytes = nvb;
           d.pofs = 0;
-          d.hdr = 0.f;
         } else {
           const uint64_t s0 = 4 + (uint64_t)tl.start * b / 8;                  // first field byte
           const uint64_t e0 = 4 + ((uint64_t)(tl.start + tl.len) * b + 7) / 8;  // end byte
@@ -115,10 +117,11 @@ __global__ void __launch_bounds__(SNT, 1) update_stream(const __grid_constant__ 
           psrc = pay + a0;
           pbytes = (uint32_t)(a1 - a0);
           d.pofs = (uint32_t)(s0 - a0);
-          d.hdr = *reinterpret_cast<const float*>(pay);
+          hbytes = 16;
         }
         sm.desc[s] = d;
-        mbar_arrive_expect_tx(&sm.full[s], 3 * nvb + pbytes);
+        mbar_arrive_expect_tx(&sm.full[s], 3 * nvb + pbytes + hbytes);
+        if (hbytes) tma_load_1d(&sm.head[s], pay, 16, &sm.full[s]);
         if (nvb) {
           tma_load_1d(sm.m[s], p.m + c.off + tl.start, nvb, &sm.full[s]);
           tma_load_1d(sm.v[s], p.v + c.off + tl.start, nvb, &sm.full[s]);
@@ -141,7 +144,8 @@ __global__ void __launch_bounds__(SNT, 1) update_stream(const __grid_constant__ 
     float* v = p.v + d.off;
     float* x = p.x + d.off;
     const uint32_t* words = reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(sm.pay[s]) + d.pofs);
-    const float unit = fdiv(d.hdr, sl);
+    const float hdr = *reinterpret_cast<const float*>(&sm.head[s]);
+    const float unit = fdiv(hdr, sl);
 #pragma unroll
     for (int k = 0; k < UK; k++) {
       const uint32_t f = threadIdx.x + k * CNT;   // float4 index inside the tile
@@ -149,9 +153,9 @@ __global__ void __launch_bounds__(SNT, 1) update_stream(const __grid_constant__ 
       const uint32_t j = d.start + 4 * f;
       float4 g4;
       if (d.raw || KIND == S_NONE) {
-        g4 = f < nvec ? sm.pay[s][f] : load4_masked(reinterpret_cast<const float*>(p.pbuf + d.pay), j, d.L);
+        g4 = f < nvec ? sm.pay[s][f] : load4_masked(reinterpret_cast<const float*>(d.pay), j, d.L);
       } else if (KIND == S_SIGN) {
-        const float h = d.hdr;
+        const float h = hdr;
         const uint32_t nib = (words[f >> 3] >> ((f & 7) * 4)) & 15u;
         g4 = make_float4(nib & 1u ? h : -h, nib & 2u ? h : -h, nib & 4u ? h : -h, nib & 8u ? h : -h);
       } else {
@@ -164,7 +168,7 @@ __global__ void __launch_bounds__(SNT, 1) update_stream(const __grid_constant__ 
             mag = fmul((float)(code >> 1), unit);
           } else {
             const uint32_t cl = code >> 1;
-            mag = fmul(cl == 0 ? 0.f : __uint_as_float((uint32_t)(127 - (cmax - (int)cl)) << 23), d.hdr);
+            mag = fmul(cl == 0 ? 0.f : __uint_as_float((uint32_t)(127 - (cmax - (int)cl)) << 23), hdr);
           }
           set(g4, u, (code & 1u) ? mag : -mag);
         }
@@ -209,11 +213,12 @@ cudaError_t launch_update_stream(int kind, const UpdateParams& p, int grid, cuda
     fn<<<g, SNT, sizeof(USmem), st>>>(p);
     return cudaGetLastError();
   };
+  const bool f = p.sync.wflags != nullptr;
   switch (kind) {
-    case S_NONE: return go(update_stream<S_NONE>);
-    case S_SIGN: return go(update_stream<S_SIGN>);
-    case S_LDITHER: return go(update_stream<S_LDITHER>);
-    case S_NDITHER: return go(update_stream<S_NDITHER>);
+    case S_NONE: return f ? go(update_stream<S_NONE, true>) : go(update_stream<S_NONE, false>);
+    case S_SIGN: return f ? go(update_stream<S_SIGN, true>) : go(update_stream<S_SIGN, false>);
+    case S_LDITHER: return f ? go(update_stream<S_LDITHER, true>) : go(update_stream<S_LDITHER, false>);
+    case S_NDITHER: return f ? go(update_stream<S_NDITHER, true>) : go(update_stream<S_NDITHER, false>);
   }
   return cudaErrorInvalidValue;
 }

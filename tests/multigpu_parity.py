@@ -67,6 +67,13 @@ def main():
                 continue
             ctx.sync()
             send = ctx.copy_state(bpc.BUF_SEND)
+            recv = ctx.copy_state(bpc.BUF_RECV)
+            slot = ctx.summary().recv_slot_bytes
+            # the fused exchange (p2p, norm-based kinds) stores payloads straight into the
+            # owners' RECV and never writes SEND
+            check_send = exchange == "nccl" or name in ("topk", "randk")
+            # ... and leaves p in its owner's P (the update kernels read it over NVLink)
+            check_all_p = check_send
             pb = ctx.copy_state(bpc.BUF_P)
             e = f32(ctx.copy_state(bpc.BUF_WORKER_ERR))
             etl = f32(ctx.copy_state(bpc.BUF_SERVER_ERR))
@@ -74,10 +81,17 @@ def main():
             for ci, (ti, off, L, raw) in enumerate(plan):
                 gc = ctx.chunk(ci)
                 po, nb = lay[ci]
-                assert send[gc.payload_offset:gc.payload_offset + nb].tobytes() == delta[rank, po:po + nb].tobytes(), \
-                    f"{name} rank {rank} step {step}: worker payload of chunk {ci} differs"
-                assert pb[gc.payload_offset:gc.payload_offset + nb].tobytes() == p[po:po + nb].tobytes(), \
-                    f"{name} rank {rank} step {step}: server payload of chunk {ci} differs (owner {gc.owner})"
+                if check_send:
+                    assert send[gc.payload_offset:gc.payload_offset + nb].tobytes() == delta[rank, po:po + nb].tobytes(), \
+                        f"{name} rank {rank} step {step}: worker payload of chunk {ci} differs"
+                if gc.owner == rank:   # every rank's delta, as received by this owner
+                    for r in range(world):
+                        got = recv[r * slot + gc.recv_offset:r * slot + gc.recv_offset + nb]
+                        assert got.tobytes() == delta[r, po:po + nb].tobytes(), \
+                            f"{name} rank {rank} step {step}: received payload of rank {r}, chunk {ci} differs"
+                if check_all_p or gc.owner == rank:
+                    assert pb[gc.payload_offset:gc.payload_offset + nb].tobytes() == p[po:po + nb].tobytes(), \
+                        f"{name} rank {rank} step {step}: server payload of chunk {ci} differs (owner {gc.owner})"
                 assert e[off:off + L].tobytes() == ost.e[rank, off:off + L].tobytes(), \
                     f"{name} rank {rank} step {step}: worker error of chunk {ci} differs"
                 if gc.owner == rank and not raw and w.comp.use_ef:
