@@ -48,6 +48,11 @@ constexpr int CNRED = CK * CCW;          // 128-element warp subtrees per slice 
 constexpr int CUNITSL = (1 << 18) / CSL; // max slices per unit (32)
 static_assert(CNRED == 32 || CNRED == 64, "slice tree expects 32 or 64 warp subtrees");
 
+template <bool B>
+struct BoolC {
+  static constexpr bool value = B;
+};
+
 struct CDesc {
   uint64_t off;        // worker: flat element offset of the chunk
   uint64_t pay;        // payload byte offset (SEND / P)
@@ -274,111 +279,198 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
   const uint32_t rng_rank = SERVER ? 0u : p.rank;
   bool bad = false;
 
+  // A slice is FULL when it holds CSL elements of its unit: no bounds checks, no
+  // tail loads (the ragged-tail code runs only for a unit's last slice).
+  // ---------------- produce: q (worker) / Delta (server) of a slice + its warp subtrees
+  auto produce = [&](auto full_tag, uint32_t i, uint32_t t, const CDesc& d, float4* val, bool comp) {
+    constexpr bool FULL = decltype(full_tag)::value;
+    const uint32_t nvec = d.len >> 2;
+#pragma unroll
+    for (int k = 0; k < CK; k++) {
+      const uint32_t f = threadIdx.x + k * CCNT;
+      const uint32_t j = d.start + 4 * f;
+      const bool inv4 = FULL || f < nvec;   // a whole float4 inside the 16-byte bulk copies
+      float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (!SERVER) {
+        const bool ef = p.use_ef && comp;
+        float4 g4 = q, e4 = q;
+        if (inv4) {
+          g4 = val[f];
+          if (ef) e4 = IE(t)[f];
+        } else if (4 * f < d.len) {   // ragged tail (not in the 16-byte bulk copy)
+          g4 = load4_masked(p.grad + d.off, j, d.L);
+          if (ef) e4 = load4_masked(p.err + d.off, j, d.L);
+        }
+        if (p.check_finite) bad |= !(isfinite(g4.x) && isfinite(g4.y) && isfinite(g4.z) && isfinite(g4.w));
+        q = ef ? make_float4(fadd(g4.x, e4.x), fadd(g4.y, e4.y), fadd(g4.z, e4.z), fadd(g4.w, e4.w)) : g4;
+      } else if (FULL || 4 * f < d.len) {
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        if (!comp) {   // raw unit: mean of the ranks' fp32 values (rank 0's staged in val)
+          for (uint32_t r = 0; r < p.n; r++) {
+            const float4 x4 = (r == 0 && inv4)
+                                  ? val[f]
+                                  : load4_masked(reinterpret_cast<const float*>(p.recv + r * p.slot_bytes + d.recv), j, d.L);
+            acc[0] += (double)x4.x;
+            acc[1] += (double)x4.y;
+            acc[2] += (double)x4.z;
+            acc[3] += (double)x4.w;
+          }
+        } else if (p.n == 1) {
+          // n = 1: Delta = fl32(fl64(dec * 1.0) + fl64(e~)) equals the fp32 sum
+          // fl32(dec + e~): the fp64 sum of two fp32 values is exact unless their
+          // exponents differ by more than 29, and then both roundings return the
+          // larger operand.  One fp32 add instead of four conversions.
+          const float h = *reinterpret_cast<const float*>(IH(t));
+          const uint32_t* words =
+              d.staged ? reinterpret_cast<const uint32_t*>(I(t) + d.pofs)
+                       : reinterpret_cast<const uint32_t*>(p.recv + d.recv + 4 + (uint64_t)d.start * b / 8);
+          const uint32_t field = KIND == C_SIGN ? ((words[f >> 3] >> ((f & 7) * 4)) & 15u)
+                                                : load_field(words, (uint64_t)b * 4 * f, nb);
+          const float unit = KIND == C_SIGN ? 0.f : fdiv(h, slv);
+          float4 e4 = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (p.use_ef) e4 = inv4 ? val[f] : load4_masked(p.err + d.etl, j, d.L);
+#pragma unroll
+          for (int u = 0; u < 4; u++) {
+            float dec;
+            if (KIND == C_SIGN) {
+              dec = ((field >> u) & 1u) ? h : -h;
+            } else {
+              const uint32_t code = (field >> (b * u)) & cmask;
+              const float mag = dither_mag<KIND>(code, h, unit, cmax);
+              dec = (code & 1u) ? mag : -mag;
+            }
+            // acc = +0.0 + dec (turns -0 into +0, as the fp64 sum does), then + e~
+            if (FULL || j + u < d.L) set(q, u, fadd(fadd(0.f, dec), get(e4, u)));
+          }
+        } else {
+          for (uint32_t r = 0; r < p.n; r++) {
+            const float h = *reinterpret_cast<const float*>(IH(t) + 16 * r);
+            const uint32_t* words =
+                d.staged ? reinterpret_cast<const uint32_t*>(I(t) + r * p.piece_stride + d.pofs)
+                         : reinterpret_cast<const uint32_t*>(p.recv + r * p.slot_bytes + d.recv + 4 +
+                                                             (uint64_t)d.start * b / 8);
+            const uint32_t field = KIND == C_SIGN ? ((words[f >> 3] >> ((f & 7) * 4)) & 15u)
+                                                  : load_field(words, (uint64_t)b * 4 * f, nb);
+            const float unit = KIND == C_SIGN ? 0.f : fdiv(h, slv);
+            const double hd64 = (double)h;   // sign: one conversion per rank, not per element
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+              double dec;
+              if (KIND == C_SIGN) {
+                dec = ((field >> u) & 1u) ? hd64 : -hd64;
+              } else {
+                const uint32_t code = (field >> (b * u)) & cmask;
+                const float mag = dither_mag<KIND>(code, h, unit, cmax);
+                dec = (double)((code & 1u) ? mag : -mag);
+              }
+              if (FULL || j + u < d.L) acc[u] += dec;
+            }
+          }
+        }
+        if (!comp || p.n != 1) {
+          float4 e4 = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (comp && p.use_ef) e4 = inv4 ? val[f] : load4_masked(p.err + d.etl, j, d.L);
+          if (FULL || j < d.L) q.x = mean_plus(acc[0], p.inv_n, (double)e4.x);
+          if (FULL || j + 1 < d.L) q.y = mean_plus(acc[1], p.inv_n, (double)e4.y);
+          if (FULL || j + 2 < d.L) q.z = mean_plus(acc[2], p.inv_n, (double)e4.z);
+          if (FULL || j + 3 < d.L) q.w = mean_plus(acc[3], p.inv_n, (double)e4.w);
+        }
+      }
+      val[f] = q;
+      if (comp) {
+        const double a = warp_tree(KIND == C_SIGN ? leaf4_abs(q) : leaf4_sq(q));
+        if (lane == 0) hd.red[i & 1][k * CCW + warp] = a;   // subtree of slice elements [128 m, 128 m + 128)
+      }
+    }
+  };
+
+  // ---------------- emit: payload (sign bits / codes / raw fp32) + error of a slice
+  auto emit = [&](auto full_tag, const CDesc& d, const float4* val, uint8_t* pay, double total) {
+    constexpr bool FULL = decltype(full_tag)::value;
+    const uint32_t L = d.L;
+    if (d.nslices == 0) {   // raw unit: fp32 payload (worker: g, no EF; server: the mean)
+#pragma unroll
+      for (int k = 0; k < CK; k++) {
+        const uint32_t f = threadIdx.x + k * CCNT;
+        if (FULL) st4(reinterpret_cast<float*>(pay) + d.start + 4 * f, val[f]);
+        else if (4 * f < d.len) store4_masked(reinterpret_cast<float*>(pay), d.start + 4 * f, L, val[f]);
+      }
+      return;
+    }
+    float* errp = p.use_ef ? (SERVER ? p.err + d.etl : p.err + d.off) : nullptr;
+    if (KIND == C_SIGN) {
+      const float sc = __double2float_rn(total / (double)L);
+#pragma unroll
+      for (int k = 0; k < CK; k++) {
+        const uint32_t f = threadIdx.x + k * CCNT;
+        const uint32_t j = d.start + 4 * f;
+        const float4 q = val[f];
+        uint32_t nib = 0;
+        float4 ev;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const float qu = get(q, u);
+          const bool bit = !(qu < 0.f);
+          if (bit && (FULL || j + u < L)) nib |= 1u << u;
+          set(ev, u, bit ? fsub(qu, sc) : fadd(qu, sc));
+        }
+        if (errp) {
+          if (FULL) st4(errp + j, ev);
+          else if (j < L) store4_masked(errp, j, L, ev);
+        }
+        uint32_t w = nib << (4 * (lane & 7));
+        w |= __shfl_xor_sync(0xffffffffu, w, 1);
+        w |= __shfl_xor_sync(0xffffffffu, w, 2);
+        w |= __shfl_xor_sync(0xffffffffu, w, 4);
+        if ((lane & 7) == 0 && (FULL || j < L)) reinterpret_cast<uint32_t*>(pay + 4)[j >> 5] = w;
+      }
+      if (d.sidx == 0 && threadIdx.x == 0) *reinterpret_cast<float*>(pay) = sc;
+    } else if (KIND == C_LDITHER || KIND == C_NDITHER) {
+      const float N = __double2float_rn(sqrt(total));
+      const float inv = N != 0.f ? fdiv(slv, N) : 0.f;
+      const float unit = fdiv(N, slv);
+      const uint64_t nwords = ((uint64_t)b * L + 31) / 32;
+#pragma unroll
+      for (int k = 0; k < CK; k++) {
+        const uint32_t f = threadIdx.x + k * CCNT;
+        const uint32_t j = d.start + 4 * f;
+        const float4 q = val[f];
+        uint32_t field = 0;
+        if (FULL || j < L) {
+          const uint4 w4 = rng4(p.seed, j >> 2, d.id, p.t, stage_id, rng_rank);
+          float4 ev;
+#pragma unroll
+          for (int u = 0; u < 4; u++) {
+            const uint32_t w = u == 0 ? w4.x : (u == 1 ? w4.y : (u == 2 ? w4.z : w4.w));
+            const float qu = get(q, u);
+            const uint32_t code = KIND == C_LDITHER ? lin_code_c(qu, N, slv, inv, w)
+                                                    : nat_code_c(qu, N, cmax, lmin, w);
+            if (FULL || j + u < L) field |= (code & cmask) << (b * u);
+            const float mag = dither_mag<KIND>(code, N, unit, cmax);
+            set(ev, u, fsub(qu, (code & 1u) ? mag : -mag));
+          }
+          if (errp) {
+            if (FULL) st4(errp + j, ev);
+            else store4_masked(errp, j, L, ev);
+          }
+        }
+        const uint32_t wd = warp_pack(field, nb);
+        const uint64_t wbase = (uint64_t)(d.start + 4 * (k * CCNT + 32 * warp)) / 32 * b;
+        if (lane < nb && (FULL || wbase + lane < nwords)) reinterpret_cast<uint32_t*>(pay + 4)[wbase + lane] = wd;
+      }
+      if (d.sidx == 0 && threadIdx.x == 0) *reinterpret_cast<float*>(pay) = N;
+    }
+  };
+
   for (uint32_t i = 0; i < mine + D; i++) {
     // ---------------- produce slice i
     if (i < mine) {
       const uint32_t hs = i % NH, t = i % CNI;
       mbar_wait(&hd.fullI[t], (i / CNI) & 1, 0x4000000u | i);
       const CDesc d = hd.desc[hs];
-      const uint32_t nvec = d.len >> 2;
       const bool comp = d.nslices > 0;
-      float4* val = H(hs);
-#pragma unroll
-      for (int k = 0; k < CK; k++) {
-        const uint32_t f = threadIdx.x + k * CCNT;
-        const uint32_t j = d.start + 4 * f;
-        float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (!SERVER) {
-          const bool ef = p.use_ef && comp;
-          float4 g4 = q, e4 = q;
-          if (f < nvec) {
-            g4 = val[f];
-            if (ef) e4 = IE(t)[f];
-          } else if (4 * f < d.len) {   // ragged tail (not in the 16-byte bulk copy)
-            g4 = load4_masked(p.grad + d.off, j, d.L);
-            if (ef) e4 = load4_masked(p.err + d.off, j, d.L);
-          }
-          if (p.check_finite) bad |= !(isfinite(g4.x) && isfinite(g4.y) && isfinite(g4.z) && isfinite(g4.w));
-          q = ef ? make_float4(fadd(g4.x, e4.x), fadd(g4.y, e4.y), fadd(g4.z, e4.z), fadd(g4.w, e4.w)) : g4;
-        } else if (4 * f < d.len) {
-          double acc[4] = {0.0, 0.0, 0.0, 0.0};
-          if (!comp) {   // raw unit: mean of the ranks' fp32 values (rank 0's staged in val)
-            for (uint32_t r = 0; r < p.n; r++) {
-              const float4 x4 = (r == 0 && f < nvec)
-                                    ? val[f]
-                                    : load4_masked(reinterpret_cast<const float*>(p.recv + r * p.slot_bytes + d.recv), j, d.L);
-              acc[0] += (double)x4.x;
-              acc[1] += (double)x4.y;
-              acc[2] += (double)x4.z;
-              acc[3] += (double)x4.w;
-            }
-          } else if (p.n == 1) {
-            // n = 1: Delta = fl32(fl64(dec * 1.0) + fl64(e~)) equals the fp32 sum
-            // fl32(dec + e~): the fp64 sum of two fp32 values is exact unless their
-            // exponents differ by more than 29, and then both roundings return the
-            // larger operand.  One fp32 add instead of four conversions.
-            const float h = *reinterpret_cast<const float*>(IH(t));
-            const uint32_t* words =
-                d.staged ? reinterpret_cast<const uint32_t*>(I(t) + d.pofs)
-                         : reinterpret_cast<const uint32_t*>(p.recv + d.recv + 4 + (uint64_t)d.start * b / 8);
-            const uint32_t field = KIND == C_SIGN ? ((words[f >> 3] >> ((f & 7) * 4)) & 15u)
-                                                  : load_field(words, (uint64_t)b * 4 * f, nb);
-            const float unit = KIND == C_SIGN ? 0.f : fdiv(h, slv);
-            float4 e4 = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (p.use_ef) e4 = f < nvec ? val[f] : load4_masked(p.err + d.etl, j, d.L);
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-              float dec;
-              if (KIND == C_SIGN) {
-                dec = ((field >> u) & 1u) ? h : -h;
-              } else {
-                const uint32_t code = (field >> (b * u)) & cmask;
-                const float mag = dither_mag<KIND>(code, h, unit, cmax);
-                dec = (code & 1u) ? mag : -mag;
-              }
-              // acc = +0.0 + dec (turns -0 into +0, as the fp64 sum does), then + e~
-              if (j + u < d.L) set(q, u, fadd(fadd(0.f, dec), get(e4, u)));
-            }
-          } else {
-            for (uint32_t r = 0; r < p.n; r++) {
-              const float h = *reinterpret_cast<const float*>(IH(t) + 16 * r);
-              const uint32_t* words =
-                  d.staged ? reinterpret_cast<const uint32_t*>(I(t) + r * p.piece_stride + d.pofs)
-                           : reinterpret_cast<const uint32_t*>(p.recv + r * p.slot_bytes + d.recv + 4 +
-                                                               (uint64_t)d.start * b / 8);
-              const uint32_t field = KIND == C_SIGN ? ((words[f >> 3] >> ((f & 7) * 4)) & 15u)
-                                                    : load_field(words, (uint64_t)b * 4 * f, nb);
-              const float unit = KIND == C_SIGN ? 0.f : fdiv(h, slv);
-              const double hd64 = (double)h;   // sign: one conversion per rank, not per element
-#pragma unroll
-              for (int u = 0; u < 4; u++) {
-                double dec;
-                if (KIND == C_SIGN) {
-                  dec = ((field >> u) & 1u) ? hd64 : -hd64;
-                } else {
-                  const uint32_t code = (field >> (b * u)) & cmask;
-                  const float mag = dither_mag<KIND>(code, h, unit, cmax);
-                  dec = (double)((code & 1u) ? mag : -mag);
-                }
-                if (j + u < d.L) acc[u] += dec;
-              }
-            }
-          }
-          if (!comp || p.n != 1) {
-            float4 e4 = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (comp && p.use_ef) e4 = f < nvec ? val[f] : load4_masked(p.err + d.etl, j, d.L);
-            if (j < d.L) q.x = mean_plus(acc[0], p.inv_n, (double)e4.x);
-            if (j + 1 < d.L) q.y = mean_plus(acc[1], p.inv_n, (double)e4.y);
-            if (j + 2 < d.L) q.z = mean_plus(acc[2], p.inv_n, (double)e4.z);
-            if (j + 3 < d.L) q.w = mean_plus(acc[3], p.inv_n, (double)e4.w);
-          }
-        }
-        val[f] = q;
-        if (comp) {
-          const double a = warp_tree(KIND == C_SIGN ? leaf4_abs(q) : leaf4_sq(q));
-          if (lane == 0) hd.red[i & 1][k * CCW + warp] = a;   // subtree of slice elements [128 m, 128 m + 128)
-        }
-      }
+      if (d.len == CSL) produce(BoolC<true>{}, i, t, d, H(hs), comp);
+      else produce(BoolC<false>{}, i, t, d, H(hs), comp);
       __syncwarp();
       if (lane == 0) mbar_arrive1(&hd.emptyI[t]);   // input stage consumed by this warp
       cons_sync();                                    // all q written, red complete
@@ -399,80 +491,15 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
       const uint32_t ie = i - D;
       const uint32_t hs = ie % NH;
       const CDesc d = hd.desc[hs];
-      const uint32_t L = d.L;
       // payload destination: worker -> the owner's RECV slot (fused push) or SEND;
       // server -> the local P
       uint8_t* const pay = (!SERVER && FUSED) ? p.dst[d.owner] + d.recv : p.out + d.pay;
-      const float4* val = H(hs);
       // every slice (raw included) waits for its reducer before the stage is
       // recycled: keeps each mbarrier at most one phase ahead of its waiters
       mbar_wait(&hd.tready[hs], (ie / NH) & 1, 0x5000000u | ie);
-      if (d.nslices == 0) {   // raw unit: fp32 payload (worker: g, no EF; server: the mean)
-#pragma unroll
-        for (int k = 0; k < CK; k++) {
-          const uint32_t f = threadIdx.x + k * CCNT;
-          if (4 * f < d.len) store4_masked(reinterpret_cast<float*>(pay), d.start + 4 * f, L, val[f]);
-        }
-      } else {
-        const double total = hd.total[hs];
-        float* errp = p.use_ef ? (SERVER ? p.err + d.etl : p.err + d.off) : nullptr;
-        if (KIND == C_SIGN) {
-          const float sc = __double2float_rn(total / (double)L);
-#pragma unroll
-          for (int k = 0; k < CK; k++) {
-            const uint32_t f = threadIdx.x + k * CCNT;
-            const uint32_t j = d.start + 4 * f;
-            const float4 q = val[f];
-            uint32_t nib = 0;
-            float4 ev;
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-              const float qu = get(q, u);
-              const bool bit = !(qu < 0.f);
-              if (bit && j + u < L) nib |= 1u << u;
-              set(ev, u, bit ? fsub(qu, sc) : fadd(qu, sc));
-            }
-            if (errp && j < L) store4_masked(errp, j, L, ev);
-            uint32_t w = nib << (4 * (lane & 7));
-            w |= __shfl_xor_sync(0xffffffffu, w, 1);
-            w |= __shfl_xor_sync(0xffffffffu, w, 2);
-            w |= __shfl_xor_sync(0xffffffffu, w, 4);
-            if ((lane & 7) == 0 && j < L) reinterpret_cast<uint32_t*>(pay + 4)[j >> 5] = w;
-          }
-          if (d.sidx == 0 && threadIdx.x == 0) *reinterpret_cast<float*>(pay) = sc;
-        } else if (KIND == C_LDITHER || KIND == C_NDITHER) {
-          const float N = __double2float_rn(sqrt(total));
-          const float inv = N != 0.f ? fdiv(slv, N) : 0.f;
-          const float unit = fdiv(N, slv);
-          const uint64_t nwords = ((uint64_t)b * L + 31) / 32;
-#pragma unroll
-          for (int k = 0; k < CK; k++) {
-            const uint32_t f = threadIdx.x + k * CCNT;
-            const uint32_t j = d.start + 4 * f;
-            const float4 q = val[f];
-            uint32_t field = 0;
-            if (j < L) {
-              const uint4 w4 = rng4(p.seed, j >> 2, d.id, p.t, stage_id, rng_rank);
-              float4 ev;
-#pragma unroll
-              for (int u = 0; u < 4; u++) {
-                const uint32_t w = u == 0 ? w4.x : (u == 1 ? w4.y : (u == 2 ? w4.z : w4.w));
-                const float qu = get(q, u);
-                const uint32_t code = KIND == C_LDITHER ? lin_code_c(qu, N, slv, inv, w)
-                                                        : nat_code_c(qu, N, cmax, lmin, w);
-                if (j + u < L) field |= (code & cmask) << (b * u);
-                const float mag = dither_mag<KIND>(code, N, unit, cmax);
-                set(ev, u, fsub(qu, (code & 1u) ? mag : -mag));
-              }
-              if (errp) store4_masked(errp, j, L, ev);
-            }
-            const uint32_t wd = warp_pack(field, nb);
-            const uint64_t wbase = (uint64_t)(d.start + 4 * (k * CCNT + 32 * warp)) / 32 * b;
-            if (lane < nb && wbase + lane < nwords) reinterpret_cast<uint32_t*>(pay + 4)[wbase + lane] = wd;
-          }
-          if (d.sidx == 0 && threadIdx.x == 0) *reinterpret_cast<float*>(pay) = N;
-        }
-      }
+      const double total = hd.total[hs];
+      if (d.len == CSL) emit(BoolC<true>{}, d, H(hs), pay, total);
+      else emit(BoolC<false>{}, d, H(hs), pay, total);
       __syncwarp();
       if (lane == 0) mbar_arrive1(&hd.emptyH[hs]);   // this warp is done with held stage hs
     }
