@@ -101,21 +101,31 @@ static __device__ __noinline__ void watchdog_fire(const char* what, uint32_t a, 
          (int)threadIdx.x, what, a, b, c, d);
   __trap();
 }
+// try_wait with a suspend-time hint: the thread sleeps in hardware until the
+// phase completes or ~hint ns pass, so a waiting warp issues almost nothing
+__device__ __forceinline__ bool mbar_try_sleep(uint64_t* bar, uint32_t parity, uint32_t hint_ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+      " selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(hint_ns)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ long long clock64_v() {   // not hoisted out of the watchdog branch
+  long long c;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+  return c;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, uint32_t tag = 0) {
   if (mbar_try(bar, parity)) return;
-  const long long t0 = clock64();
-  for (uint32_t it = 1; !mbar_try(bar, parity); it++) {
-    if ((it & 63) == 0 && clock64() - t0 > BPC_WATCHDOG_CYCLES)
+  const long long t0 = clock64_v();
+  while (!mbar_try_sleep(bar, parity, 20000u)) {
+    if (clock64_v() - t0 > BPC_WATCHDOG_CYCLES)
       watchdog_fire("mbarrier", tag, parity, (unsigned long long)smem_u32(bar), 0);
-  }
-}
-// spin (with backoff) until *flag >= target; flag is a shared-memory counter
-__device__ __forceinline__ void smem_wait_geq(const uint32_t* flag, uint32_t target, uint32_t tag) {
-  if (*reinterpret_cast<const volatile uint32_t*>(flag) >= target) return;
-  const long long t0 = clock64();
-  for (uint32_t it = 1; *reinterpret_cast<const volatile uint32_t*>(flag) < target; it++) {
-    __nanosleep(64);
-    if ((it & 63) == 0 && clock64() - t0 > BPC_WATCHDOG_CYCLES) watchdog_fire("smem flag", tag, 0, 0, target);
   }
 }
 // gpu-scope release add / acquire load on unit counters (cross-CTA unit reductions)
@@ -135,11 +145,15 @@ __device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long lon
 // spin with relaxed loads (no L1 invalidation per poll), then one acquire
 __device__ __forceinline__ void wait_counter(const unsigned long long* p, unsigned long long target,
                                              uint32_t tag = 0) {
-  const long long t0 = clock64();
-  unsigned long long v;
-  for (uint32_t it = 1; (v = ld_relaxed(p)) < target; it++) {
-    __nanosleep(128);
-    if ((it & 63) == 0 && clock64() - t0 > BPC_WATCHDOG_CYCLES) watchdog_fire("counter", tag, 0, v, target);
+  unsigned long long v = ld_relaxed(p);
+  if (v < target) {
+    const long long t0 = clock64_v();
+    for (uint32_t it = 1; (v = ld_relaxed(p)) < target; it++) {
+      __nanosleep(256);
+      if ((it & 63) == 0) {
+        if (clock64_v() - t0 > BPC_WATCHDOG_CYCLES) watchdog_fire("counter", tag, 0, v, target);
+      }
+    }
   }
   (void)ld_acquire(p);
 }

@@ -26,7 +26,8 @@
 // All CTAs are co-resident (cooperative launch) and every slice's partial is
 // published before its CTA waits on an earlier unit, so the waits cannot
 // deadlock.  Each mbarrier has a single in-order waiter group; the reducers,
-// which run out of order, wait on a monotonic shared-memory counter instead.
+// run out of order (slice i -> reducer i % 4) but each waits on its slice's
+// held-stage barrier, which cannot run a phase ahead of it.
 #include "device.cuh"
 
 namespace bpc {
@@ -67,7 +68,7 @@ struct CDesc {
 
 struct __align__(128) CHead {
   uint64_t fullI[CNI], emptyI[CNI], emptyH[CMAXH], tready[CMAXH];
-  uint32_t produced;   // slices produced so far (monotonic; the reducers wait on it out of order)
+  uint64_t pready[CMAXH];   // slice in held stage s produced (its reducer waits on it)
   CDesc desc[CMAXH];
   double red[2][CNRED];
   double part[CMAXH];
@@ -147,12 +148,12 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
     for (uint32_t s = 0; s < NH; s++) {
       mbar_init(&hd.emptyH[s], CCW);
       mbar_init(&hd.tready[s], 1);
+      mbar_init(&hd.pready[s], 1);
     }
     for (uint32_t t = 0; t < (uint32_t)CNI; t++) {
       mbar_init(&hd.fullI[t], 1);
       mbar_init(&hd.emptyI[t], CCW);
     }
-    hd.produced = 0;
     fence_mbar_init();
   }
   __syncthreads();
@@ -237,8 +238,9 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
   if (warp >= CRED) {
     for (uint32_t i = warp - CRED; i < mine; i += CRW) {
       const uint32_t hs = i % NH;
-      smem_wait_geq(&hd.produced, i + 1, 0x2000000u | i);   // slice i produced
-      __threadfence_block();
+      // slice i produced.  Cannot alias: slice i + NH needs stage hs back, which
+      // needs this reducer's tready arrive for slice i first.
+      mbar_wait(&hd.pready[hs], (i / NH) & 1, 0x2000000u | i);
       const uint32_t ns = hd.desc[hs].nslices;
       if (ns > 1) {
         if (lane == 0) {
@@ -480,10 +482,7 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
                                                  : hd.red[i & 1][lane]);
           if (lane == 0) hd.part[hs] = r;   // the slice's reducer publishes it
         }
-        if (lane == 0) {
-          __threadfence_block();
-          *reinterpret_cast<volatile uint32_t*>(&hd.produced) = i + 1;
-        }
+        if (lane == 0) mbar_arrive1(&hd.pready[hs]);   // release: q and part[hs] visible to the reducer
       }
     }
     // ---------------- emit slice i - D
