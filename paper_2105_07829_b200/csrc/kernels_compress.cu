@@ -20,13 +20,16 @@ namespace bpc {
 
 enum { K_NONE = 0, K_SIGN = 2, K_TOPK = 3, K_RANDK = 4, K_LDITHER = 5, K_NDITHER = 6 };
 
-constexpr int FNB = 1024;   // bins of the sparse kinds' 10-bit key histogram (= candidate capacity)
+constexpr int FNB = 1024;   // bins of the sparse kinds' 10-bit key histogram
+constexpr int FCAP = FNB / 2;   // candidate capacity: CTA 0 keeps (key, index) pairs in fh
+constexpr int SELCAP = 512;     // small-k emit: a CTA's selected (index, value) pairs in bsum / hist
 
 struct __align__(16) Smem {
   float4 q[SLICE / 4];      // the slice of q (worker) or Delta (server)
   union {
     double red[128];        // dense kinds: warp subtree sums
-    uint32_t fh[FNB];       // sparse kinds: 10-bit key histogram (DSMEM), then CTA 0's candidate keys
+    uint32_t fh[FNB];       // sparse kinds: 10-bit key histogram (DSMEM), then CTA 0's candidate
+                            // keys [0, FCAP) and their indices [FCAP, 2 FCAP)
   };
   union {
     uint32_t bsum[FNB];     // sparse: this CTA's share of the cluster-wide histogram (DSMEM)
@@ -37,7 +40,7 @@ struct __align__(16) Smem {
   };
   double part;              // this slice's subtree sum (read through DSMEM)
   double total;             // unit total
-  uint32_t cnt[2];          // (#key > T, #key == T) of this slice (DSMEM)
+  uint32_t cnt[2];          // (#key > T, #key == T) of this slice (DSMEM); small k: cnt[0] = #selected
   uint32_t scan[NWARP + 1];
   uint32_t info[8];
   uint32_t btot;            // sum of bsum (DSMEM)
@@ -425,7 +428,7 @@ __device__ void emit_sparse(const CompressParams& p, const DevChunk& c, Smem& sm
                             uint32_t crank, uint8_t* pay, float* errp, uint32_t stage, uint32_t rrank) {
   const uint32_t L = c.len, k = c.k, cs = p.cs;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint32_t prefix = 0, pmask = 0, kk = k;
+  uint32_t prefix = 0, pmask = 0, kk = k, tie_cut = 0;
   bool selected = false;
   // ---- fast exact select of the k-th largest key over the unit (cluster):
   // (1) 10-bit histogram of the top key bits per slice (plain smem atomics);
@@ -505,8 +508,8 @@ __device__ void emit_sparse(const CompressParams& p, const DevChunk& c, Smem& sm
       // refine while the bin is large: CTA 0 ranks the candidates in O(C^2 / NT)
       if (cnt <= 256u) break;   // cluster-uniform
     }
-    // candidates: the keys with (key >> dsh) == bin
-    if (cnt <= (uint32_t)FNB) {   // cluster-uniform
+    // candidates: the keys with (key >> dsh) == bin, with their unit indices
+    if (cnt <= (uint32_t)FCAP) {   // cluster-uniform
       uint32_t* cand = dsmem(sm.fh, 0u);
       uint32_t* ccount = dsmem(&sm.ccount, 0u);
 #pragma unroll 2
@@ -518,7 +521,11 @@ __device__ void emit_sparse(const CompressParams& p, const DevChunk& c, Smem& sm
 #pragma unroll
         for (int u = 0; u < 4; u++) {
           const uint32_t key = getu(kq, u);
-          if (j + u < L && (key >> dsh) == bin) cand[atomicAdd(ccount, 1u)] = key;
+          if (j + u < L && (key >> dsh) == bin) {
+            const uint32_t slot = atomicAdd(ccount, 1u);
+            cand[slot] = key;
+            cand[FCAP + slot] = j + u;
+          }
         }
       }
       cluster_sync_all();   // candidates gathered in CTA 0
@@ -537,15 +544,27 @@ __device__ void emit_sparse(const CompressParams& p, const DevChunk& c, Smem& sm
             sm.info[3] = kk2 - gt;
           }
         }
+        __syncthreads();
+        // tie cut: the (kk2 - gt)-th smallest index among the candidates equal to T
+        const uint32_t T0 = sm.info[2], need = sm.info[3];
+        for (uint32_t a = threadIdx.x; a < cnt; a += NT) {
+          if (sm.fh[a] != T0) continue;
+          const uint32_t ia = sm.fh[FCAP + a];
+          uint32_t below = 0;
+          for (uint32_t b2 = 0; b2 < cnt; b2++) below += sm.fh[b2] == T0 && sm.fh[FCAP + b2] < ia;
+          if (below + 1 == need) sm.info[7] = ia;
+        }
       }
       cluster_sync_all();   // T published by CTA 0
       if (threadIdx.x == 0) {
         sm.info[0] = *dsmem(&sm.info[2], 0u);
         sm.info[1] = *dsmem(&sm.info[3], 0u);
+        sm.info[4] = *dsmem(&sm.info[7], 0u);
       }
       __syncthreads();
       prefix = sm.info[0];
       kk = sm.info[1];
+      tie_cut = sm.info[4];
       selected = true;
       __syncthreads();
     }
@@ -613,6 +632,74 @@ __device__ void emit_sparse(const CompressParams& p, const DevChunk& c, Smem& sm
     __syncthreads();
   }
   const uint32_t T = prefix;   // the k-th largest key; take kk of the keys equal to T (lowest index)
+  const bool scaled = KIND == K_RANDK && p.randk_scaled;
+  const float scale = (float)((double)L / (double)k);
+  uint32_t* idx_out = reinterpret_cast<uint32_t*>(pay + 8);
+  float* val_out = reinterpret_cast<float*>(pay + 8 + 4ull * k);
+  if (selected && k <= (uint32_t)SELCAP) {   // cluster-uniform
+    // ---- small k: the selected entries are key > T, or key == T at index <= tie_cut.
+    // One pass writes the error and collects this slice's (index, value) pairs in
+    // shared memory (bsum / hist, no longer read by peers); a cluster prefix of the
+    // per-slice counts and a rank by index place them in ascending order.
+    uint32_t* sidx = sm.bsum;
+    float* sval = reinterpret_cast<float*>(sm.bsum) + SELCAP;
+    if (threadIdx.x == 0) sm.cnt[0] = 0;
+    __syncthreads();
+    for (int it = 0; it < IT; it++) {
+      const uint32_t i4 = it * NT + threadIdx.x;
+      const uint32_t j = s0 + 4 * i4;
+      const float4 q = sm.q[i4];
+      float4 ev = q;
+      uint32_t selm = 0;
+      if (j < L) {
+        const uint4 kq = keys4<KIND>(q, j, p, c.id, stage, rrank);
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const uint32_t key = getu(kq, u);
+          if (j + u < L && (key > T || (key == T && j + u <= tie_cut))) selm |= 1u << u;
+        }
+      }
+      const uint32_t nsel = __popc(selm);
+      const uint32_t wsum = __reduce_add_sync(0xffffffffu, nsel);
+      if (wsum) {
+        uint32_t incl = nsel;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        uint32_t base = 0;
+        if (lane == 31) base = atomicAdd(&sm.cnt[0], incl);
+        base = __shfl_sync(0xffffffffu, base, 31);
+        uint32_t pos = base + incl - nsel;
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+          if ((selm >> u) & 1u) {
+            const float qu = get(q, u);
+            const float val = scaled ? fmul(qu, scale) : qu;
+            sidx[pos] = j + u;
+            sval[pos] = val;
+            set(ev, u, fsub(qu, val));
+            pos++;
+          }
+      }
+      if (errp && j < L) store4_masked(errp, j, L, ev);
+    }
+    cluster_sync_all();   // per-slice counts visible
+    uint32_t base = 0;
+    for (uint32_t r = 0; r < crank; r++) base += *dsmem(&sm.cnt[0], r);
+    const uint32_t m = sm.cnt[0];
+    for (uint32_t a = threadIdx.x; a < m; a += NT) {
+      const uint32_t ia = sidx[a];
+      uint32_t rank = 0;
+      for (uint32_t b2 = 0; b2 < m; b2++) rank += sidx[b2] < ia;
+      idx_out[base + rank] = ia;
+      val_out[base + rank] = sval[a];
+    }
+    cluster_arrive_relaxed();   // done with peers' smem; the matching wait is at kernel exit
+    if (crank == 0 && threadIdx.x == 0) *reinterpret_cast<uint64_t*>(pay) = (uint64_t)k;
+    return;
+  }
   // ---- per-slice counts -> cluster prefix
   if (threadIdx.x < 2) sm.cnt[threadIdx.x] = 0;
   __syncthreads();
@@ -655,10 +742,6 @@ __device__ void emit_sparse(const CompressParams& p, const DevChunk& c, Smem& sm
   cluster_arrive_relaxed();   // done with peers' smem; the matching wait is at kernel exit
   const uint32_t take_eq = sm.info[3];
   uint32_t sel_run = sm.info[2], eq_run = 0;
-  uint32_t* idx_out = reinterpret_cast<uint32_t*>(pay + 8);
-  float* val_out = reinterpret_cast<float*>(pay + 8 + 4ull * k);
-  const bool scaled = KIND == K_RANDK && p.randk_scaled;
-  const float scale = (float)((double)L / (double)k);
   // ---- ordered compaction (index ascending) + error write
   for (int it = 0; it < IT; it++) {
     const uint32_t i4 = it * NT + threadIdx.x;
