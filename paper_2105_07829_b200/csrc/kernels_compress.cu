@@ -476,29 +476,44 @@ __device__ void emit_sparse(const CompressParams& p, const DevChunk& c, Smem& sm
       __syncthreads();
       if (lane == 0) atomicAdd(&sm.btot, bt);
       cluster_sync_all();   // block sums visible
-      if (threadIdx.x == 0) {
-        uint32_t ab = above, blk = 0, bn = 0, cn = 0;
-        for (int r = (int)cs - 1; r >= 0; r--) {
-          const uint32_t t = *dsmem(&sm.btot, (uint32_t)r);
-          if (ab + t >= k) {
-            blk = (uint32_t)r;
-            break;
+      if (warp == 0) {
+        // warp-parallel scan from the top: lane l holds block cs-1-l (one DSMEM
+        // round trip), then that block's bins 32 at a time
+        auto incl_scan = [&](uint32_t v) {
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += y;
           }
-          ab += t;
-        }
+          return v;
+        };
+        const uint32_t t = (uint32_t)lane < cs ? *dsmem(&sm.btot, cs - 1 - lane) : 0u;
+        const uint32_t ti = incl_scan(t);
+        const uint32_t hitb = __ballot_sync(0xffffffffu, (uint32_t)lane < cs && above + ti >= k);
+        const int lb = __ffs(hitb) - 1;   // exists: the unit holds >= k keys of this round
+        const uint32_t blk = cs - 1 - (uint32_t)lb;
+        uint32_t ab = above + __shfl_sync(0xffffffffu, ti - t, lb);
         const uint32_t* bs = dsmem(sm.bsum, blk);
-        for (int b = (int)B - 1; b >= 0; b--) {
-          const uint32_t v = bs[b];
-          if (ab + v >= k) {
-            bn = blk * B + (uint32_t)b;
-            cn = v;
+        uint32_t bn = 0, cn = 0;
+        for (int top = (int)B - 1; top >= 0; top -= 32) {
+          const int b = top - lane;
+          const uint32_t v = b >= 0 ? bs[b] : 0u;
+          const uint32_t vi = incl_scan(v);
+          const uint32_t hit = __ballot_sync(0xffffffffu, b >= 0 && ab + vi >= k);
+          if (hit) {
+            const int lh = __ffs(hit) - 1;
+            bn = blk * B + (uint32_t)(top - lh);
+            cn = __shfl_sync(0xffffffffu, v, lh);
+            ab += __shfl_sync(0xffffffffu, vi - v, lh);
             break;
           }
-          ab += v;
+          ab += __shfl_sync(0xffffffffu, vi, 31);
         }
-        sm.info[4] = round == 0 ? bn : ((pbin << 10) | bn);
-        sm.info[5] = ab;
-        sm.info[6] = cn;
+        if (lane == 0) {
+          sm.info[4] = round == 0 ? bn : ((pbin << 10) | bn);
+          sm.info[5] = ab;
+          sm.info[6] = cn;
+        }
       }
       __syncthreads();
       bin = sm.info[4];
