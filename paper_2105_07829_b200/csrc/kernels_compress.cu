@@ -247,18 +247,32 @@ __device__ __forceinline__ void produce_server_sparse(const CompressParams& p, c
   const uint32_t L = c.len, k = c.k;
   const float* et = p.etl + c.etl;
   float* sq = reinterpret_cast<float*>(sm.q);
-#pragma unroll 2
-  for (int it = 0; it < IT; it++) {
-    const uint32_t i4 = it * NT + threadIdx.x;
-    const uint32_t j = s0 + 4 * i4;
-    float4 e4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (p.use_ef && j < L) e4 = load4_masked(et, j, L);
+  auto base = [&](int it, float4 e4) {
     float4 d;
     d.x = mean_plus(0.0, p.inv_n, (double)e4.x);
     d.y = mean_plus(0.0, p.inv_n, (double)e4.y);
     d.z = mean_plus(0.0, p.inv_n, (double)e4.z);
     d.w = mean_plus(0.0, p.inv_n, (double)e4.w);
-    sm.q[i4] = d;
+    sm.q[it * NT + threadIdx.x] = d;
+  };
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (p.use_ef && s0 + SLICE <= L) {
+    // whole slice valid: batches of B iterations keep B 16-byte loads in flight per thread
+    constexpr int B = 8;
+#pragma unroll
+    for (int it0 = 0; it0 < IT; it0 += B) {
+      float4 e4[B];
+#pragma unroll
+      for (int b = 0; b < B; b++) e4[b] = ldg4_stream(et + s0 + 4 * ((it0 + b) * NT + threadIdx.x));
+#pragma unroll
+      for (int b = 0; b < B; b++) base(it0 + b, e4[b]);
+    }
+  } else {
+#pragma unroll 2
+    for (int it = 0; it < IT; it++) {
+      const uint32_t j = s0 + 4 * (it * NT + threadIdx.x);
+      base(it, (p.use_ef && j < L) ? load4_masked(et, j, L) : z);
+    }
   }
   __syncthreads();
   const uint32_t jlo = s0, jhi = min(s0 + (uint32_t)SLICE, L);
