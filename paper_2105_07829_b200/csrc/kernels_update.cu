@@ -17,6 +17,27 @@ __device__ __forceinline__ void adam1(float g, float& m, float& v, float& x, con
   x = fsub(x, fmul(p.lr, fadd(r, fmul(p.wd, x))));             // x update (Adam core)
 }
 
+// first position with a[pos] >= key in the ascending a[0, n): each warp probes 32
+// positions per round (2 dependent loads for n <= 1024 instead of log2 n)
+__device__ __forceinline__ uint32_t warp_lower_bound(const uint32_t* a, uint32_t n, uint32_t key) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t lo = 0, hi = n;   // answer in [lo, hi]
+  while (hi - lo > 32) {
+    const uint32_t step = (hi - lo + 31) / 32;
+    const uint32_t pos = lo + lane * step;
+    const bool below = pos < hi && a[pos] < key;
+    const uint32_t nb = __popc(__ballot_sync(0xffffffffu, below));
+    if (nb == 0) return lo;
+    const uint32_t last = lo + (nb - 1) * step;   // a[last] < key
+    const uint32_t next = lo + nb * step;          // a[next] >= key, or past hi
+    lo = last + 1;
+    if (next < hi) hi = next;
+  }
+  const uint32_t pos = lo + lane;
+  const bool below = pos < hi && a[pos] < key;
+  return lo + __popc(__ballot_sync(0xffffffffu, below));
+}
+
 template <int KIND>
 __global__ void __launch_bounds__(UNT) update_kernel(const __grid_constant__ UpdateParams p) {
   constexpr bool SPARSE = KIND == U_TOPK || KIND == U_RANDK;
@@ -30,27 +51,8 @@ __global__ void __launch_bounds__(UNT) update_kernel(const __grid_constant__ Upd
   float* x = p.x + c.off;
   const bool raw = c.raw != 0;
   const int b = (int)p.bits;
-  if constexpr (SPARSE) {
-    if (!raw) {
-      for (uint32_t i = threadIdx.x; i < UTILE; i += UNT) gts[i] = 0.f;
-      __syncthreads();
-      const uint32_t k = c.k;
-      const uint32_t* idx = reinterpret_cast<const uint32_t*>(pay + 8);
-      const float* val = reinterpret_cast<const float*>(pay + 8 + 4ull * k);
-      uint32_t lo = 0, hi = k;
-      while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (idx[mid] < tl.start) lo = mid + 1; else hi = mid;
-      }
-      for (uint32_t e = lo + threadIdx.x; e < k; e += UNT) {
-        const uint32_t j = idx[e];
-        if (j >= tl.start + tl.len) break;
-        gts[j - tl.start] = val[e];
-      }
-      __syncthreads();
-    }
-  }
-  // full tiles (the common case): unconditional 16-byte loads, 3 * UIT in flight per thread
+  // full tiles (the common case): unconditional 16-byte loads, 3 * UIT in flight per
+  // thread, issued before the sparse payload search so its latency overlaps them
   const bool full = tl.len == UTILE;
   float4 m4[UIT], v4[UIT], x4[UIT];
 #pragma unroll
@@ -65,6 +67,22 @@ __global__ void __launch_bounds__(UNT) update_kernel(const __grid_constant__ Upd
       m4[it] = load4_masked(m, j, L);
       v4[it] = load4_masked(v, j, L);
       x4[it] = load4_masked(x, j, L);
+    }
+  }
+  if constexpr (SPARSE) {
+    if (!raw) {
+      for (uint32_t i = threadIdx.x; i < UTILE; i += UNT) gts[i] = 0.f;
+      __syncthreads();
+      const uint32_t k = c.k;
+      const uint32_t* idx = reinterpret_cast<const uint32_t*>(pay + 8);
+      const float* val = reinterpret_cast<const float*>(pay + 8 + 4ull * k);
+      const uint32_t lo = warp_lower_bound(idx, k, tl.start);
+      for (uint32_t e = lo + threadIdx.x; e < k; e += UNT) {
+        const uint32_t j = idx[e];
+        if (j >= tl.start + tl.len) break;
+        gts[j - tl.start] = val[e];
+      }
+      __syncthreads();
     }
   }
   const float hdr = raw ? 0.f : *reinterpret_cast<const float*>(pay);
