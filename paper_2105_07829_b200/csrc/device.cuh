@@ -128,6 +128,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, uint32
       watchdog_fire("mbarrier", tag, parity, (unsigned long long)smem_u32(bar), 0);
   }
 }
+// poll with a sleep between tries, for waiters off the critical path: a
+// try_wait's own suspend is woken by any barrier traffic in the CTA, so a
+// long wait there keeps issuing instructions the compute warps need
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity, uint32_t ns, uint32_t tag = 0) {
+  if (mbar_try(bar, parity)) return;
+  const long long t0 = clock64_v();
+  for (uint32_t it = 1; !mbar_try(bar, parity); it++) {
+    __nanosleep(ns);
+    if ((it & 63) == 0) {
+      if (clock64_v() - t0 > BPC_WATCHDOG_CYCLES)
+        watchdog_fire("mbarrier", tag, parity, (unsigned long long)smem_u32(bar), 0);
+    }
+  }
+}
 // gpu-scope release add / acquire load on unit counters (cross-CTA unit reductions)
 __device__ __forceinline__ void red_release_add(unsigned long long* p, unsigned long long v) {
   asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");

@@ -82,16 +82,15 @@ __device__ __forceinline__ void cons_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(CCNT) : "memory");
 }
 
-__device__ __forceinline__ uint32_t lin_code_c(float q, float N, float sl, float inv, uint32_t w) {
+// inv = fl32(s / N), or 0 when N = 0: then every q of the unit is +-0, r = 0 and
+// the level is 0 without a branch (N = 0 implies all-zero q: q*q is exact in fp64)
+__device__ __forceinline__ uint32_t lin_code_c(float q, float sl, float inv, uint32_t w) {
   const uint32_t sign = !(q < 0.f);
-  uint32_t level = 0;
-  if (N != 0.f) {
-    const float r = fminf(fmul(fabsf(q), inv), sl);
-    const float l = floorf(r);
-    const float f = fsub(r, l);
-    const float u = (float)(w >> 8) * 0x1p-24f;
-    level = (uint32_t)l + (u < f ? 1u : 0u);
-  }
+  const float r = fminf(fmul(fabsf(q), inv), sl);
+  const float l = floorf(r);
+  const float f = fsub(r, l);
+  const float u = (float)(w >> 8) * 0x1p-24f;
+  const uint32_t level = (uint32_t)l + (u < f ? 1u : 0u);
   return sign | (level << 1);
 }
 __device__ __forceinline__ uint32_t nat_code_c(float q, float N, int cmax, float lmin, uint32_t w) {
@@ -240,7 +239,7 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
       const uint32_t hs = i % NH;
       // slice i produced.  Cannot alias: slice i + NH needs stage hs back, which
       // needs this reducer's tready arrive for slice i first.
-      mbar_wait(&hd.pready[hs], (i / NH) & 1, 0x2000000u | i);
+      mbar_wait_backoff(&hd.pready[hs], (i / NH) & 1, 200, 0x2000000u | i);
       const uint32_t ns = hd.desc[hs].nslices;
       if (ns > 1) {
         if (lane == 0) {
@@ -441,17 +440,22 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
         if (FULL || j < L) {
           const uint4 w4 = rng4(p.seed, j >> 2, d.id, p.t, stage_id, rng_rank);
           float4 ev;
+          uint32_t codes[4];
 #pragma unroll
           for (int u = 0; u < 4; u++) {
             const uint32_t w = u == 0 ? w4.x : (u == 1 ? w4.y : (u == 2 ? w4.z : w4.w));
             const float qu = get(q, u);
-            const uint32_t code = KIND == C_LDITHER ? lin_code_c(qu, N, slv, inv, w)
+            const uint32_t code = KIND == C_LDITHER ? lin_code_c(qu, slv, inv, w)
                                                     : nat_code_c(qu, N, cmax, lmin, w);
             if (FULL || j + u < L) field |= (code & cmask) << (b * u);
-            const float mag = dither_mag<KIND>(code, N, unit, cmax);
-            set(ev, u, fsub(qu, (code & 1u) ? mag : -mag));
+            codes[u] = code;
           }
-          if (errp) {
+          if (errp) {   // e = q - dec (EF runs only); no error arithmetic otherwise
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+              const float mag = dither_mag<KIND>(codes[u], N, unit, cmax);
+              set(ev, u, fsub(get(q, u), (codes[u] & 1u) ? mag : -mag));
+            }
             if (FULL) st4(errp + j, ev);
             else store4_masked(errp, j, L, ev);
           }

@@ -2,6 +2,9 @@
 DRAM bytes) and/or a `--set full` report (.ncu-rep, read with `ncu -i`).
 
 usage: python tools/ncu_summary.py [--launches gpurun_out/launches.csv] [--rep gpurun_out/prof.ncu-rep]
+                                   [--traffic CFG --out profiles/<round>/traffic.json]
+--traffic merges the report's per-launch DRAM bytes (read + write), averaged per
+kernel role (compress / server / update), into the traffic JSON under CFG.
 """
 from __future__ import annotations
 
@@ -95,11 +98,53 @@ def report(path):
     return "\n".join(out)
 
 
+def role(name: str):
+    if "update" in name:
+        return "update"
+    for pat, r in (("stream_kernel<", None), ("compress_kernel<", None)):
+        if pat in name:
+            args = name.split(pat, 1)[1].split(">", 1)[0].replace("(int)", "").replace("(bool)", "")
+            parts = [a.strip() for a in args.split(",")]
+            server = parts[1] in ("1", "true")
+            return "server" if server else "compress"
+    return None
+
+
+def traffic(path):
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    col = {h: i for i, h in enumerate(hdr)}
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    acc = defaultdict(list)
+    for r in rows[2:]:
+        rl = role(r[col["Kernel Name"]])
+        if rl is None:
+            continue
+        b = 0.0
+        for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            b += float(r[col[m]].replace(",", "")) * scale[units[col[m]]]
+        acc[rl].append(b)
+    return {k: int(sum(v) / len(v)) for k, v in acc.items()}
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--launches")
     ap.add_argument("--rep")
+    ap.add_argument("--traffic")
+    ap.add_argument("--out")
     a = ap.parse_args()
+    if a.traffic:
+        import json
+        import os
+        d = json.load(open(a.out)) if a.out and os.path.exists(a.out) else {}
+        d["_source"] = ("ncu --set full --clock-control none captures of `python bench.py --config <C> --steps 5 "
+                        "--warmup 3 --no-e2e --no-cpu`: dram__bytes_read.sum + dram__bytes_write.sum per launch")
+        d[a.traffic] = traffic(a.rep)
+        json.dump(d, open(a.out, "w"), indent=1)
+        print(a.traffic, d[a.traffic])
+        raise SystemExit
     if a.launches:
         print(launches(a.launches))
     if a.rep:
