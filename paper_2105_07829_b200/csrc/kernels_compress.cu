@@ -111,9 +111,28 @@ __device__ __forceinline__ void leaf_to_red(Smem& sm, int it, double leaf) {
   if ((threadIdx.x & 31) == 0) sm.red[it * NWARP + (threadIdx.x >> 5)] = a;
 }
 
+// key of an element for the "k largest keys, lowest index first" selection:
+// top-k: |q| bits (R9); random-k: ~Philox word (k smallest words, R10)
+template <int KIND>
+__device__ __forceinline__ uint4 keys4(float4 q, uint32_t j, const CompressParams& p, uint32_t id,
+                                       uint32_t stage, uint32_t rrank) {
+  if (KIND == K_TOPK) {
+    return make_uint4(__float_as_uint(q.x) & 0x7fffffffu, __float_as_uint(q.y) & 0x7fffffffu,
+                      __float_as_uint(q.z) & 0x7fffffffu, __float_as_uint(q.w) & 0x7fffffffu);
+  } else {
+    const uint4 w = rng4(p.seed, j >> 2, id, p.t, stage, rrank);
+    return make_uint4(~w.x, ~w.y, ~w.z, ~w.w);
+  }
+}
+__device__ __forceinline__ uint32_t getu(const uint4& v, int u) {
+  return u == 0 ? v.x : (u == 1 ? v.y : (u == 2 ? v.z : v.w));
+}
+
 // ---------------------------------------------------------------- producers
-// worker: q = g + e (use_ef) or q = g; slice -> sm.q; leaf sums -> lv
-template <bool L2, bool LEAF>
+// worker: q = g + e (use_ef) or q = g; slice -> sm.q; leaf sums -> sm.red (LEAF);
+// HISTK (top-k / random-k): the round-0 10-bit key histogram of the selection
+// (emit_sparse) is built here, on the fly, instead of in a separate pass
+template <bool L2, bool LEAF, int HISTK = 0>
 __device__ __forceinline__ void produce_worker(const CompressParams& p, const DevChunk& c, Smem& sm,
                                                uint32_t s0) {
   const float* g = p.grad + c.off;
@@ -127,6 +146,16 @@ __device__ __forceinline__ void produce_worker(const CompressParams& p, const De
                               : g4;
     sm.q[it * NT + threadIdx.x] = q;
     if (LEAF) leaf_to_red(sm, it, L2 ? leaf4_sq(q) : leaf4_abs(q));
+    if (HISTK) {
+      constexpr int DSH = HISTK == K_TOPK ? 21 : 22;
+      const uint32_t j = s0 + 4 * (it * NT + threadIdx.x);
+      if (j < L) {
+        const uint4 kq = keys4<HISTK>(q, j, p, c.id, 0u, p.rank);
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+          if (j + u < L) atomicAdd(&sm.fh[(getu(kq, u) >> DSH) & (FNB - 1)], 1u);
+      }
+    }
   };
   const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
   if (s0 + SLICE <= L) {
@@ -420,26 +449,10 @@ __device__ __forceinline__ void emit_dither(const CompressParams& p, const DevCh
   if (crank == 0 && threadIdx.x == 0) *reinterpret_cast<float*>(pay) = N;
 }
 
-// key of an element for the "k largest keys, lowest index first" selection:
-// top-k: |q| bits (R9); random-k: ~Philox word (k smallest words, R10)
-template <int KIND>
-__device__ __forceinline__ uint4 keys4(float4 q, uint32_t j, const CompressParams& p, uint32_t id,
-                                       uint32_t stage, uint32_t rrank) {
-  if (KIND == K_TOPK) {
-    return make_uint4(__float_as_uint(q.x) & 0x7fffffffu, __float_as_uint(q.y) & 0x7fffffffu,
-                      __float_as_uint(q.z) & 0x7fffffffu, __float_as_uint(q.w) & 0x7fffffffu);
-  } else {
-    const uint4 w = rng4(p.seed, j >> 2, id, p.t, stage, rrank);
-    return make_uint4(~w.x, ~w.y, ~w.z, ~w.w);
-  }
-}
-__device__ __forceinline__ uint32_t getu(const uint4& v, int u) {
-  return u == 0 ? v.x : (u == 1 ? v.y : (u == 2 ? v.z : v.w));
-}
-
 template <int KIND>
 __device__ void emit_sparse(const CompressParams& p, const DevChunk& c, Smem& sm, uint32_t s0,
-                            uint32_t crank, uint8_t* pay, float* errp, uint32_t stage, uint32_t rrank) {
+                            uint32_t crank, uint8_t* pay, float* errp, uint32_t stage, uint32_t rrank,
+                            bool prehist) {
   const uint32_t L = c.len, k = c.k, cs = p.cs;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t prefix = 0, pmask = 0, kk = k, tie_cut = 0;
@@ -461,10 +474,13 @@ __device__ void emit_sparse(const CompressParams& p, const DevChunk& c, Smem& sm
     for (int round = 0; round < 2; round++) {
       dsh = DSH - 10 * round;
       const uint32_t pbin = bin;   // round 1: keys with (key >> DSH) == pbin
-      for (uint32_t b = threadIdx.x; b < (uint32_t)FNB; b += NT) sm.fh[b] = 0;
-      __syncthreads();
+      const bool built = round == 0 && prehist;   // round 0 built by the producer
+      if (!built) {
+        for (uint32_t b = threadIdx.x; b < (uint32_t)FNB; b += NT) sm.fh[b] = 0;
+        __syncthreads();
+      }
 #pragma unroll 2
-      for (int it = 0; it < IT; it++) {
+      for (int it = 0; it < IT && !built; it++) {
         const uint32_t i4 = it * NT + threadIdx.x;
         const uint32_t j = s0 + 4 * i4;
         if (j >= L) continue;
@@ -872,10 +888,15 @@ __global__ void __launch_bounds__(NT, 3) compress_kernel(const __grid_constant__
       if (KIND == K_SIGN) emit_sign(c, sm, s0, crank, total, pay, errp);
       else emit_dither<KIND>(p, c, sm, s0, crank, total, pay, errp, stage, rrank);
     } else {
-      if (SERVER) produce_server_sparse(p, c, sm, s0);
-      else produce_worker<false, false>(p, c, sm, s0);
+      if (SERVER) {
+        produce_server_sparse(p, c, sm, s0);
+      } else {
+        for (uint32_t b = threadIdx.x; b < (uint32_t)FNB; b += NT) sm.fh[b] = 0;
+        __syncthreads();
+        produce_worker<false, false, KIND>(p, c, sm, s0);
+      }
       __syncthreads();
-      emit_sparse<KIND>(p, c, sm, s0, crank, pay, errp, stage, rrank);
+      emit_sparse<KIND>(p, c, sm, s0, crank, pay, errp, stage, rrank, !SERVER);
     }
     cluster_wait();   // no CTA exits while a peer may still read its shared memory
   }
