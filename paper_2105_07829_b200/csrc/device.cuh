@@ -172,6 +172,16 @@ __device__ __forceinline__ void wait_counter(const unsigned long long* p, unsign
   (void)ld_acquire(p);
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// The streaming kernels are launched with programmatic stream serialization:
+// a kernel may start (prologue: barrier init) while its predecessor's last CTAs
+// drain.  Every thread waits for the predecessor's completion (and memory)
+// before touching global data, then lets its own successor be scheduled.
+__device__ __forceinline__ void pdl_wait_and_release() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- NVLink peer sync
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");

@@ -156,6 +156,7 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
     fence_mbar_init();
   }
   __syncthreads();
+  pdl_wait_and_release();
 
   // ===================================================== producer
   if (warp == CPROD) {
@@ -549,11 +550,13 @@ static cudaError_t launch_cstream_t(int kind, StreamParams p, int grid, cudaStre
     cfg.blockDim = dim3(CSNT);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute a[1];
+    cudaLaunchAttribute a[2];
     a[0].id = cudaLaunchAttributeCooperative;   // all CTAs co-resident: the unit waits need it
     a[0].val.cooperative = 1;
+    a[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // prologue overlaps the predecessor
+    a[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = a;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, fn, p);
   };
   const bool fused = p.ndst > 0 || p.sync.wflags != nullptr;

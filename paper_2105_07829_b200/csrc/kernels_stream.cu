@@ -87,6 +87,7 @@ __global__ void __launch_bounds__(SNT, 1) update_stream(const __grid_constant__ 
     fence_mbar_init();
   }
   __syncthreads();
+  pdl_wait_and_release();
   if (warp == CW) {   // ---------------- producer
     if (lane == 0) {
       if (FUSED) peer_wait(p.sync);   // fused exchange: every owner's p has landed in P
@@ -209,9 +210,17 @@ cudaError_t launch_update_stream(int kind, const UpdateParams& p, int grid, cuda
   auto go = [&](auto fn) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(USmem));
     if (e != cudaSuccess) return e;
-    const int g = (int)std::min<uint32_t>((uint32_t)grid, p.n_tiles);
-    fn<<<g, SNT, sizeof(USmem), st>>>(p);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)std::min<uint32_t>((uint32_t)grid, p.n_tiles));
+    cfg.blockDim = dim3(SNT);
+    cfg.dynamicSmemBytes = sizeof(USmem);
+    cfg.stream = st;
+    cudaLaunchAttribute a[1];
+    a[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // prologue overlaps the predecessor
+    a[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = a;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, fn, p);
   };
   const bool f = p.sync.wflags != nullptr;
   switch (kind) {
