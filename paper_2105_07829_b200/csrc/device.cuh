@@ -308,6 +308,27 @@ __device__ __forceinline__ uint32_t load_field(const uint32_t* words, uint64_t p
   return (uint32_t)((v >> sh) & mask);
 }
 
+// first position with a[pos] >= key in the ascending a[0, n): each warp probes 32
+// positions per round (2 dependent loads for n <= 1024 instead of log2 n)
+__device__ __forceinline__ uint32_t warp_lower_bound(const uint32_t* a, uint32_t n, uint32_t key) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t lo = 0, hi = n;   // answer in [lo, hi]
+  while (hi - lo > 32) {
+    const uint32_t step = (hi - lo + 31) / 32;
+    const uint32_t pos = lo + lane * step;
+    const bool below = pos < hi && a[pos] < key;
+    const uint32_t nb = __popc(__ballot_sync(0xffffffffu, below));
+    if (nb == 0) return lo;
+    const uint32_t last = lo + (nb - 1) * step;   // a[last] < key
+    const uint32_t next = lo + nb * step;          // a[next] >= key, or past hi
+    lo = last + 1;
+    if (next < hi) hi = next;
+  }
+  const uint32_t pos = lo + lane;
+  const bool below = pos < hi && a[pos] < key;
+  return lo + __popc(__ballot_sync(0xffffffffu, below));
+}
+
 __device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
 __device__ __forceinline__ float4 ldg4_stream(const float* p) {
   float4 r;

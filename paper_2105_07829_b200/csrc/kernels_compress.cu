@@ -45,7 +45,28 @@ struct __align__(16) Smem {
   uint32_t info[8];
   uint32_t btot;            // sum of bsum (DSMEM)
   uint32_t ccount;          // candidates gathered into CTA 0 (DSMEM atomics)
+  uint64_t qbar;            // whole-slice bulk copy of g (worker) / e~ (server) into q
 };
+
+// Thread 0 bulk-copies the whole 64 KB slice src[0, SLICE) into sm.q (TMA,
+// completes on sm.qbar); the caller waits with slice_wait().  The bytes arrive
+// while the threads load the rest of their inputs through registers.
+__device__ __forceinline__ void slice_bulk_load(Smem& sm, const float* src) {
+  if (threadIdx.x == 0) {
+    mbar_init(&sm.qbar, 1);
+    fence_mbar_init();
+    constexpr uint32_t PIECE = SLICE * 4 / 4;
+    mbar_arrive_expect_tx(&sm.qbar, SLICE * 4);
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+      tma_load_1d(reinterpret_cast<uint8_t*>(sm.q) + i * PIECE, reinterpret_cast<const uint8_t*>(src) + i * PIECE,
+                  PIECE, &sm.qbar);
+  }
+}
+__device__ __forceinline__ void slice_wait(Smem& sm) {
+  __syncthreads();   // the barrier's init is visible
+  mbar_wait(&sm.qbar, 0);
+}
 
 size_t compress_smem_bytes() { return sizeof(Smem); }
 
@@ -159,17 +180,27 @@ __device__ __forceinline__ void produce_worker(const CompressParams& p, const De
   };
   const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
   if (s0 + SLICE <= L) {
-    // whole slice valid: batches of B iterations keep 2B 16-byte loads in flight per thread
-    constexpr int B = 4;
+    // whole slice valid: g lands in sm.q by one bulk copy while each thread
+    // loads its e in batches of B (B 16-byte loads in flight), then q = g + e in place
+    slice_bulk_load(sm, g + s0);
+    constexpr int B = 8;
+    float4 e4[B];
+#pragma unroll
+    for (int b = 0; b < B; b++) e4[b] = p.use_ef ? ld4(e + s0 + 4 * (b * NT + threadIdx.x)) : z;
+    slice_wait(sm);
 #pragma unroll
     for (int it0 = 0; it0 < IT; it0 += B) {
-      float4 g4[B], e4[B];
+      float4 en[B];
+      if (it0 + B < IT) {
 #pragma unroll
-      for (int b = 0; b < B; b++) g4[b] = ldg4_stream(g + s0 + 4 * ((it0 + b) * NT + threadIdx.x));
+        for (int b = 0; b < B; b++) en[b] = p.use_ef ? ld4(e + s0 + 4 * ((it0 + B + b) * NT + threadIdx.x)) : z;
+      }
 #pragma unroll
-      for (int b = 0; b < B; b++) e4[b] = p.use_ef ? ld4(e + s0 + 4 * ((it0 + b) * NT + threadIdx.x)) : z;
+      for (int b = 0; b < B; b++) finish(it0 + b, sm.q[(it0 + b) * NT + threadIdx.x], e4[b]);
+      if (it0 + B < IT) {
 #pragma unroll
-      for (int b = 0; b < B; b++) finish(it0 + b, g4[b], e4[b]);
+        for (int b = 0; b < B; b++) e4[b] = en[b];
+      }
     }
   } else {
 #pragma unroll 2
@@ -286,16 +317,11 @@ __device__ __forceinline__ void produce_server_sparse(const CompressParams& p, c
   };
   const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
   if (p.use_ef && s0 + SLICE <= L) {
-    // whole slice valid: batches of B iterations keep B 16-byte loads in flight per thread
-    constexpr int B = 8;
-#pragma unroll
-    for (int it0 = 0; it0 < IT; it0 += B) {
-      float4 e4[B];
-#pragma unroll
-      for (int b = 0; b < B; b++) e4[b] = ldg4_stream(et + s0 + 4 * ((it0 + b) * NT + threadIdx.x));
-#pragma unroll
-      for (int b = 0; b < B; b++) base(it0 + b, e4[b]);
-    }
+    // whole slice valid: e~ lands in sm.q by one bulk copy, Delta formed in place
+    slice_bulk_load(sm, et + s0);
+    slice_wait(sm);
+#pragma unroll 4
+    for (int it = 0; it < IT; it++) base(it, sm.q[it * NT + threadIdx.x]);
   } else {
 #pragma unroll 2
     for (int it = 0; it < IT; it++) {
@@ -310,7 +336,7 @@ __device__ __forceinline__ void produce_server_sparse(const CompressParams& p, c
     const uint8_t* pl = p.recv + r * p.slot_bytes + c.recv;
     const uint32_t* idx = reinterpret_cast<const uint32_t*>(pl + 8);
     const float* val = reinterpret_cast<const float*>(pl + 8 + 4ull * k);
-    const uint32_t lo = lower_bound_u32(idx, k, jlo), hi = lower_bound_u32(idx, k, jhi);
+    const uint32_t lo = warp_lower_bound(idx, k, jlo), hi = warp_lower_bound(idx, k, jhi);
     for (uint32_t e = lo + threadIdx.x; e < hi; e += NT) {
       const uint32_t j = idx[e];
       bool first = true;
