@@ -381,6 +381,60 @@ void orc_adam(uint64_t L, const float* gt, float* m, float* v, float* x, uint32_
   }
 }
 
+/* LANS block update (CLAN, Alg. 5 lines 12-18; the same
+ * step as Alg. 2 lines 8-14), in the paper's order:
+ *   m, v, m~, v~ as in orc_adam (lines 12-15, R16/R21);
+ *   line 16: r = m~ / (sqrt(v~) + eps),  c = g~ / (sqrt(v~) + eps);
+ *   line 17: d~ = phi(||x_b||) [ beta1 (r + lambda x)/||r + lambda x||
+ *                               + (1 - beta1)(c + lambda x)/||c + lambda x|| ];
+ *   line 18: x = x - eta d~.
+ * Reading R22: the three block norms are fp64 pairwise sums (R6)
+ * of the exact fp64 squares of the fp32 values, square-rooted in fp64;
+ * phi(z) = min(max(fl32(||x_b||), alpha_l), alpha_u); the two
+ * per-block coefficients a = fl32(phi * beta1 / ||r + lambda x||) and
+ * b = fl32(phi * (1 - beta1) / ||c + lambda x||) are formed in fp64, and a
+ * zero norm makes its term zero; per element, in fp32,
+ * d = a u + b w and x = x - eta d. */
+void orc_lans_block(uint64_t L, const float* gt, float* m, float* v, float* x, uint32_t t,
+                    float lr, float beta1, float beta2, float eps, float wd, float alpha_l,
+                    float alpha_u) {
+  float omb1 = (float)(1.0 - (double)beta1);
+  float omb2 = (float)(1.0 - (double)beta2);
+  float ibc1 = (float)(1.0 / (1.0 - pow((double)beta1, (double)t)));
+  float ibc2 = (float)(1.0 / (1.0 - pow((double)beta2, (double)t)));
+  float* u = (float*)malloc(sizeof(float) * (size_t)(L ? L : 1));
+  float* w = (float*)malloc(sizeof(float) * (size_t)(L ? L : 1));
+  double* sq = (double*)malloc(sizeof(double) * (size_t)(L ? L : 1));
+  for (uint64_t j = 0; j < L; j++) {
+    float g = gt[j];
+    m[j] = beta1 * m[j] + omb1 * g;                 /* line 12 */
+    v[j] = beta2 * v[j] + omb2 * (g * g);           /* line 13 */
+    float mh = m[j] * ibc1;                         /* line 14 */
+    float vh = v[j] * ibc2;                         /* line 15 */
+    float den = sqrtf(vh) + eps;
+    float r = mh / den;                             /* line 16: r */
+    float c = g / den;                              /* line 16: c */
+    u[j] = r + wd * x[j];                           /* r + lambda x */
+    w[j] = c + wd * x[j];                           /* c + lambda x */
+  }
+  for (uint64_t j = 0; j < L; j++) sq[j] = (double)x[j] * (double)x[j];
+  double nx = sqrt(orc_pairwise_sum(sq, L));
+  for (uint64_t j = 0; j < L; j++) sq[j] = (double)u[j] * (double)u[j];
+  double nu = sqrt(orc_pairwise_sum(sq, L));
+  for (uint64_t j = 0; j < L; j++) sq[j] = (double)w[j] * (double)w[j];
+  double nw = sqrt(orc_pairwise_sum(sq, L));
+  float phi = (float)nx;
+  if (phi < alpha_l) phi = alpha_l;
+  if (phi > alpha_u) phi = alpha_u;
+  float a = nu > 0.0 ? (float)((double)phi * (double)beta1 / nu) : 0.0f;
+  float b = nw > 0.0 ? (float)((double)phi * (1.0 - (double)beta1) / nw) : 0.0f;
+  for (uint64_t j = 0; j < L; j++) {
+    float d = a * u[j] + b * w[j];                  /* line 17 */
+    x[j] = x[j] - lr * d;                           /* line 18 */
+  }
+  free(u); free(w); free(sq);
+}
+
 /* ------------------------------------------------------------------------ */
 int orc_round(const orc_cfg* cfg, uint64_t D, const float* grads, float* e, float* et,
               float* m, float* v, float* x, uint32_t t, float lr,
@@ -405,6 +459,7 @@ int orc_round(const orc_cfg* cfg, uint64_t D, const float* grads, float* e, floa
   float* dec = (float*)malloc(sizeof(float) * maxL);
   double* acc = (double*)malloc(sizeof(double) * maxL);
   float* gt = (float*)malloc(sizeof(float) * maxL);
+  float* gall = cfg->optimizer == 1 ? (float*)calloc((size_t)(D ? D : 1), sizeof(float)) : NULL;
   int err = 0;
 
   /* ---- workers (Alg. 4 lines 5-7; Alg. 3 line 4) */
@@ -444,11 +499,21 @@ int orc_round(const orc_cfg* cfg, uint64_t D, const float* grads, float* e, floa
     if (ef)
       for (uint64_t j = 0; j < L; j++) et[o + j] = q[j] - gt[j];                     /* e~ = Delta - p */
     /* ---- workers: g~ = dec(p), then the adaptive update (Alg. 5 l.12-18) */
-    orc_adam(L, gt, m + o, v + o, x + o, t, lr, cfg->beta1, cfg->beta2, cfg->eps, cfg->weight_decay);
+    if (cfg->optimizer == 1)
+      memcpy(gall + o, gt, sizeof(float) * L);      /* LANS: per-block update after all chunks */
+    else
+      orc_adam(L, gt, m + o, v + o, x + o, t, lr, cfg->beta1, cfg->beta2, cfg->eps, cfg->weight_decay);
     if (gtilde_out) memcpy(gtilde_out + o, gt, sizeof(float) * L);
     off += pb;
   }
 
+  if (!err && cfg->optimizer == 1)                  /* LANS: one block per tensor */
+    for (uint32_t b = 0; b < cfg->num_tensors; b++) {
+      uint64_t o = cfg->offset[b], L = cfg->numel[b];
+      orc_lans_block(L, gall + o, m + o, v + o, x + o, t, lr, cfg->beta1, cfg->beta2, cfg->eps,
+                     cfg->weight_decay, cfg->alpha_l, cfg->alpha_u);
+    }
+  free(gall);
   if (!err && delta_out) memcpy(delta_out, delta, (size_t)(n * total));
   if (!err && p_out) memcpy(p_out, pbuf, (size_t)total);
   free(delta); free(pbuf); free(q); free(dec); free(acc); free(gt); free(ch);

@@ -50,6 +50,8 @@ typedef struct {
   uint64_t threshold_bytes;      /* PAPER.md:505 size threshold (R3) */
   orc_comp comp;
   float beta1, beta2, eps, weight_decay;   /* Alg. 5 inputs, R15 */
+  int32_t optimizer;             /* 0: Adam core (R15); 1: LANS block-normalised update (R22) */
+  float alpha_l, alpha_u;        /* LANS: phi = clamp(., alpha_l, alpha_u) */
 } orc_cfg;
 
 typedef struct {
@@ -94,6 +96,11 @@ int orc_round(const orc_cfg* cfg, uint64_t D, const float* grads, float* e, floa
 void orc_push_pull(uint32_t n, uint64_t D, const float* grads, float* out);
 
 /* Alg. 5 lines 12-15 + x update (Adam core, R15/R16) on one vector. */
+/* LANS / CLAN update of one block G_b (Alg. 5 lines 12-18, PAPER.md:285-295;
+ * Alg. 2), reading R22. */
+void orc_lans_block(uint64_t L, const float* gtilde, float* m, float* v, float* x, uint32_t t,
+                    float lr, float beta1, float beta2, float eps, float wd, float alpha_l,
+                    float alpha_u);
 void orc_adam(uint64_t L, const float* gtilde, float* m, float* v, float* x, uint32_t t,
               float lr, float beta1, float beta2, float eps, float weight_decay);
 
