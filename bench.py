@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
                     help="N>1 transport of the push/pull exchange: NVLink peer stores or NCCL send/recv")
+    ap.add_argument("--optimizer", choices=["adam", "lans"], default="adam",
+                    help="bpc_step update: Adam core (A9) or the LANS / CLAN block-normalised update (NEXT #1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -108,8 +110,10 @@ class Clocks:
 
 
 # ---------------------------------------------------------------- byte models
-def kernel_bytes(chunks, comp, n, rank):
-    """Algorithmic HBM bytes per launch of each kernel."""
+def kernel_bytes(chunks, comp, n, rank, lans=False):
+    """Algorithmic HBM bytes per launch of each kernel; LANS's
+    update = pass 1 (m, v, x read, m, v written) + pass 2 (m, v, x read, x
+    written) + the payload read twice."""
     ef = comp.use_ef
     w = s = u = 0
     for c in chunks:
@@ -118,12 +122,12 @@ def kernel_bytes(chunks, comp, n, rank):
             w += 8 * L
             if c.owner == rank:
                 s += 4 * n * L + 4 * L
-            u += 24 * L + 4 * L
+            u += (36 * L + 8 * L) if lans else (24 * L + 4 * L)
         else:
             w += (12 if ef else 4) * L + pb
             if c.owner == rank:
                 s += n * pb + (8 * L if ef else 0) + pb
-            u += 24 * L + pb
+            u += (36 * L + 2 * pb) if lans else (24 * L + pb)
     return {"compress": w, "server": s, "update": u}
 
 
@@ -194,7 +198,7 @@ def run_reference(args):
     budget = max(4096.0, 60.0 * rate / max(1, args.steps + args.warmup) / n)
     s = max(1, int(np.ceil(d_full / budget)))
     w = config(args.config, n=n, scale=s, threshold_bytes=full.threshold_bytes // s,
-               chunk_elems=max(1, full.chunk_elems // s))
+               chunk_elems=max(1, full.chunk_elems // s), optimizer=args.optimizer)
     oracle.build()
     numels = w.tensor_numels()
     offs, D = layout(numels)
@@ -247,7 +251,7 @@ def run_ours(args):
     import paper_2105_07829_b200 as bpc
     from workloads import config, gen_grad_torch, gen_params, layout
 
-    w = config(args.config, n=world)
+    w = config(args.config, n=world, optimizer=args.optimizer)
     numels = w.tensor_numels()
     offs, D = layout(numels)
     d = sum(numels)
@@ -305,7 +309,7 @@ def run_ours(args):
     barrier()
     tim = ctx.timing()
     ctx.set_timing(False)
-    kb = kernel_bytes(chunks, w.comp, world, rank)
+    kb = kernel_bytes(chunks, w.comp, world, rank, lans=args.optimizer == "lans")
     per = {k: (tim[k][0] / max(1, tim[k][1]), tim[k][1]) for k in ("compress", "server", "update", "push", "pull")}
     dom = max(("compress", "server", "update"), key=lambda k: per[k][0])
     peak, peak_src = peaks()
@@ -394,7 +398,8 @@ def run_ours(args):
                        "compression_rate_vs_fp32": round(4 * d / s.payload_total, 2),
                        "l2": "inputs larger than L2 (g, e, m, v, x = %.0f MB per rank)" % (20 * D / 1e6),
                        "parallelism": f"dp{world} (sharded server: all-to-all + all-gather)",
-                       "exchange": ctx.exchange if world > 1 else None},
+                       "exchange": ctx.exchange if world > 1 else None,
+                       "optimizer": args.optimizer},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                          "traffic_source": traffic_src, "peak_source": peak_src,

@@ -96,7 +96,21 @@ typedef struct {
   float beta1, beta2, eps, weight_decay;   /* Alg. 5 inputs; weight_decay = lambda (R15) */
   int32_t check_finite;          /* 1: flag non-finite gradients (reported by bpc_sync) */
   int32_t exchange;              /* bpc_exchange_mode requested for A4/A8 when world_size > 1 */
+  int32_t optimizer;             /* bpc_optimizer applied by bpc_step */
+  float lans_alpha_l, lans_alpha_u;  /* LANS: phi(z) = min(max(z, alpha_l), alpha_u),
+                                        0 < alpha_l <= alpha_u */
 } bpc_config;
+
+/* The adaptive update of bpc_step (A9).
+ * BPC_OPT_ADAM: Alg. 5 lines 12-16 and x = x - lr (r + weight_decay x)
+ *   (R15, R21), one fused pass (24 B/element + payload).
+ * BPC_OPT_LANS: CLAN proper, Alg. 5 lines 12-18 (Alg. 2
+ *   PAPER.md:157-163): per block G_b = one tensor,
+ *   d = phi(||x_b||) [beta1 (r + lambda x)/||r + lambda x|| + (1 - beta1)(c + lambda x)/||c + lambda x||],
+ *   c = g~/(sqrt(v~) + eps), x = x - lr d (reading R22).  Two streaming passes
+ *   plus one CTA per block for the norms (36 B/element + 2 payload reads);
+ *   every tensor must have <= 2^25 elements (else BPC_ERR_INVALID_ARGUMENT). */
+typedef enum { BPC_OPT_ADAM = 0, BPC_OPT_LANS = 1 } bpc_optimizer;
 
 /* Transport of the exchange steps A4 (push) and A8 (pull), world_size > 1.
  * BPC_EXCHANGE_P2P: every rank maps its peers' RECV / P / flag buffers with CUDA

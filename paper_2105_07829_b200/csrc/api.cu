@@ -88,6 +88,10 @@ bpc_status make_plan(const bpc_config* cfg, Plan* P, std::string* err) {
     return fail(BPC_ERR_INVALID_ARGUMENT, "eps and weight_decay must be >= 0");
   if (cfg->exchange != BPC_EXCHANGE_P2P && cfg->exchange != BPC_EXCHANGE_NCCL)
     return fail(BPC_ERR_INVALID_ARGUMENT, "unknown exchange mode");
+  if (cfg->optimizer != BPC_OPT_ADAM && cfg->optimizer != BPC_OPT_LANS)
+    return fail(BPC_ERR_INVALID_ARGUMENT, "unknown optimizer");
+  if (cfg->optimizer == BPC_OPT_LANS && !(cfg->lans_alpha_l > 0.f && cfg->lans_alpha_l <= cfg->lans_alpha_u))
+    return fail(BPC_ERR_INVALID_ARGUMENT, "LANS needs 0 < alpha_l <= alpha_u");
   uint64_t ce = cfg->chunk_elems ? cfg->chunk_elems : (1ull << 18);
   if (ce < kSlice || ce > 16 * kSlice || (ce & (ce - 1)))
     return fail(BPC_ERR_INVALID_ARGUMENT, "chunk_elems must be a power of two in [2^14, 2^18]");
@@ -99,6 +103,8 @@ bpc_status make_plan(const bpc_config* cfg, Plan* P, std::string* err) {
     const uint64_t L = cfg->tensor_numel[t], o = cfg->tensor_offset[t];
     if (L == 0) return fail(BPC_ERR_EMPTY_BLOCK, "tensor with numel 0");
     if (L >= (1ull << 31)) return fail(BPC_ERR_INVALID_ARGUMENT, "tensor numel >= 2^31");
+    if (cfg->optimizer == BPC_OPT_LANS && L > 4096ull * LANS_MAX_TILES)
+      return fail(BPC_ERR_INVALID_ARGUMENT, "LANS block (tensor) larger than 2^25 elements");
     if (o % 4) return fail(BPC_ERR_INVALID_ARGUMENT, "tensor offsets must be multiples of 4 elements");
     iv.push_back({o, o + L});
     P->D = std::max(P->D, o + L);
@@ -224,6 +230,10 @@ struct bpc_ctx {
   std::vector<uint8_t*> peer_recv, peer_p;
   std::vector<unsigned long long*> peer_flags;
   uint32_t push_epoch = 0, pull_epoch = 0;
+  // LANS (BPC_OPT_LANS): per update tile partial sums, per block coefficients
+  double* d_lans_part = nullptr;
+  float2* d_lans_coef = nullptr;
+  uint32_t* d_blk_tile = nullptr;
   int push_grid = 1, pull_grid = 1;
   uint32_t t = 1;
   int phase = 0;   // 0 compress, 1 push, 2 server, 3 pull, 4 step
@@ -283,6 +293,8 @@ void free_ctx(bpc_ctx* ctx) {
   for (int r = 0; r < (int)ctx->peer_flags.size(); r++)
     if (ctx->peer_flags[r] && r != ctx->cfg.rank) cudaIpcCloseMemHandle(ctx->peer_flags[r]);
   if (ctx->d_xflags) cudaFree(ctx->d_xflags);
+  for (void* q : {(void*)ctx->d_lans_part, (void*)ctx->d_lans_coef, (void*)ctx->d_blk_tile})
+    if (q) cudaFree(q);
   if (ctx->d_xdone) cudaFree(ctx->d_xdone);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   for (void* p : {(void*)ctx->e, (void*)ctx->etl, (void*)ctx->m, (void*)ctx->v, (void*)ctx->send,
@@ -526,6 +538,7 @@ bpc_status bpc_init(const bpc_config* cfg, bpc_ctx** out) {
   std::vector<DevChunk> dch(P.chunks.size());
   std::vector<uint32_t> witems, sitems;
   std::vector<Tile> wraw, sraw, utiles;
+  std::vector<uint32_t> blk_tile;   // first update tile of each tensor
   for (uint32_t c = 0; c < P.chunks.size(); c++) {
     const auto& ci = P.chunks[c];
     DevChunk& d = dch[c];
@@ -549,8 +562,10 @@ bpc_status bpc_init(const bpc_config* cfg, bpc_ctx** out) {
         if (mine) sraw.push_back(tl);
       }
     }
+    if (blk_tile.size() <= ci.tensor) blk_tile.resize(ci.tensor + 1, (uint32_t)utiles.size());
     for (uint64_t s0 = 0; s0 < ci.len; s0 += 4096) {
-      Tile tl = {c, (uint32_t)s0, (uint32_t)std::min<uint64_t>(4096, ci.len - s0), 0};
+      // pad = block (tensor) index: LANS reduces per block (tiles of a tensor are contiguous)
+      Tile tl = {c, (uint32_t)s0, (uint32_t)std::min<uint64_t>(4096, ci.len - s0), ci.tensor};
       utiles.push_back(tl);
     }
   }
@@ -565,6 +580,14 @@ bpc_status bpc_init(const bpc_config* cfg, bpc_ctx** out) {
   ctx->n_wraw = (uint32_t)wraw.size();
   ctx->n_sraw = (uint32_t)sraw.size();
   ctx->n_utiles = (uint32_t)utiles.size();
+  if (cfg->optimizer == BPC_OPT_LANS) {
+    blk_tile.push_back((uint32_t)utiles.size());   // [num_tensors + 1]
+    if ((s = upload(ctx, &ctx->d_blk_tile, blk_tile)) != BPC_OK) return bail(s);
+    if ((ce = alloc((void**)&ctx->d_lans_part, 24ull * utiles.size())) != cudaSuccess)
+      return bail(cuda_fail(ctx, ce, "alloc LANS partials"));
+    if ((ce = alloc((void**)&ctx->d_lans_coef, 8ull * cfg->num_tensors)) != cudaSuccess)
+      return bail(cuda_fail(ctx, ce, "alloc LANS coefficients"));
+  }
   // streaming-worker slices: compressed units in 2^13-element slices (multi-slice
   // units combine partials through global memory), raw units as plain tiles
   // (the server's: only the units this rank owns)
@@ -874,12 +897,33 @@ bpc_status bpc_step(bpc_ctx* ctx, float* d_params, float lr) {
   }
   cudaEvent_t b = nullptr;
   timer_begin(ctx, BPC_TIMER_UPDATE, &b);
-  if (c.comp.kind == BPC_TOP_K || c.comp.kind == BPC_RANDOM_K)
-    CK(launch_update(c.comp.kind, p, ctx->stream), "update launch");   // sparse decode: per-tile scatter
-  else
-    CK(launch_update_stream(c.comp.kind, p, ctx->num_sms, ctx->stream), "update launch");
+  const bool sparse = c.comp.kind == BPC_TOP_K || c.comp.kind == BPC_RANDOM_K;
+  auto pass = [&](int mode) -> cudaError_t {
+    p.mode = mode;
+    return sparse ? launch_update(c.comp.kind, p, ctx->stream)   // sparse decode: per-tile scatter
+                  : launch_update_stream(c.comp.kind, p, ctx->num_sms, ctx->stream);
+  };
+  if (c.optimizer == BPC_OPT_LANS) {
+    // LANS (R22): m, v + per-tile block sums; per-block coefficients; x
+    p.lans_part = ctx->d_lans_part;
+    p.lans_coef = ctx->d_lans_coef;
+    CK(pass(1), "LANS pass 1 launch");
+    LansCoefParams lc = {};
+    lc.part = ctx->d_lans_part;
+    lc.blk_tile = ctx->d_blk_tile;
+    lc.nblk = c.num_tensors;
+    lc.coef = ctx->d_lans_coef;
+    lc.beta1 = c.beta1;
+    lc.alpha_l = c.lans_alpha_l;
+    lc.alpha_u = c.lans_alpha_u;
+    CK(launch_lans_coef(lc, ctx->stream), "LANS coefficient launch");
+    CK(pass(2), "LANS pass 2 launch");
+    ctx->launches += 3;
+  } else {
+    CK(pass(0), "update launch");
+    ctx->launches++;
+  }
   timer_end(ctx, BPC_TIMER_UPDATE, b);
-  ctx->launches++;
   ctx->t++;
   ctx->phase = 0;
   return BPC_OK;

@@ -77,6 +77,9 @@ struct UpdateParams {
   float* x;
   float beta1, beta2, omb1, omb2, bc1, bc2, eps, lr, wd;   // bc = 1 / (1 - beta^t), R21
   uint32_t bits;
+  int32_t mode;           // 0 Adam core; LANS (R22): 1 = pass 1 (m, v, block sums), 2 = pass 2 (x)
+  double* lans_part;      // LANS pass 1: per update tile the pairwise sums of x^2, u^2, w^2
+  const float2* lans_coef;  // LANS pass 2: per block (a, b) coefficients
   PeerSync sync;          // fused exchange: wait for the owners' p (pull) ...
   const uint8_t* psrc[P2P_MAXJ];   // ... and read chunk payloads from psrc[owner] (P of each rank)
 };
@@ -143,6 +146,18 @@ struct P2PWait {
   int nslots;
   uint32_t epoch;
 };
+
+// LANS block coefficients (R22): one CTA per block reduces its tiles' partial
+// sums (pairwise, padded to a power of two) and writes (a, b)
+struct LansCoefParams {
+  const double* part;        // [3 * n_tiles]
+  const uint32_t* blk_tile;  // per block: first tile index; blk_tile[nblk] = n_tiles
+  uint32_t nblk;
+  float2* coef;              // [nblk]
+  float beta1, alpha_l, alpha_u;
+};
+cudaError_t launch_lans_coef(const LansCoefParams& p, cudaStream_t s);
+constexpr uint32_t LANS_MAX_TILES = 8192;   // tiles per block (2^25 elements)
 
 // host launchers (return the launch error)
 cudaError_t launch_p2p_copy(const P2PParams& p, int grid, cudaStream_t s);

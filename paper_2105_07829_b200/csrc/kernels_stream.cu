@@ -19,6 +19,8 @@
 // of slice i so the wait overlaps useful work.  All CTAs are co-resident
 // (cooperative launch) and every CTA publishes a slice before it waits on an
 // earlier one, so the waits cannot deadlock.
+#include <type_traits>
+
 #include "device.cuh"
 
 namespace bpc {
@@ -27,7 +29,7 @@ enum { S_NONE = 0, S_SIGN = 2, S_TOPK = 3, S_RANDK = 4, S_LDITHER = 5, S_NDITHER
 
 constexpr int CW = 16;                 // consumer warps
 constexpr int CNT = 32 * CW;           // consumer threads
-constexpr int SNT = CNT + 32;          // + 1 producer warp
+constexpr int SNT = CNT + 64;          // + 1 producer warp + 1 reducer warp (LANS pass 1)
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -48,6 +50,8 @@ struct UDesc {
   uint32_t L;
   uint32_t raw;
   uint32_t pofs;   // byte offset of the tile's first payload field inside the staged piece
+  uint32_t tile;   // global tile index (LANS partials)
+  float ca, cb;    // LANS pass 2: the tile's block coefficients (R22)
 };
 
 struct __align__(128) USmem {
@@ -58,6 +62,8 @@ struct __align__(128) USmem {
   float4 head[UST];               // the payload's first 16 bytes: scale (sign) / norm (dither)
   UDesc desc[UST];
   uint64_t full[UST], empty[UST];
+  uint64_t sums[UST];             // LANS pass 1: the consumers' warp subtrees of stage s are in red[s]
+  double red[UST][3][2 * CW];     // LANS pass 1: 128-element subtrees of x^2, u^2, w^2
 };
 
 __device__ __forceinline__ void adam1s(float g, float& m, float& v, float& x, const UpdateParams& p) {
@@ -69,9 +75,23 @@ __device__ __forceinline__ void adam1s(float g, float& m, float& v, float& x, co
   x = fsub(x, fmul(p.lr, fadd(r, fmul(p.wd, x))));             // x update (Adam core)
 }
 
+// LANS (R22): u = r + lambda x, w = c + lambda x with r = m~/(sqrt(v~)+eps),
+// c = g~/(sqrt(v~)+eps), from the already-updated m, v (the oracle's order)
+__device__ __forceinline__ void lans_uw(float g, float m, float v, float x, const UpdateParams& p, float& u,
+                                        float& w) {
+  const float den = fadd(__fsqrt_rn(fmul(v, p.bc2)), p.eps);
+  u = fadd(fdiv(fmul(m, p.bc1), den), fmul(p.wd, x));
+  w = fadd(fdiv(g, den), fmul(p.wd, x));
+}
+
 // FUSED: wait for the owners' p (fused NVLink exchange), then bulk-copy each
-// chunk's payload straight from its owner's P (p.psrc[owner], IPC-mapped)
-template <int KIND, bool FUSED>
+// chunk's payload straight from its owner's P (p.psrc[owner], IPC-mapped).
+// MODE 0: Adam core (A9).  LANS (NEXT #1, R22) runs two passes:
+// MODE 1: m, v updated and stored; per tile the fp64 pairwise subtrees of
+//         x^2, u^2, w^2 (a reducer warp writes p.lans_part[3 tile + q]);
+// MODE 2: u, w recomputed from the stored m, v; x -= lr (a u + b w) with the
+//         tile's block coefficients (p.lans_coef, from lans_coef_kernel).
+template <int KIND, bool FUSED, int MODE>
 __global__ void __launch_bounds__(SNT, 1) update_stream(const __grid_constant__ UpdateParams p) {
   extern __shared__ __align__(128) unsigned char sraw[];
   USmem& sm = *reinterpret_cast<USmem*>(sraw);
@@ -82,7 +102,8 @@ __global__ void __launch_bounds__(SNT, 1) update_stream(const __grid_constant__ 
   if (threadIdx.x == 0) {
     for (int s = 0; s < UST; s++) {
       mbar_init(&sm.full[s], 1);
-      mbar_init(&sm.empty[s], CW);
+      mbar_init(&sm.empty[s], MODE == 1 ? CW + 1 : CW);
+      mbar_init(&sm.sums[s], CW);
     }
     fence_mbar_init();
   }
@@ -105,6 +126,12 @@ __global__ void __launch_bounds__(SNT, 1) update_stream(const __grid_constant__ 
         d.len = tl.len;
         d.L = c.len;
         d.raw = c.raw;
+        d.tile = blockIdx.x + i * G;
+        if (MODE == 2) {
+          const float2 cf = p.lans_coef[tl.pad];   // Tile.pad = block (tensor) index
+          d.ca = cf.x;
+          d.cb = cf.y;
+        }
         const uint8_t* psrc;
         uint32_t pbytes, hbytes = 0;
         if (c.raw || KIND == S_NONE) {
@@ -133,6 +160,23 @@ __global__ void __launch_bounds__(SNT, 1) update_stream(const __grid_constant__ 
     }
     return;
   }
+  if (warp == CW + 1) {   // ---------------- reducer (LANS pass 1 only)
+    if (MODE == 1) {
+      for (uint32_t i = 0; i < mine; i++) {
+        const int s = i % UST;
+        mbar_wait(&sm.sums[s], (i / UST) & 1);
+        const uint32_t tile = sm.desc[s].tile;
+#pragma unroll
+        for (int q = 0; q < 3; q++) {   // tile total: pairwise tree over its 32 subtrees (R6)
+          const double t = warp_tree(sm.red[s][q][lane]);
+          if (lane == 0) p.lans_part[3ull * tile + q] = t;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[s]);
+      }
+    }
+    return;
+  }
   // ---------------- consumers
   const float sl = (float)((1u << (p.bits - 1)) - 1u);
   const int cmax = (1 << (p.bits - 1)) - 1;
@@ -150,10 +194,12 @@ __global__ void __launch_bounds__(SNT, 1) update_stream(const __grid_constant__ 
 #pragma unroll
     for (int k = 0; k < UK; k++) {
       const uint32_t f = threadIdx.x + k * CNT;   // float4 index inside the tile
-      if (4 * f >= d.len) continue;
+      const bool in = 4 * f < d.len;
+      if (MODE != 1 && !in) continue;
       const uint32_t j = d.start + 4 * f;
-      float4 g4;
-      if (d.raw || KIND == S_NONE) {
+      float4 g4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (!in) {
+      } else if (d.raw || KIND == S_NONE) {
         g4 = f < nvec ? sm.pay[s][f] : load4_masked(reinterpret_cast<const float*>(d.pay), j, d.L);
       } else if (KIND == S_SIGN) {
         const float h = hdr;
@@ -174,32 +220,82 @@ __global__ void __launch_bounds__(SNT, 1) update_stream(const __grid_constant__ 
           set(g4, u, (code & 1u) ? mag : -mag);
         }
       }
-      float4 m4, v4, x4;
+      float4 m4 = make_float4(0.f, 0.f, 0.f, 0.f), v4 = m4, x4 = m4;
       if (f < nvec) {
         m4 = sm.m[s][f];
         v4 = sm.v[s][f];
         x4 = sm.x[s][f];
-      } else {   // ragged tail of a unit: not covered by the 16-byte bulk copies
+      } else if (in) {   // ragged tail of a unit: not covered by the 16-byte bulk copies
         m4 = load4_masked(m, j, d.L);
         v4 = load4_masked(v, j, d.L);
         x4 = load4_masked(x, j, d.L);
       }
-      adam1s(g4.x, m4.x, v4.x, x4.x, p);
-      adam1s(g4.y, m4.y, v4.y, x4.y, p);
-      adam1s(g4.z, m4.z, v4.z, x4.z, p);
-      adam1s(g4.w, m4.w, v4.w, x4.w, p);
-      if (f < nvec) {
-        st4(m + j, m4);
-        st4(v + j, v4);
-        st4(x + j, x4);
-      } else {
-        store4_masked(m, j, d.L, m4);
-        store4_masked(v, j, d.L, v4);
-        store4_masked(x, j, d.L, x4);
+      if (MODE == 0) {
+        adam1s(g4.x, m4.x, v4.x, x4.x, p);
+        adam1s(g4.y, m4.y, v4.y, x4.y, p);
+        adam1s(g4.z, m4.z, v4.z, x4.z, p);
+        adam1s(g4.w, m4.w, v4.w, x4.w, p);
+        if (f < nvec) {
+          st4(m + j, m4);
+          st4(v + j, v4);
+          st4(x + j, x4);
+        } else {
+          store4_masked(m, j, d.L, m4);
+          store4_masked(v, j, d.L, v4);
+          store4_masked(x, j, d.L, x4);
+        }
+      } else if (MODE == 1) {
+        float4 u4, w4;
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          float mm = get(m4, e), vv = get(v4, e);
+          const float g = get(g4, e);
+          mm = fadd(fmul(p.beta1, mm), fmul(p.omb1, g));            // line 12
+          vv = fadd(fmul(p.beta2, vv), fmul(p.omb2, fmul(g, g)));   // line 13
+          set(m4, e, mm);
+          set(v4, e, vv);
+          float uu, ww;
+          lans_uw(g, mm, vv, get(x4, e), p, uu, ww);
+          const bool valid = in && j + e < d.L;   // padding contributes +0 to the block sums
+          set(u4, e, valid ? uu : 0.f);
+          set(w4, e, valid ? ww : 0.f);
+          if (!valid) set(x4, e, 0.f);
+        }
+        if (in) {
+          if (f < nvec) {
+            st4(m + j, m4);
+            st4(v + j, v4);
+          } else {
+            store4_masked(m, j, d.L, m4);
+            store4_masked(v, j, d.L, v4);
+          }
+        }
+        // subtree m = k * CW + warp covers tile elements [128 m, 128 m + 128)
+        const double tx = warp_tree(leaf4_sq(x4));
+        const double tu = warp_tree(leaf4_sq(u4));
+        const double tw = warp_tree(leaf4_sq(w4));
+        if (lane == 0) {
+          sm.red[s][0][k * CW + warp] = tx;
+          sm.red[s][1][k * CW + warp] = tu;
+          sm.red[s][2][k * CW + warp] = tw;
+        }
+      } else {   // MODE 2
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          float uu, ww;
+          lans_uw(get(g4, e), get(m4, e), get(v4, e), get(x4, e), p, uu, ww);
+          const float dd = fadd(fmul(d.ca, uu), fmul(d.cb, ww));   // line 17
+          set(x4, e, fsub(get(x4, e), fmul(p.lr, dd)));           // line 18
+        }
+        if (f < nvec) st4(x + j, x4);
+        else store4_masked(x, j, d.L, x4);
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.empty[s]);   // this warp is done with stage s
+    if (lane == 0) {
+      if (MODE == 1) mbar_arrive(&sm.sums[s]);    // red[s] written (release)
+      mbar_arrive(&sm.empty[s]);                  // this warp is done with stage s
+    }
   }
 }
 
@@ -223,11 +319,23 @@ cudaError_t launch_update_stream(int kind, const UpdateParams& p, int grid, cuda
     return cudaLaunchKernelEx(&cfg, fn, p);
   };
   const bool f = p.sync.wflags != nullptr;
+  auto pick = [&](auto kind_tag) -> cudaError_t {
+    constexpr int K = decltype(kind_tag)::value;
+    switch (p.mode * 2 + (f ? 1 : 0)) {
+      case 0: return go(update_stream<K, false, 0>);
+      case 1: return go(update_stream<K, true, 0>);
+      case 2: return go(update_stream<K, false, 1>);
+      case 3: return go(update_stream<K, true, 1>);
+      case 4: return go(update_stream<K, false, 2>);
+      case 5: return go(update_stream<K, true, 2>);
+    }
+    return cudaErrorInvalidValue;
+  };
   switch (kind) {
-    case S_NONE: return f ? go(update_stream<S_NONE, true>) : go(update_stream<S_NONE, false>);
-    case S_SIGN: return f ? go(update_stream<S_SIGN, true>) : go(update_stream<S_SIGN, false>);
-    case S_LDITHER: return f ? go(update_stream<S_LDITHER, true>) : go(update_stream<S_LDITHER, false>);
-    case S_NDITHER: return f ? go(update_stream<S_NDITHER, true>) : go(update_stream<S_NDITHER, false>);
+    case S_NONE: return pick(std::integral_constant<int, S_NONE>{});
+    case S_SIGN: return pick(std::integral_constant<int, S_SIGN>{});
+    case S_LDITHER: return pick(std::integral_constant<int, S_LDITHER>{});
+    case S_NDITHER: return pick(std::integral_constant<int, S_NDITHER>{});
   }
   return cudaErrorInvalidValue;
 }

@@ -17,10 +17,21 @@ __device__ __forceinline__ void adam1(float g, float& m, float& v, float& x, con
   x = fsub(x, fmul(p.lr, fadd(r, fmul(p.wd, x))));             // x update (Adam core)
 }
 
-template <int KIND>
+// LANS (R22): u = r + lambda x, w = c + lambda x from the updated m, v
+__device__ __forceinline__ void lans_uw1(float g, float m, float v, float x, const UpdateParams& p, float& u,
+                                         float& w) {
+  const float den = fadd(__fsqrt_rn(fmul(v, p.bc2)), p.eps);
+  u = fadd(fdiv(fmul(m, p.bc1), den), fmul(p.wd, x));
+  w = fadd(fdiv(g, den), fmul(p.wd, x));
+}
+
+// MODE 0: Adam core; LANS (R22) MODE 1: m, v + the tile's pairwise sums of
+// x^2, u^2, w^2 -> p.lans_part; MODE 2: x -= lr (a u + b w)   (see update_stream)
+template <int KIND, int MODE>
 __global__ void __launch_bounds__(UNT) update_kernel(const __grid_constant__ UpdateParams p) {
   constexpr bool SPARSE = KIND == U_TOPK || KIND == U_RANDK;
   __shared__ float gts[SPARSE ? UTILE : 1];
+  __shared__ double red[MODE == 1 ? 3 : 1][32];
   const Tile tl = p.tiles[blockIdx.x];
   const DevChunk c = p.chunks[tl.chunk];
   const uint8_t* pay = p.pbuf + c.pay;
@@ -38,6 +49,7 @@ __global__ void __launch_bounds__(UNT) update_kernel(const __grid_constant__ Upd
   for (int it = 0; it < UIT; it++) {
     const uint32_t i4 = it * UNT + threadIdx.x;
     const uint32_t j = tl.start + 4 * i4;
+    m4[it] = v4[it] = x4[it] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (full) {
       m4[it] = ld4(m + j);
       v4[it] = ld4(v + j);
@@ -68,13 +80,18 @@ __global__ void __launch_bounds__(UNT) update_kernel(const __grid_constant__ Upd
   const float sl = (float)((1u << (b - 1)) - 1u);
   const int cmax = (1 << (b - 1)) - 1;
   const float unit = fdiv(hdr, sl);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float2 cf = make_float2(0.f, 0.f);
+  if (MODE == 2) cf = p.lans_coef[tl.pad];   // Tile.pad = block (tensor) index
 #pragma unroll
   for (int it = 0; it < UIT; it++) {
     const uint32_t i4 = it * UNT + threadIdx.x;
     const uint32_t j = tl.start + 4 * i4;
-    if (!full && 4 * i4 >= tl.len) continue;
-    float4 g4;
-    if (raw || KIND == U_NONE) {
+    const bool in = full || 4 * i4 < tl.len;
+    if (MODE != 1 && !in) continue;
+    float4 g4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (!in) {
+    } else if (raw || KIND == U_NONE) {
       g4 = full ? ld4(reinterpret_cast<const float*>(pay) + j) : load4_masked(reinterpret_cast<const float*>(pay), j, L);
     } else if (KIND == U_SIGN) {
       const uint32_t nib = (reinterpret_cast<const uint32_t*>(pay + 4)[j >> 5] >> (j & 31)) & 15u;
@@ -97,34 +114,139 @@ __global__ void __launch_bounds__(UNT) update_kernel(const __grid_constant__ Upd
         set(g4, u, (code & 1u) ? mag : -mag);
       }
     }
-    adam1(g4.x, m4[it].x, v4[it].x, x4[it].x, p);
-    adam1(g4.y, m4[it].y, v4[it].y, x4[it].y, p);
-    adam1(g4.z, m4[it].z, v4[it].z, x4[it].z, p);
-    adam1(g4.w, m4[it].w, v4[it].w, x4[it].w, p);
-    if (full) {
-      st4(m + j, m4[it]);
-      st4(v + j, v4[it]);
-      st4(x + j, x4[it]);
-    } else {
-      store4_masked(m, j, L, m4[it]);
-      store4_masked(v, j, L, v4[it]);
-      store4_masked(x, j, L, x4[it]);
+    if (MODE == 0) {
+      adam1(g4.x, m4[it].x, v4[it].x, x4[it].x, p);
+      adam1(g4.y, m4[it].y, v4[it].y, x4[it].y, p);
+      adam1(g4.z, m4[it].z, v4[it].z, x4[it].z, p);
+      adam1(g4.w, m4[it].w, v4[it].w, x4[it].w, p);
+      if (full) {
+        st4(m + j, m4[it]);
+        st4(v + j, v4[it]);
+        st4(x + j, x4[it]);
+      } else {
+        store4_masked(m, j, L, m4[it]);
+        store4_masked(v, j, L, v4[it]);
+        store4_masked(x, j, L, x4[it]);
+      }
+    } else if (MODE == 1) {
+      float4 u4, w4, xv = x4[it];
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        float mm = get(m4[it], e), vv = get(v4[it], e);
+        const float g = get(g4, e);
+        mm = fadd(fmul(p.beta1, mm), fmul(p.omb1, g));            // line 12
+        vv = fadd(fmul(p.beta2, vv), fmul(p.omb2, fmul(g, g)));   // line 13
+        set(m4[it], e, mm);
+        set(v4[it], e, vv);
+        float uu, ww;
+        lans_uw1(g, mm, vv, get(xv, e), p, uu, ww);
+        const bool valid = in && j + e < L;   // padding contributes +0 to the block sums
+        set(u4, e, valid ? uu : 0.f);
+        set(w4, e, valid ? ww : 0.f);
+        if (!valid) set(xv, e, 0.f);
+      }
+      if (in) {
+        if (full) {
+          st4(m + j, m4[it]);
+          st4(v + j, v4[it]);
+        } else {
+          store4_masked(m, j, L, m4[it]);
+          store4_masked(v, j, L, v4[it]);
+        }
+      }
+      // subtree it * 8 + warp covers tile elements [128 (it * 8 + warp), + 128)
+      const double tx = warp_tree(leaf4_sq(xv));
+      const double tu = warp_tree(leaf4_sq(u4));
+      const double tw = warp_tree(leaf4_sq(w4));
+      if (lane == 0) {
+        red[0][it * 8 + warp] = tx;
+        red[MODE == 1 ? 1 : 0][it * 8 + warp] = tu;
+        red[MODE == 1 ? 2 : 0][it * 8 + warp] = tw;
+      }
+    } else {   // MODE 2
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        float uu, ww;
+        lans_uw1(get(g4, e), get(m4[it], e), get(v4[it], e), get(x4[it], e), p, uu, ww);
+        const float dd = fadd(fmul(cf.x, uu), fmul(cf.y, ww));   // line 17
+        set(x4[it], e, fsub(get(x4[it], e), fmul(p.lr, dd)));    // line 18
+      }
+      if (full) st4(x + j, x4[it]);
+      else store4_masked(x, j, L, x4[it]);
     }
   }
+  if (MODE == 1) {   // tile totals: pairwise tree over the 32 subtrees (R6)
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+      for (int q = 0; q < 3; q++) {
+        const double t = warp_tree(red[MODE == 1 ? q : 0][lane]);
+        if (lane == 0) p.lans_part[3ull * blockIdx.x + q] = t;
+      }
+    }
+  }
+}
+
+// LANS block coefficients (R22): CTA b sums its tiles' partials in pairwise
+// order over the tile count padded to a power of two (= the pairwise tree over
+// the block padded to a power of two: tiles are 4096-aligned inside a block),
+// then phi = clamp(fl32(||x_b||)), a = fl32(phi beta1 / ||u_b||),
+// b = fl32(phi (1 - beta1) / ||w_b||), a zero norm -> 0.
+__global__ void __launch_bounds__(256) lans_coef_kernel(const __grid_constant__ LansCoefParams p) {
+  extern __shared__ double acc[];   // [LANS_MAX_TILES]
+  __shared__ double tot[3];
+  const uint32_t b = blockIdx.x;
+  const uint32_t first = p.blk_tile[b], T = p.blk_tile[b + 1] - first;
+  uint32_t P = 1;
+  while (P < T) P <<= 1;
+  for (int q = 0; q < 3; q++) {
+    for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) acc[i] = i < T ? p.part[3ull * (first + i) + q] : 0.0;
+    __syncthreads();
+    for (uint32_t st = 1; st < P; st <<= 1) {
+      for (uint32_t i = threadIdx.x * 2 * st; i < P; i += blockDim.x * 2 * st) acc[i] = acc[i] + acc[i + st];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) tot[q] = acc[0];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double nx = sqrt(tot[0]), nu = sqrt(tot[1]), nw = sqrt(tot[2]);
+    float phi = (float)nx;
+    phi = fminf(fmaxf(phi, p.alpha_l), p.alpha_u);
+    const float a = nu > 0.0 ? (float)((double)phi * (double)p.beta1 / nu) : 0.f;
+    const float bb = nw > 0.0 ? (float)((double)phi * (1.0 - (double)p.beta1) / nw) : 0.f;
+    p.coef[b] = make_float2(a, bb);
+  }
+}
+
+cudaError_t launch_lans_coef(const LansCoefParams& p, cudaStream_t s) {
+  if (p.nblk == 0) return cudaSuccess;
+  const size_t smem = sizeof(double) * LANS_MAX_TILES;
+  cudaError_t e = cudaFuncSetAttribute(lans_coef_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  lans_coef_kernel<<<p.nblk, 256, smem, s>>>(p);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_update(int kind, const UpdateParams& p, cudaStream_t s) {
   if (p.n_tiles == 0) return cudaSuccess;
   const dim3 grid(p.n_tiles), block(UNT);
+#define BPC_UPD(K)                                                       \
+  case K:                                                                \
+    if (p.mode == 0) update_kernel<K, 0><<<grid, block, 0, s>>>(p);      \
+    else if (p.mode == 1) update_kernel<K, 1><<<grid, block, 0, s>>>(p); \
+    else update_kernel<K, 2><<<grid, block, 0, s>>>(p);                  \
+    break;
   switch (kind) {
-    case U_NONE: update_kernel<U_NONE><<<grid, block, 0, s>>>(p); break;
-    case U_SIGN: update_kernel<U_SIGN><<<grid, block, 0, s>>>(p); break;
-    case U_TOPK: update_kernel<U_TOPK><<<grid, block, 0, s>>>(p); break;
-    case U_RANDK: update_kernel<U_RANDK><<<grid, block, 0, s>>>(p); break;
-    case U_LDITHER: update_kernel<U_LDITHER><<<grid, block, 0, s>>>(p); break;
-    case U_NDITHER: update_kernel<U_NDITHER><<<grid, block, 0, s>>>(p); break;
+    BPC_UPD(U_NONE)
+    BPC_UPD(U_SIGN)
+    BPC_UPD(U_TOPK)
+    BPC_UPD(U_RANDK)
+    BPC_UPD(U_LDITHER)
+    BPC_UPD(U_NDITHER)
     default: return cudaErrorInvalidValue;
   }
+#undef BPC_UPD
   return cudaGetLastError();
 }
 
