@@ -27,7 +27,8 @@ def build(force: bool = False) -> str:
 
 class _Comp(C.Structure):
     _fields_ = [("kind", C.c_int32), ("k_num", C.c_uint32), ("k_den", C.c_uint32),
-                ("bits", C.c_uint32), ("randk_scaled", C.c_int32), ("use_ef", C.c_int32)]
+                ("bits", C.c_uint32), ("randk_scaled", C.c_int32), ("use_ef", C.c_int32),
+                ("f16", C.c_int32)]
 
 
 class _Cfg(C.Structure):
@@ -90,7 +91,7 @@ def comp_struct(kind, k_num=1, k_den=1000, bits=7, randk_scaled=0, use_ef=1) -> 
 def _comp_of(c) -> _Comp:
     if isinstance(c, _Comp):
         return c
-    return _Comp(c.kind, c.k_num, c.k_den, c.bits, c.randk_scaled, c.use_ef)
+    return _Comp(c.kind, c.k_num, c.k_den, c.bits, c.randk_scaled, c.use_ef, getattr(c, "f16", 0))
 
 
 def philox(ctr, key) -> list[int]:

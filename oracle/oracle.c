@@ -126,13 +126,30 @@ uint64_t orc_topk_k(const orc_comp* c, uint64_t L) {
   return k < 1 ? 1 : k;
 }
 
+/* R23: a sparse value in binary16 (PAPER.md:648 counts 16-bit values): the
+ * fp32 value saturated to the largest finite half, +-65504, then rounded to
+ * nearest even (the C compiler's float -> _Float16 conversion). */
+static uint16_t f32_to_f16(float v) {
+  if (v > 65504.0f) v = 65504.0f;
+  if (v < -65504.0f) v = -65504.0f;
+  _Float16 h = (_Float16)v;
+  uint16_t u;
+  memcpy(&u, &h, 2);
+  return u;
+}
+static float f16_to_f32(uint16_t u) {
+  _Float16 h;
+  memcpy(&h, &u, 2);
+  return (float)h;
+}
+
 /* Closed-form payload sizes. */
 uint64_t orc_payload_bytes(const orc_comp* c, int raw, uint64_t L) {
   if (raw || c->kind == ORC_NONE) return 4 * L;
   switch (c->kind) {
     case ORC_SCALED_SIGN: return 4 + (L + 7) / 8;
     case ORC_TOP_K:
-    case ORC_RANDOM_K: return 8 + 8 * orc_topk_k(c, L);
+    case ORC_RANDOM_K: return 8 + (c->f16 ? 6 : 8) * orc_topk_k(c, L);
     case ORC_LINEAR_DITHER:
     case ORC_NATURAL_DITHER: return 4 + (c->bits * L + 7) / 8;
   }
@@ -205,7 +222,12 @@ int orc_compress(const orc_comp* c, int raw, const float* x, uint64_t L, uint64_
       for (uint64_t i = 0; i < k; i++) {
         put_u32(out + 8 + 4 * i, (uint32_t)idx[i]);
         float val = scaled ? x[idx[i]] * scale : x[idx[i]];
-        put_f32(out + 8 + 4 * k + 4 * i, val);
+        if (c->f16) {                                     /* R23 */
+          uint16_t h = f32_to_f16(val);
+          memcpy(out + 8 + 4 * k + 2 * i, &h, 2);
+        } else {
+          put_f32(out + 8 + 4 * k + 4 * i, val);
+        }
       }
       free(idx);
       free(it);
@@ -291,7 +313,13 @@ int orc_decompress(const orc_comp* c, int raw, const uint8_t* in, uint64_t L, fl
       for (uint64_t i = 0; i < k; i++) {
         uint64_t j = get_u32(in + 8 + 4 * i);
         if (j >= L || (i > 0 && j <= prev)) return 1;   /* malformed */
-        out[j] = get_f32(in + 8 + 4 * k + 4 * i);
+        if (c->f16) {
+          uint16_t h;
+          memcpy(&h, in + 8 + 4 * k + 2 * i, 2);
+          out[j] = f16_to_f32(h);
+        } else {
+          out[j] = get_f32(in + 8 + 4 * k + 4 * i);
+        }
         prev = j;
       }
       return 0;

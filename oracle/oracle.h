@@ -38,6 +38,7 @@ typedef struct {
   uint32_t bits;           /* dither bits including the sign bit, 2..8 (R11) */
   int32_t randk_scaled;    /* random-k: 1 = values * L/k (unbiased, Alg. 3); 0 = unscaled (R10) */
   int32_t use_ef;          /* Alg. 5 use_ef */
+  int32_t f16;             /* sparse kinds: values as IEEE binary16 (PAPER.md:648's 333x, R23) */
 } orc_comp;
 
 typedef struct {
