@@ -31,7 +31,7 @@ METRIC = "compressed aggregate+update step: gradient GB/s per step at 1/2/4/8 B2
 DESCR = {
     "C1": "d=4096 synthetic gradient, onebit scaled-sign + EF (configs[0])",
     "C2": "ResNet-50-shaped gradient (25.6M params, 161 tensors), onebit two-way + EF + Adam (configs[1])",
-    "C3": "VGG16-shaped gradient (138M params), top-k 0.1% + EF + Adam (configs[2])",
+    "C3": "VGG16-shaped gradient (138M params), top-k 0.1% (binary16 values, PAPER.md:648) + EF + Adam (configs[2])",
     "C4": "BERT-base-shaped gradient (110M params), linear dithering 7 bits (Alg. 3) + Adam (configs[3])",
     "C5": "BERT-large-shaped gradient (336M params), onebit two-way + EF + Adam (configs[4])",
 }

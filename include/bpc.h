@@ -73,6 +73,9 @@ typedef struct {
   uint32_t bits;           /* dither bits including the sign bit, 2..8 */
   int32_t randk_scaled;    /* random-k: 1 = values * L/k (unbiased); 0 = unscaled */
   int32_t use_ef;          /* Alg. 5 use_ef: 1 = Alg. 4 (error feedback), 0 = Alg. 3 */
+  int32_t f16_values;      /* sparse kinds: 1 = values as IEEE binary16, saturated to +-65504,
+                              round to nearest even (PAPER.md:648's 333x payload; DESIGN.md
+                              R23); payload [u64 k][k x u32 index][k x f16]; 0 = fp32 (R20) */
 } bpc_compressor;
 
 typedef struct {

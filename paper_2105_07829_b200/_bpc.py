@@ -33,7 +33,7 @@ class BpcError(RuntimeError):
 
 class Compressor(C.Structure):
     _fields_ = [("kind", C.c_int32), ("k_num", C.c_uint32), ("k_den", C.c_uint32), ("bits", C.c_uint32),
-                ("randk_scaled", C.c_int32), ("use_ef", C.c_int32)]
+                ("randk_scaled", C.c_int32), ("use_ef", C.c_int32), ("f16_values", C.c_int32)]
 
 
 class Config(C.Structure):
@@ -121,7 +121,8 @@ def make_config(numels, offsets, comp, *, world_size=1, rank=0, device=0, stream
     cfg = Config(world_size, rank, device, stream, C.cast(idbuf, C.c_void_p) if idbuf is not None else None,
                  seed, len(numel), numel.ctypes.data_as(C.POINTER(C.c_uint64)),
                  offset.ctypes.data_as(C.POINTER(C.c_uint64)), chunk_elems, threshold_bytes,
-                 Compressor(comp.kind, comp.k_num, comp.k_den, comp.bits, comp.randk_scaled, comp.use_ef),
+                 Compressor(comp.kind, comp.k_num, comp.k_den, comp.bits, comp.randk_scaled, comp.use_ef,
+                            getattr(comp, "f16", 0)),
                  beta1, beta2, eps, weight_decay, check_finite, exchange, optimizer, lans_alpha_l,
                  lans_alpha_u)
     cfg._keep = (numel, offset, idbuf)   # keep the arrays alive with the struct

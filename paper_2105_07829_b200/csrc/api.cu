@@ -53,7 +53,7 @@ uint64_t payload_size(const bpc_compressor& c, bool raw, uint64_t L) {
   switch (c.kind) {
     case BPC_SCALED_SIGN: return 4 + (L + 7) / 8;
     case BPC_TOP_K:
-    case BPC_RANDOM_K: return 8 + 8 * sparse_k(c, L);
+    case BPC_RANDOM_K: return 8 + (c.f16_values ? 6 : 8) * sparse_k(c, L);
     case BPC_LINEAR_DITHER:
     case BPC_NATURAL_DITHER: return 4 + ((uint64_t)c.bits * L + 7) / 8;
   }
@@ -82,6 +82,8 @@ bpc_status make_plan(const bpc_config* cfg, Plan* P, std::string* err) {
       break;
     default: return fail(BPC_ERR_UNSUPPORTED_KIND, "unknown compressor kind");
   }
+  if (C.f16_values != 0 && !(C.f16_values == 1 && (C.kind == BPC_TOP_K || C.kind == BPC_RANDOM_K)))
+    return fail(BPC_ERR_INVALID_ARGUMENT, "f16_values is 0 or 1, and 1 only for top-k / random-k");
   if (!(cfg->beta1 > 0.f && cfg->beta1 < 1.f && cfg->beta2 > 0.f && cfg->beta2 < 1.f))
     return fail(BPC_ERR_INVALID_ARGUMENT, "betas must lie in (0, 1)");
   if (!(cfg->eps >= 0.f) || !(cfg->weight_decay >= 0.f))
@@ -434,6 +436,7 @@ CompressParams base_params(bpc_ctx* ctx) {
   p.bits = ctx->cfg.comp.bits;
   p.randk_scaled = ctx->cfg.comp.randk_scaled;
   p.use_ef = ctx->cfg.comp.use_ef;
+  p.f16 = ctx->cfg.comp.f16_values;
   p.check_finite = ctx->cfg.check_finite;
   p.flag = ctx->d_flag;
   return p;
@@ -888,6 +891,7 @@ bpc_status bpc_step(bpc_ctx* ctx, float* d_params, float lr) {
   p.lr = lr;
   p.wd = c.weight_decay;
   p.bits = c.comp.bits;
+  p.f16 = c.comp.f16_values;
   p.sync = peer_sync(ctx);
   if (fused_exchange(ctx)) {   // wait for every owner's p, then read it from the owner's P
     p.sync.wflags = ctx->d_xflags;

@@ -4,6 +4,7 @@
 // arithmetic wrappers.  Nothing here is shared with oracle/.
 #pragma once
 #include <cooperative_groups.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <cstdio>
@@ -327,6 +328,25 @@ __device__ __forceinline__ uint32_t warp_lower_bound(const uint32_t* a, uint32_t
   const uint32_t pos = lo + lane;
   const bool below = pos < hi && a[pos] < key;
   return lo + __popc(__ballot_sync(0xffffffffu, below));
+}
+
+// ---------------------------------------------------------------- sparse values (R23)
+// binary16 values: saturate to +-65504 (the oracle's comparisons, NaN passes
+// through), then round to nearest even; returns the decoded fp32 value
+__device__ __forceinline__ float quant_val(float v, bool f16) {
+  if (!f16) return v;
+  if (v > 65504.f) v = 65504.f;
+  if (v < -65504.f) v = -65504.f;
+  return __half2float(__float2half_rn(v));
+}
+// value i of a payload's value array (fp32, or binary16 when f16)
+__device__ __forceinline__ float get_val(const uint8_t* vals, uint32_t i, bool f16) {
+  return f16 ? __half2float(reinterpret_cast<const __half*>(vals)[i]) : reinterpret_cast<const float*>(vals)[i];
+}
+// store an already-quantised value (exact in binary16 when f16)
+__device__ __forceinline__ void put_val(uint8_t* vals, uint32_t i, float v, bool f16) {
+  if (f16) reinterpret_cast<__half*>(vals)[i] = __float2half_rn(v);
+  else reinterpret_cast<float*>(vals)[i] = v;
 }
 
 __device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }

@@ -335,7 +335,7 @@ __device__ __forceinline__ void produce_server_sparse(const CompressParams& p, c
   for (uint32_t r = 0; r < p.n; r++) {
     const uint8_t* pl = p.recv + r * p.slot_bytes + c.recv;
     const uint32_t* idx = reinterpret_cast<const uint32_t*>(pl + 8);
-    const float* val = reinterpret_cast<const float*>(pl + 8 + 4ull * k);
+    const uint8_t* val = pl + 8 + 4ull * k;
     const uint32_t lo = warp_lower_bound(idx, k, jlo), hi = warp_lower_bound(idx, k, jhi);
     for (uint32_t e = lo + threadIdx.x; e < hi; e += NT) {
       const uint32_t j = idx[e];
@@ -347,12 +347,12 @@ __device__ __forceinline__ void produce_server_sparse(const CompressParams& p, c
       }
       if (!first) continue;
       double acc = 0.0;
-      acc += (double)val[e];
+      acc += (double)get_val(val, e, p.f16);
       for (uint32_t r2 = r + 1; r2 < p.n; r2++) {
         const uint8_t* pl2 = p.recv + r2 * p.slot_bytes + c.recv;
         const uint32_t* idx2 = reinterpret_cast<const uint32_t*>(pl2 + 8);
         const uint32_t pos = lower_bound_u32(idx2, k, j);
-        if (pos < k && idx2[pos] == j) acc += (double)reinterpret_cast<const float*>(pl2 + 8 + 4ull * k)[pos];
+        if (pos < k && idx2[pos] == j) acc += (double)get_val(pl2 + 8 + 4ull * k, pos, p.f16);
       }
       const double ev = p.use_ef ? (double)et[j] : 0.0;
       sq[j - s0] = mean_plus(acc, p.inv_n, ev);
@@ -706,7 +706,7 @@ __device__ void emit_sparse(const CompressParams& p, const DevChunk& c, Smem& sm
   const bool scaled = KIND == K_RANDK && p.randk_scaled;
   const float scale = (float)((double)L / (double)k);
   uint32_t* idx_out = reinterpret_cast<uint32_t*>(pay + 8);
-  float* val_out = reinterpret_cast<float*>(pay + 8 + 4ull * k);
+  uint8_t* val_out = pay + 8 + 4ull * k;   // fp32, or binary16 values (R23)
   if (selected && k <= (uint32_t)SELCAP) {   // cluster-uniform
     // ---- small k: the selected entries are key > T, or key == T at index <= tie_cut.
     // One pass writes the error and collects this slice's (index, value) pairs in
@@ -747,7 +747,7 @@ __device__ void emit_sparse(const CompressParams& p, const DevChunk& c, Smem& sm
         for (int u = 0; u < 4; u++)
           if ((selm >> u) & 1u) {
             const float qu = get(q, u);
-            const float val = scaled ? fmul(qu, scale) : qu;
+            const float val = quant_val(scaled ? fmul(qu, scale) : qu, p.f16);   // R23
             sidx[pos] = j + u;
             sval[pos] = val;
             set(ev, u, fsub(qu, val));
@@ -765,7 +765,7 @@ __device__ void emit_sparse(const CompressParams& p, const DevChunk& c, Smem& sm
       uint32_t rank = 0;
       for (uint32_t b2 = 0; b2 < m; b2++) rank += sidx[b2] < ia;
       idx_out[base + rank] = ia;
-      val_out[base + rank] = sval[a];
+      put_val(val_out, base + rank, sval[a], p.f16);
     }
     cluster_arrive_relaxed();   // done with peers' smem; the matching wait is at kernel exit
     if (crank == 0 && threadIdx.x == 0) *reinterpret_cast<uint64_t*>(pay) = (uint64_t)k;
@@ -846,9 +846,9 @@ __device__ void emit_sparse(const CompressParams& p, const DevChunk& c, Smem& sm
       for (int u = 0; u < 4; u++)
         if ((selm >> u) & 1u) {
           const float qu = get(q, u);
-          const float val = scaled ? fmul(qu, scale) : qu;
+          const float val = quant_val(scaled ? fmul(qu, scale) : qu, p.f16);   // R23
           idx_out[pos] = j + u;
-          val_out[pos] = val;
+          put_val(val_out, pos, val, p.f16);
           set(ev, u, fsub(qu, val));
           pos++;
         }

@@ -66,12 +66,12 @@ __global__ void __launch_bounds__(UNT) update_kernel(const __grid_constant__ Upd
       __syncthreads();
       const uint32_t k = c.k;
       const uint32_t* idx = reinterpret_cast<const uint32_t*>(pay + 8);
-      const float* val = reinterpret_cast<const float*>(pay + 8 + 4ull * k);
+      const uint8_t* val = pay + 8 + 4ull * k;   // fp32, or binary16 values (R23)
       const uint32_t lo = warp_lower_bound(idx, k, tl.start);
       for (uint32_t e = lo + threadIdx.x; e < k; e += UNT) {
         const uint32_t j = idx[e];
         if (j >= tl.start + tl.len) break;
-        gts[j - tl.start] = val[e];
+        gts[j - tl.start] = get_val(val, e, p.f16);
       }
       __syncthreads();
     }

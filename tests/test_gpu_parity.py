@@ -42,6 +42,8 @@ KINDS = [
     ("ldither2_ef", Comp(LINEAR_DITHER, bits=2, use_ef=1)),
     ("ndither3", Comp(NATURAL_DITHER, bits=3, use_ef=0)),
     ("none", Comp(NONE, use_ef=1)),
+    ("topk_f16_ef", Comp(TOP_K, 1, 1000, use_ef=1, f16=1)),          # R23: binary16 values
+    ("randk_scaled_f16", Comp(RANDOM_K, 1, 32, randk_scaled=1, use_ef=0, f16=1)),
 ]
 
 
