@@ -37,7 +37,7 @@ class _Cfg(C.Structure):
                 ("chunk_elems", C.c_uint64), ("threshold_bytes", C.c_uint64), ("comp", _Comp),
                 ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
                 ("weight_decay", C.c_float), ("optimizer", C.c_int32), ("alpha_l", C.c_float),
-                ("alpha_u", C.c_float)]
+                ("alpha_u", C.c_float), ("momentum", C.c_float)]
 
 
 class _Chunk(C.Structure):
@@ -73,6 +73,7 @@ def lib():
         L.orc_push_pull.argtypes = [C.c_uint32, C.c_uint64, C.c_void_p, C.c_void_p]
         L.orc_adam.argtypes = [C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                C.c_uint32, C.c_float, C.c_float, C.c_float, C.c_float, C.c_float]
+        L.orc_nag.argtypes = [C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_float, C.c_float, C.c_float]
         L.orc_lans_block.argtypes = [C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                      C.c_uint32, C.c_float, C.c_float, C.c_float, C.c_float, C.c_float,
                                      C.c_float, C.c_float]
@@ -146,14 +147,14 @@ class Cfg:
 
     def __init__(self, n, numels, offsets, comp, *, seed=0, chunk_elems=1 << 18,
                  threshold_bytes=1 << 20, beta1=0.9, beta2=0.999, eps=1e-6, weight_decay=0.0,
-                 optimizer="adam", alpha_l=0.01, alpha_u=10.0):
+                 optimizer="adam", alpha_l=0.01, alpha_u=10.0, momentum=0.9):
         self.numel = np.ascontiguousarray(numels, dtype=np.uint64)
         self.offset = np.ascontiguousarray(offsets, dtype=np.uint64)
         self.s = _Cfg(n, seed, len(self.numel),
                       self.numel.ctypes.data_as(C.POINTER(C.c_uint64)),
                       self.offset.ctypes.data_as(C.POINTER(C.c_uint64)),
                       chunk_elems, threshold_bytes, _comp_of(comp), beta1, beta2, eps, weight_decay,
-                      {"adam": 0, "lans": 1}[optimizer], alpha_l, alpha_u)
+                      {"adam": 0, "lans": 1, "nag": 2}[optimizer], alpha_l, alpha_u, momentum)
 
     @classmethod
     def from_workload(cls, wcfg, n=None):
@@ -164,7 +165,7 @@ class Cfg:
                    chunk_elems=wcfg.chunk_elems, threshold_bytes=wcfg.threshold_bytes,
                    beta1=wcfg.beta1, beta2=wcfg.beta2, eps=wcfg.eps, weight_decay=wcfg.weight_decay,
                    optimizer=getattr(wcfg, "optimizer", "adam"), alpha_l=getattr(wcfg, "alpha_l", 0.01),
-                   alpha_u=getattr(wcfg, "alpha_u", 10.0))
+                   alpha_u=getattr(wcfg, "alpha_u", 10.0), momentum=getattr(wcfg, "momentum", 0.9))
 
     def plan(self) -> list[tuple[int, int, int, int]]:
         n = lib().orc_plan(C.byref(self.s), None, 0)
@@ -230,6 +231,14 @@ def lans_block(gt, m, v, x, t, lr, beta1, beta2, eps, wd, alpha_l=0.01, alpha_u=
     gt = np.ascontiguousarray(gt, dtype=np.float32)
     lib().orc_lans_block(gt.size, _ptr(gt), _ptr(m), _ptr(v), _ptr(x), t, lr, beta1, beta2, eps, wd,
                          alpha_l, alpha_u)
+
+
+def nag(gt, vel, x, lr, mu, wd):
+    """One NAG step in place (R24); vel is the velocity."""
+    for a in (vel, x):
+        assert a.dtype == np.float32 and a.flags["C_CONTIGUOUS"]
+    gt = np.ascontiguousarray(gt, dtype=np.float32)
+    lib().orc_nag(gt.size, _ptr(gt), _ptr(vel), _ptr(x), lr, mu, wd)
 
 
 def adam(gt, m, v, x, t, lr, beta1, beta2, eps, wd):

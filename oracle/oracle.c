@@ -409,6 +409,19 @@ void orc_adam(uint64_t L, const float* gt, float* m, float* v, float* x, uint32_
   }
 }
 
+/* NAG, the optimizer every compressor is applied to in the CNN experiments
+ * ("All the compression methods are applied to NAG"), in the
+ * form of SPEC.md:393 with weight decay folded into the gradient as in the
+ * SGD of the paper's training recipe (reading R24):
+ *   g = g~ + lambda x;  v = mu v + g;  x = x - eta (g + mu v). */
+void orc_nag(uint64_t L, const float* gt, float* vel, float* x, float lr, float mu, float wd) {
+  for (uint64_t j = 0; j < L; j++) {
+    float g = gt[j] + wd * x[j];
+    vel[j] = mu * vel[j] + g;
+    x[j] = x[j] - lr * (g + mu * vel[j]);
+  }
+}
+
 /* LANS block update (CLAN, Alg. 5 lines 12-18; the same
  * step as Alg. 2 lines 8-14), in the paper's order:
  *   m, v, m~, v~ as in orc_adam (lines 12-15, R16/R21);
@@ -529,6 +542,8 @@ int orc_round(const orc_cfg* cfg, uint64_t D, const float* grads, float* e, floa
     /* ---- workers: g~ = dec(p), then the adaptive update (Alg. 5 l.12-18) */
     if (cfg->optimizer == 1)
       memcpy(gall + o, gt, sizeof(float) * L);      /* LANS: per-block update after all chunks */
+    else if (cfg->optimizer == 2)
+      orc_nag(L, gt, m + o, x + o, lr, cfg->momentum, cfg->weight_decay);   /* velocity in m */
     else
       orc_adam(L, gt, m + o, v + o, x + o, t, lr, cfg->beta1, cfg->beta2, cfg->eps, cfg->weight_decay);
     if (gtilde_out) memcpy(gtilde_out + o, gt, sizeof(float) * L);

@@ -51,8 +51,10 @@ typedef struct {
   uint64_t threshold_bytes;      /* PAPER.md:505 size threshold (R3) */
   orc_comp comp;
   float beta1, beta2, eps, weight_decay;   /* Alg. 5 inputs, R15 */
-  int32_t optimizer;             /* 0: Adam core (R15); 1: LANS block-normalised update (R22) */
+  int32_t optimizer;             /* 0: Adam core (R15); 1: LANS block-normalised update (R22);
+                                    2: NAG (R24) */
   float alpha_l, alpha_u;        /* LANS: phi = clamp(., alpha_l, alpha_u) */
+  float momentum;                /* NAG: mu in [0, 1) */
 } orc_cfg;
 
 typedef struct {
@@ -102,6 +104,8 @@ void orc_push_pull(uint32_t n, uint64_t D, const float* grads, float* out);
 void orc_lans_block(uint64_t L, const float* gtilde, float* m, float* v, float* x, uint32_t t,
                     float lr, float beta1, float beta2, float eps, float wd, float alpha_l,
                     float alpha_u);
+/* Nesterov momentum (NAG) on the aggregated gradient, R24. */
+void orc_nag(uint64_t L, const float* gtilde, float* vel, float* x, float lr, float mu, float wd);
 void orc_adam(uint64_t L, const float* gtilde, float* m, float* v, float* x, uint32_t t,
               float lr, float beta1, float beta2, float eps, float weight_decay);
 
