@@ -46,8 +46,9 @@ def parse():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
                     help="N>1 transport of the push/pull exchange: NVLink peer stores or NCCL send/recv")
-    ap.add_argument("--optimizer", choices=["adam", "lans"], default="adam",
-                    help="bpc_step update: Adam core (A9) or the LANS / CLAN block-normalised update (NEXT #1)")
+    ap.add_argument("--optimizer", choices=["adam", "lans", "nag"], default="adam",
+                    help="bpc_step update: Adam core (A9), the LANS / CLAN block-normalised update (NEXT #1) "
+                         "or NAG (the CNN runs' optimizer, R24)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -110,7 +111,7 @@ class Clocks:
 
 
 # ---------------------------------------------------------------- byte models
-def kernel_bytes(chunks, comp, n, rank, lans=False):
+def kernel_bytes(chunks, comp, n, rank, lans=False, nag=False):
     """Algorithmic HBM bytes per launch of each kernel; LANS's
     update = pass 1 (m, v, x read, m, v written) + pass 2 (m, v, x read, x
     written) + the payload read twice."""
@@ -122,12 +123,12 @@ def kernel_bytes(chunks, comp, n, rank, lans=False):
             w += 8 * L
             if c.owner == rank:
                 s += 4 * n * L + 4 * L
-            u += (36 * L + 8 * L) if lans else (24 * L + 4 * L)
+            u += (36 * L + 8 * L) if lans else (16 * L + 4 * L) if nag else (24 * L + 4 * L)
         else:
             w += (12 if ef else 4) * L + pb
             if c.owner == rank:
                 s += n * pb + (8 * L if ef else 0) + pb
-            u += (36 * L + 2 * pb) if lans else (24 * L + pb)
+            u += (36 * L + 2 * pb) if lans else (16 * L + pb) if nag else (24 * L + pb)
     return {"compress": w, "server": s, "update": u}
 
 
@@ -309,7 +310,7 @@ def run_ours(args):
     barrier()
     tim = ctx.timing()
     ctx.set_timing(False)
-    kb = kernel_bytes(chunks, w.comp, world, rank, lans=args.optimizer == "lans")
+    kb = kernel_bytes(chunks, w.comp, world, rank, lans=args.optimizer == "lans", nag=args.optimizer == "nag")
     per = {k: (tim[k][0] / max(1, tim[k][1]), tim[k][1]) for k in ("compress", "server", "update", "push", "pull")}
     dom = max(("compress", "server", "update"), key=lambda k: per[k][0])
     peak, peak_src = peaks()

@@ -102,9 +102,10 @@ typedef struct {
   int32_t optimizer;             /* bpc_optimizer applied by bpc_step */
   float lans_alpha_l, lans_alpha_u;  /* LANS: phi(z) = min(max(z, alpha_l), alpha_u),
                                         0 < alpha_l <= alpha_u */
+  float momentum;                /* NAG: mu in [0, 1) */
 } bpc_config;
 
-/* The adaptive update of bpc_step (A9).
+/* The update of bpc_step (A9).
  * BPC_OPT_ADAM: Alg. 5 lines 12-16 and x = x - lr (r + weight_decay x)
  *   (R15, R21), one fused pass (24 B/element + payload).
  * BPC_OPT_LANS: CLAN proper, Alg. 5 lines 12-18 (Alg. 2
@@ -112,8 +113,12 @@ typedef struct {
  *   d = phi(||x_b||) [beta1 (r + lambda x)/||r + lambda x|| + (1 - beta1)(c + lambda x)/||c + lambda x||],
  *   c = g~/(sqrt(v~) + eps), x = x - lr d (reading R22).  Two streaming passes
  *   plus one CTA per block for the norms (36 B/element + 2 payload reads);
- *   every tensor must have <= 2^25 elements (else BPC_ERR_INVALID_ARGUMENT). */
-typedef enum { BPC_OPT_ADAM = 0, BPC_OPT_LANS = 1 } bpc_optimizer;
+ *   every tensor must have <= 2^25 elements (else BPC_ERR_INVALID_ARGUMENT).
+ * BPC_OPT_NAG: Nesterov momentum, the optimizer every compressor is applied to
+ *   in the paper's CNN runs (R24): g = g~ + lambda x,
+ *   v = momentum v + g, x = x - lr (g + momentum v); the velocity lives in the
+ *   BPC_BUF_M buffer, BPC_BUF_V is unused (16 B/element + payload). */
+typedef enum { BPC_OPT_ADAM = 0, BPC_OPT_LANS = 1, BPC_OPT_NAG = 2 } bpc_optimizer;
 
 /* Transport of the exchange steps A4 (push) and A8 (pull), world_size > 1.
  * BPC_EXCHANGE_P2P: every rank maps its peers' RECV / P / flag buffers with CUDA

@@ -90,8 +90,10 @@ bpc_status make_plan(const bpc_config* cfg, Plan* P, std::string* err) {
     return fail(BPC_ERR_INVALID_ARGUMENT, "eps and weight_decay must be >= 0");
   if (cfg->exchange != BPC_EXCHANGE_P2P && cfg->exchange != BPC_EXCHANGE_NCCL)
     return fail(BPC_ERR_INVALID_ARGUMENT, "unknown exchange mode");
-  if (cfg->optimizer != BPC_OPT_ADAM && cfg->optimizer != BPC_OPT_LANS)
+  if (cfg->optimizer != BPC_OPT_ADAM && cfg->optimizer != BPC_OPT_LANS && cfg->optimizer != BPC_OPT_NAG)
     return fail(BPC_ERR_INVALID_ARGUMENT, "unknown optimizer");
+  if (cfg->optimizer == BPC_OPT_NAG && !(cfg->momentum >= 0.f && cfg->momentum < 1.f))
+    return fail(BPC_ERR_INVALID_ARGUMENT, "NAG momentum must lie in [0, 1)");
   if (cfg->optimizer == BPC_OPT_LANS && !(cfg->lans_alpha_l > 0.f && cfg->lans_alpha_l <= cfg->lans_alpha_u))
     return fail(BPC_ERR_INVALID_ARGUMENT, "LANS needs 0 < alpha_l <= alpha_u");
   uint64_t ce = cfg->chunk_elems ? cfg->chunk_elems : (1ull << 18);
@@ -892,6 +894,7 @@ bpc_status bpc_step(bpc_ctx* ctx, float* d_params, float lr) {
   p.wd = c.weight_decay;
   p.bits = c.comp.bits;
   p.f16 = c.comp.f16_values;
+  p.mu = c.momentum;
   p.sync = peer_sync(ctx);
   if (fused_exchange(ctx)) {   // wait for every owner's p, then read it from the owner's P
     p.sync.wflags = ctx->d_xflags;
@@ -924,7 +927,7 @@ bpc_status bpc_step(bpc_ctx* ctx, float* d_params, float lr) {
     CK(pass(2), "LANS pass 2 launch");
     ctx->launches += 3;
   } else {
-    CK(pass(0), "update launch");
+    CK(pass(c.optimizer == BPC_OPT_NAG ? 3 : 0), "update launch");
     ctx->launches++;
   }
   timer_end(ctx, BPC_TIMER_UPDATE, b);

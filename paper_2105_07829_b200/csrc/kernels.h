@@ -78,8 +78,10 @@ struct UpdateParams {
   float* x;
   float beta1, beta2, omb1, omb2, bc1, bc2, eps, lr, wd;   // bc = 1 / (1 - beta^t), R21
   uint32_t bits;
-  int32_t mode;           // 0 Adam core; LANS (R22): 1 = pass 1 (m, v, block sums), 2 = pass 2 (x)
+  int32_t mode;           // 0 Adam core; LANS (R22): 1 = pass 1 (m, v, block sums), 2 = pass 2 (x);
+                          // 3 NAG (R24, velocity in m)
   int32_t f16;            // sparse kinds: binary16 values (R23)
+  float mu;               // NAG momentum (mode 3, R24)
   double* lans_part;      // LANS pass 1: per update tile the pairwise sums of x^2, u^2, w^2
   const float2* lans_coef;  // LANS pass 2: per block (a, b) coefficients
   PeerSync sync;          // fused exchange: wait for the owners' p (pull) ...

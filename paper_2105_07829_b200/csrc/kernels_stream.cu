@@ -91,6 +91,8 @@ __device__ __forceinline__ void lans_uw(float g, float m, float v, float x, cons
 //         x^2, u^2, w^2 (a reducer warp writes p.lans_part[3 tile + q]);
 // MODE 2: u, w recomputed from the stored m, v; x -= lr (a u + b w) with the
 //         tile's block coefficients (p.lans_coef, from lans_coef_kernel).
+// MODE 3: NAG (R24): g = g~ + lambda x, m = mu m + g (m holds the velocity),
+//         x -= lr (g + mu m); v is neither read nor written (16 B/element).
 template <int KIND, bool FUSED, int MODE>
 __global__ void __launch_bounds__(SNT, 1) update_stream(const __grid_constant__ UpdateParams p) {
   extern __shared__ __align__(128) unsigned char sraw[];
@@ -148,11 +150,11 @@ __global__ void __launch_bounds__(SNT, 1) update_stream(const __grid_constant__ 
           hbytes = 16;
         }
         sm.desc[s] = d;
-        mbar_arrive_expect_tx(&sm.full[s], 3 * nvb + pbytes + hbytes);
+        mbar_arrive_expect_tx(&sm.full[s], (MODE == 3 ? 2 : 3) * nvb + pbytes + hbytes);
         if (hbytes) tma_load_1d(&sm.head[s], pay, 16, &sm.full[s]);
         if (nvb) {
           tma_load_1d(sm.m[s], p.m + c.off + tl.start, nvb, &sm.full[s]);
-          tma_load_1d(sm.v[s], p.v + c.off + tl.start, nvb, &sm.full[s]);
+          if (MODE != 3) tma_load_1d(sm.v[s], p.v + c.off + tl.start, nvb, &sm.full[s]);
           tma_load_1d(sm.x[s], p.x + c.off + tl.start, nvb, &sm.full[s]);
         }
         if (pbytes) tma_load_1d(sm.pay[s], psrc, pbytes, &sm.full[s]);
@@ -223,11 +225,11 @@ __global__ void __launch_bounds__(SNT, 1) update_stream(const __grid_constant__ 
       float4 m4 = make_float4(0.f, 0.f, 0.f, 0.f), v4 = m4, x4 = m4;
       if (f < nvec) {
         m4 = sm.m[s][f];
-        v4 = sm.v[s][f];
+        if (MODE != 3) v4 = sm.v[s][f];
         x4 = sm.x[s][f];
       } else if (in) {   // ragged tail of a unit: not covered by the 16-byte bulk copies
         m4 = load4_masked(m, j, d.L);
-        v4 = load4_masked(v, j, d.L);
+        if (MODE != 3) v4 = load4_masked(v, j, d.L);
         x4 = load4_masked(x, j, d.L);
       }
       if (MODE == 0) {
@@ -279,6 +281,22 @@ __global__ void __launch_bounds__(SNT, 1) update_stream(const __grid_constant__ 
           sm.red[s][1][k * CW + warp] = tu;
           sm.red[s][2][k * CW + warp] = tw;
         }
+      } else if (MODE == 3) {   // NAG (R24)
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          const float xx = get(x4, e);
+          const float g = fadd(get(g4, e), fmul(p.wd, xx));
+          const float vel = fadd(fmul(p.mu, get(m4, e)), g);
+          set(m4, e, vel);
+          set(x4, e, fsub(xx, fmul(p.lr, fadd(g, fmul(p.mu, vel)))));
+        }
+        if (f < nvec) {
+          st4(m + j, m4);
+          st4(x + j, x4);
+        } else {
+          store4_masked(m, j, d.L, m4);
+          store4_masked(x, j, d.L, x4);
+        }
       } else {   // MODE 2
 #pragma unroll
         for (int e = 0; e < 4; e++) {
@@ -328,6 +346,8 @@ cudaError_t launch_update_stream(int kind, const UpdateParams& p, int grid, cuda
       case 3: return go(update_stream<K, true, 1>);
       case 4: return go(update_stream<K, false, 2>);
       case 5: return go(update_stream<K, true, 2>);
+      case 6: return go(update_stream<K, false, 3>);
+      case 7: return go(update_stream<K, true, 3>);
     }
     return cudaErrorInvalidValue;
   };

@@ -52,11 +52,11 @@ __global__ void __launch_bounds__(UNT) update_kernel(const __grid_constant__ Upd
     m4[it] = v4[it] = x4[it] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (full) {
       m4[it] = ld4(m + j);
-      v4[it] = ld4(v + j);
+      if (MODE != 3) v4[it] = ld4(v + j);
       x4[it] = ld4(x + j);
     } else if (4 * i4 < tl.len) {
       m4[it] = load4_masked(m, j, L);
-      v4[it] = load4_masked(v, j, L);
+      if (MODE != 3) v4[it] = load4_masked(v, j, L);
       x4[it] = load4_masked(x, j, L);
     }
   }
@@ -163,6 +163,22 @@ __global__ void __launch_bounds__(UNT) update_kernel(const __grid_constant__ Upd
         red[MODE == 1 ? 1 : 0][it * 8 + warp] = tu;
         red[MODE == 1 ? 2 : 0][it * 8 + warp] = tw;
       }
+    } else if (MODE == 3) {   // NAG (R24): velocity in m
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        const float xx = get(x4[it], e);
+        const float g = fadd(get(g4, e), fmul(p.wd, xx));
+        const float vel = fadd(fmul(p.mu, get(m4[it], e)), g);
+        set(m4[it], e, vel);
+        set(x4[it], e, fsub(xx, fmul(p.lr, fadd(g, fmul(p.mu, vel)))));
+      }
+      if (full) {
+        st4(m + j, m4[it]);
+        st4(x + j, x4[it]);
+      } else {
+        store4_masked(m, j, L, m4[it]);
+        store4_masked(x, j, L, x4[it]);
+      }
     } else {   // MODE 2
 #pragma unroll
       for (int e = 0; e < 4; e++) {
@@ -235,7 +251,8 @@ cudaError_t launch_update(int kind, const UpdateParams& p, cudaStream_t s) {
   case K:                                                                \
     if (p.mode == 0) update_kernel<K, 0><<<grid, block, 0, s>>>(p);      \
     else if (p.mode == 1) update_kernel<K, 1><<<grid, block, 0, s>>>(p); \
-    else update_kernel<K, 2><<<grid, block, 0, s>>>(p);                  \
+    else if (p.mode == 2) update_kernel<K, 2><<<grid, block, 0, s>>>(p); \
+    else update_kernel<K, 3><<<grid, block, 0, s>>>(p);                  \
     break;
   switch (kind) {
     BPC_UPD(U_NONE)
