@@ -28,7 +28,7 @@ __device__ __forceinline__ void lans_uw1(float g, float m, float v, float x, con
 // MODE 0: Adam core; LANS (R22) MODE 1: m, v + the tile's pairwise sums of
 // x^2, u^2, w^2 -> p.lans_part; MODE 2: x -= lr (a u + b w)   (see update_stream)
 template <int KIND, int MODE>
-__global__ void __launch_bounds__(UNT) update_kernel(const __grid_constant__ UpdateParams p) {
+__global__ void __launch_bounds__(UNT, 4) update_kernel(const __grid_constant__ UpdateParams p) {
   constexpr bool SPARSE = KIND == U_TOPK || KIND == U_RANDK;
   __shared__ float gts[SPARSE ? UTILE : 1];
   __shared__ double red[MODE == 1 ? 3 : 1][32];
