@@ -323,26 +323,36 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
           // exponents differ by more than 29, and then both roundings return the
           // larger operand.  One fp32 add instead of four conversions.
           const float h = *reinterpret_cast<const float*>(IH(t));
-          const uint32_t* words =
-              d.staged ? reinterpret_cast<const uint32_t*>(I(t) + d.pofs)
-                       : reinterpret_cast<const uint32_t*>(p.recv + d.recv + 4 + (uint64_t)d.start * b / 8);
-          const uint32_t field = KIND == C_SIGN ? ((words[f >> 3] >> ((f & 7) * 4)) & 15u)
-                                                : load_field(words, (uint64_t)b * 4 * f, nb);
+          // staged words are read with shared-memory loads (no generic pointer merge)
+          uint32_t field;
+          if (d.staged) {
+            const uint32_t* words = reinterpret_cast<const uint32_t*>(I(t) + d.pofs);
+            field = KIND == C_SIGN ? ((words[f >> 3] >> ((f & 7) * 4)) & 15u)
+                                   : load_field(words, (uint64_t)b * 4 * f, nb);
+          } else {
+            const uint32_t* words =
+                reinterpret_cast<const uint32_t*>(p.recv + d.recv + 4 + (uint64_t)d.start * b / 8);
+            field = KIND == C_SIGN ? ((words[f >> 3] >> ((f & 7) * 4)) & 15u)
+                                   : load_field(words, (uint64_t)b * 4 * f, nb);
+          }
           const float unit = KIND == C_SIGN ? 0.f : fdiv(h, slv);
+          // sign: h >= +0, and for h = 0 both decodes are +0 (the fp64 sum of the
+          // oracle starts at +0, so -0 never survives): one add per element
+          const float hneg = h == 0.f ? 0.f : -h;
           float4 e4 = make_float4(0.f, 0.f, 0.f, 0.f);
           if (p.use_ef) e4 = inv4 ? val[f] : load4_masked(p.err + d.etl, j, d.L);
 #pragma unroll
           for (int u = 0; u < 4; u++) {
-            float dec;
+            float dsum;
             if (KIND == C_SIGN) {
-              dec = ((field >> u) & 1u) ? h : -h;
+              dsum = fadd(((field >> u) & 1u) ? h : hneg, get(e4, u));
             } else {
               const uint32_t code = (field >> (b * u)) & cmask;
               const float mag = dither_mag<KIND>(code, h, unit, cmax);
-              dec = (code & 1u) ? mag : -mag;
+              // acc = +0.0 + dec (turns -0 into +0, as the fp64 sum does), then + e~
+              dsum = fadd(fadd(0.f, (code & 1u) ? mag : -mag), get(e4, u));
             }
-            // acc = +0.0 + dec (turns -0 into +0, as the fp64 sum does), then + e~
-            if (FULL || j + u < d.L) set(q, u, fadd(fadd(0.f, dec), get(e4, u)));
+            if (FULL || j + u < d.L) set(q, u, dsum);
           }
         } else {
           for (uint32_t r = 0; r < p.n; r++) {
