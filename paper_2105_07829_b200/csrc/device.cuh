@@ -272,6 +272,18 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1
   return c;
 }
 // the 4 words of elements 4*g .. 4*g+3 of unit `chunk` (counter layout R13)
+// the same generator with the 10 round keys precomputed on the host (key
+// schedule k + r * (0x9E3779B9, 0xBB67AE85) mod 2^32): in the kernel parameter
+// space they are constant-bank operands of the xors, no key arithmetic per call
+__device__ __forceinline__ uint4 philox4x32_10_rk(uint4 c, const uint32_t (&rk)[20]) {
+#pragma unroll
+  for (int r = 0; r < 10; r++) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ rk[2 * r], lo1, hi0 ^ c.w ^ rk[2 * r + 1], lo0);
+  }
+  return c;
+}
 __device__ __forceinline__ uint4 rng4(uint64_t seed, uint32_t g, uint32_t chunk, uint32_t t,
                                       uint32_t stage, uint32_t rank) {
   return philox4x32_10(make_uint4(g, chunk, t, (stage << 31) | rank), (uint32_t)seed,

@@ -122,6 +122,7 @@ struct StreamParams {
   uint32_t stage_payload;   // server: stage the n ranks' payload pieces in smem
   uint32_t piece_stride;    // server: bytes per staged piece
   uint32_t nstages, stage_a, stage_b;   // ring geometry (set by the launcher)
+  uint32_t rk[20];          // Philox round keys of the seed (set by the launcher, R13)
   // fused exchange (BPC_EXCHANGE_P2P, n > 1):
   //  worker: ndst = n, the payload of a chunk owned by r goes to dst[r] +
   //          chunk.recv (slot `rank` of r's RECV, IPC-mapped), then signals push;

@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
         const float4 q = val[f];
         uint32_t field = 0;
         if (FULL || j < L) {
-          const uint4 w4 = rng4(p.seed, j >> 2, d.id, p.t, stage_id, rng_rank);
+          const uint4 w4 = philox4x32_10_rk(make_uint4(j >> 2, d.id, p.t, (stage_id << 31) | rng_rank), p.rk);
           float4 ev;
           uint32_t codes[4];
 #pragma unroll
@@ -551,6 +551,10 @@ static cudaError_t launch_cstream_t(int kind, StreamParams p, int grid, cudaStre
   if (p.n_slices == 0) return cudaSuccess;
   size_t smem;
   cstream_geometry(SERVER, p, &p.stage_a, &p.stage_b, &p.nstages, &smem);
+  for (int r = 0; r < 10; r++) {   // Philox4x32-10 key schedule of the seed (R13)
+    p.rk[2 * r] = (uint32_t)p.seed + (uint32_t)r * 0x9E3779B9u;
+    p.rk[2 * r + 1] = (uint32_t)(p.seed >> 32) + (uint32_t)r * 0xBB67AE85u;
+  }
   if (p.nstages < 3) return cudaErrorInvalidConfiguration;   // deferral >= 1 needs 3 held stages
   auto go = [&](auto fn) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
