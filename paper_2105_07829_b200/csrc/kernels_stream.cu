@@ -63,7 +63,7 @@ struct __align__(128) USmem {
   UDesc desc[UST];
   uint64_t full[UST], empty[UST];
   uint64_t sums[UST];             // LANS pass 1: the consumers' warp subtrees of stage s are in red[s]
-  double red[UST][3][2 * CW];     // LANS pass 1: 128-element subtrees of x^2, u^2, w^2
+  double red[UST][3][UTILE / 16];  // LANS pass 1: 16-element subtrees of x^2, u^2, w^2
 };
 
 __device__ __forceinline__ void adam1s(float g, float& m, float& v, float& x, const UpdateParams& p) {
@@ -169,8 +169,10 @@ __global__ void __launch_bounds__(SNT, 1) update_stream(const __grid_constant__ 
         mbar_wait(&sm.sums[s], (i / UST) & 1);
         const uint32_t tile = sm.desc[s].tile;
 #pragma unroll
-        for (int q = 0; q < 3; q++) {   // tile total: pairwise tree over its 32 subtrees (R6)
-          const double t = warp_tree(sm.red[s][q][lane]);
+        for (int q = 0; q < 3; q++) {   // tile total: pairwise tree over its 256 subtrees (R6)
+          const double* r8 = &sm.red[s][q][8 * lane];   // lane l: elements [128 l, 128 l + 128)
+          const double a = ((r8[0] + r8[1]) + (r8[2] + r8[3])) + ((r8[4] + r8[5]) + (r8[6] + r8[7]));
+          const double t = warp_tree(a);
           if (lane == 0) p.lans_part[3ull * tile + q] = t;
         }
         __syncwarp();
@@ -272,14 +274,20 @@ __global__ void __launch_bounds__(SNT, 1) update_stream(const __grid_constant__ 
             store4_masked(v, j, d.L, v4);
           }
         }
-        // subtree m = k * CW + warp covers tile elements [128 m, 128 m + 128)
-        const double tx = warp_tree(leaf4_sq(x4));
-        const double tu = warp_tree(leaf4_sq(u4));
-        const double tw = warp_tree(leaf4_sq(w4));
-        if (lane == 0) {
-          sm.red[s][0][k * CW + warp] = tx;
-          sm.red[s][1][k * CW + warp] = tu;
-          sm.red[s][2][k * CW + warp] = tw;
+        // two butterfly levels: lanes 4q hold the 16-element subtree 8 (k CW + warp) + q
+        // of tile elements [16 i, 16 i + 16); the reducer warp completes the tree
+        double tx = leaf4_sq(x4), tu = leaf4_sq(u4), tw = leaf4_sq(w4);
+#pragma unroll
+        for (int o = 1; o < 4; o <<= 1) {
+          tx = tx + __shfl_xor_sync(0xffffffffu, tx, o);
+          tu = tu + __shfl_xor_sync(0xffffffffu, tu, o);
+          tw = tw + __shfl_xor_sync(0xffffffffu, tw, o);
+        }
+        if ((lane & 3) == 0) {
+          const uint32_t i16 = 8 * (k * CW + warp) + (lane >> 2);
+          sm.red[s][0][i16] = tx;
+          sm.red[s][1][i16] = tu;
+          sm.red[s][2][i16] = tw;
         }
       } else if (MODE == 3) {   // NAG (R24)
 #pragma unroll
