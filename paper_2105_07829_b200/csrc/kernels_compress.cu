@@ -605,7 +605,13 @@ __device__ void emit_sparse(const CompressParams& p, const DevChunk& c, Smem& sm
         for (uint32_t a = threadIdx.x; a < cnt; a += NT) {
           const uint32_t ka = sm.fh[a];
           uint32_t gt = 0, eq = 0;
-          for (uint32_t b2 = 0; b2 < cnt; b2++) {
+          uint32_t b2 = 0;
+          for (; b2 + 4 <= cnt; b2 += 4) {   // 4 keys per shared-memory broadcast
+            const uint4 kb = *reinterpret_cast<const uint4*>(&sm.fh[b2]);
+            gt += (kb.x > ka) + (kb.y > ka) + (kb.z > ka) + (kb.w > ka);
+            eq += (kb.x == ka) + (kb.y == ka) + (kb.z == ka) + (kb.w == ka);
+          }
+          for (; b2 < cnt; b2++) {
             const uint32_t kb = sm.fh[b2];
             gt += kb > ka;
             eq += kb == ka;
