@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--optimizer", choices=["adam", "lans", "nag"], default="adam",
                     help="bpc_step update: Adam core (A9), the LANS / CLAN block-normalised update (NEXT #1) "
                          "or NAG (the CNN runs' optimizer, R24)")
+    ap.add_argument("--units", choices=["chunk", "tensor"], default="chunk",
+                    help="compression unit: 2^18-element chunks (R1) or whole tensors (PAPER.md:505, "
+                         "two-pass kernels; norm-based compressors only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -252,7 +255,8 @@ def run_ours(args):
     import paper_2105_07829_b200 as bpc
     from workloads import config, gen_grad_torch, gen_params, layout
 
-    w = config(args.config, n=world, optimizer=args.optimizer)
+    w = config(args.config, n=world, optimizer=args.optimizer,
+               **({"chunk_elems": 0} if args.units == "tensor" else {}))
     numels = w.tensor_numels()
     offs, D = layout(numels)
     d = sum(numels)
@@ -400,7 +404,7 @@ def run_ours(args):
                        "l2": "inputs larger than L2 (g, e, m, v, x = %.0f MB per rank)" % (20 * D / 1e6),
                        "parallelism": f"dp{world} (sharded server: all-to-all + all-gather)",
                        "exchange": ctx.exchange if world > 1 else None,
-                       "optimizer": args.optimizer},
+                       "optimizer": args.optimizer, "units": args.units},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                          "traffic_source": traffic_src, "peak_source": peak_src,

@@ -103,6 +103,11 @@ typedef struct {
   float lans_alpha_l, lans_alpha_u;  /* LANS: phi(z) = min(max(z, alpha_l), alpha_u),
                                         0 < alpha_l <= alpha_u */
   float momentum;                /* NAG: mu in [0, 1) */
+  int32_t unit_mode;             /* compression unit: 0 = chunks of chunk_elems (R1); 1 = one unit
+                                    per tensor, the paper's granularity (NEXT #4),
+                                    scaled sign / dithering / NONE only, tensors <= 2^27 elements:
+                                    worker and server then run two passes (slice partials, a
+                                    per-unit tree, the emitting pass; 20 B/element for onebit+EF) */
 } bpc_config;
 
 /* The update of bpc_step (A9).

@@ -22,9 +22,11 @@ def context_for(wcfg, *, rank=0, world_size=None, device=0, stream=None, nccl_id
     offs, _ = layout(numels)
     if stream is None:
         stream = torch.cuda.current_stream(device).cuda_stream
+    # chunk_elems = 0 is the oracle's per-tensor unit: unit_mode 1
     cfg = make_config(numels, offs, wcfg.comp, world_size=wcfg.n if world_size is None else world_size,
                       rank=rank, device=device, stream=stream, nccl_id=nccl_id, seed=wcfg.seed,
-                      chunk_elems=wcfg.chunk_elems, threshold_bytes=wcfg.threshold_bytes, beta1=wcfg.beta1,
+                      chunk_elems=wcfg.chunk_elems or (1 << 18), unit_mode=1 if wcfg.chunk_elems == 0 else 0,
+                      threshold_bytes=wcfg.threshold_bytes, beta1=wcfg.beta1,
                       beta2=wcfg.beta2, eps=wcfg.eps, weight_decay=wcfg.weight_decay,
                       check_finite=check_finite, exchange={"p2p": 0, "nccl": 1}[exchange],
                       optimizer={"adam": 0, "lans": 1, "nag": 2}[getattr(wcfg, "optimizer", "adam")],

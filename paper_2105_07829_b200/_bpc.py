@@ -44,7 +44,8 @@ class Config(C.Structure):
                 ("size_threshold_bytes", C.c_uint64), ("comp", Compressor), ("beta1", C.c_float),
                 ("beta2", C.c_float), ("eps", C.c_float), ("weight_decay", C.c_float),
                 ("check_finite", C.c_int32), ("exchange", C.c_int32), ("optimizer", C.c_int32),
-                ("lans_alpha_l", C.c_float), ("lans_alpha_u", C.c_float), ("momentum", C.c_float)]
+                ("lans_alpha_l", C.c_float), ("lans_alpha_u", C.c_float), ("momentum", C.c_float),
+                ("unit_mode", C.c_int32)]
 
 
 class ChunkInfo(C.Structure):
@@ -114,7 +115,7 @@ def unique_id() -> bytes:
 def make_config(numels, offsets, comp, *, world_size=1, rank=0, device=0, stream=0, nccl_id=None,
                 seed=0, chunk_elems=1 << 18, threshold_bytes=1 << 20, beta1=0.9, beta2=0.999, eps=1e-6,
                 weight_decay=0.0, check_finite=0, exchange=0, optimizer=0, lans_alpha_l=0.01,
-                lans_alpha_u=10.0, momentum=0.9):
+                lans_alpha_u=10.0, momentum=0.9, unit_mode=0):
     numel = np.ascontiguousarray(numels, dtype=np.uint64)
     offset = np.ascontiguousarray(offsets, dtype=np.uint64)
     idbuf = (C.c_uint8 * 128).from_buffer_copy(nccl_id) if nccl_id is not None else None
@@ -124,7 +125,7 @@ def make_config(numels, offsets, comp, *, world_size=1, rank=0, device=0, stream
                  Compressor(comp.kind, comp.k_num, comp.k_den, comp.bits, comp.randk_scaled, comp.use_ef,
                             getattr(comp, "f16", 0)),
                  beta1, beta2, eps, weight_decay, check_finite, exchange, optimizer, lans_alpha_l,
-                 lans_alpha_u, momentum)
+                 lans_alpha_u, momentum, unit_mode)
     cfg._keep = (numel, offset, idbuf)   # keep the arrays alive with the struct
     return cfg
 

@@ -96,6 +96,9 @@ bpc_status make_plan(const bpc_config* cfg, Plan* P, std::string* err) {
     return fail(BPC_ERR_INVALID_ARGUMENT, "NAG momentum must lie in [0, 1)");
   if (cfg->optimizer == BPC_OPT_LANS && !(cfg->lans_alpha_l > 0.f && cfg->lans_alpha_l <= cfg->lans_alpha_u))
     return fail(BPC_ERR_INVALID_ARGUMENT, "LANS needs 0 < alpha_l <= alpha_u");
+  if (cfg->unit_mode != 0 && cfg->unit_mode != 1) return fail(BPC_ERR_INVALID_ARGUMENT, "unit_mode is 0 or 1");
+  if (cfg->unit_mode == 1 && !stream_worker(C.kind))
+    return fail(BPC_ERR_UNSUPPORTED_KIND, "per-tensor units: scaled sign, dithering or NONE only");
   uint64_t ce = cfg->chunk_elems ? cfg->chunk_elems : (1ull << 18);
   if (ce < kSlice || ce > 16 * kSlice || (ce & (ce - 1)))
     return fail(BPC_ERR_INVALID_ARGUMENT, "chunk_elems must be a power of two in [2^14, 2^18]");
@@ -107,6 +110,8 @@ bpc_status make_plan(const bpc_config* cfg, Plan* P, std::string* err) {
     const uint64_t L = cfg->tensor_numel[t], o = cfg->tensor_offset[t];
     if (L == 0) return fail(BPC_ERR_EMPTY_BLOCK, "tensor with numel 0");
     if (L >= (1ull << 31)) return fail(BPC_ERR_INVALID_ARGUMENT, "tensor numel >= 2^31");
+    if (cfg->unit_mode == 1 && L > (uint64_t)kStreamSlice * UNIT_MAX_SLICES)
+      return fail(BPC_ERR_INVALID_ARGUMENT, "per-tensor unit larger than 2^27 elements");
     if (cfg->optimizer == BPC_OPT_LANS && L > 4096ull * LANS_MAX_TILES)
       return fail(BPC_ERR_INVALID_ARGUMENT, "LANS block (tensor) larger than 2^25 elements");
     if (o % 4) return fail(BPC_ERR_INVALID_ARGUMENT, "tensor offsets must be multiples of 4 elements");
@@ -122,7 +127,7 @@ bpc_status make_plan(const bpc_config* cfg, Plan* P, std::string* err) {
   for (uint32_t t = 0; t < cfg->num_tensors; t++) {
     const uint64_t L = cfg->tensor_numel[t];
     const bool raw = (4 * L < cfg->size_threshold_bytes) || C.kind == BPC_NONE;
-    const uint64_t unit = raw ? L : ce;
+    const uint64_t unit = (raw || cfg->unit_mode == 1) ? L : ce;   // per-tensor units
     for (uint64_t s = 0; s < L; s += unit) {
       bpc_chunk_info ci = {};
       ci.tensor = t;
@@ -236,6 +241,10 @@ struct bpc_ctx {
   uint32_t push_epoch = 0, pull_epoch = 0;
   // LANS (BPC_OPT_LANS): per update tile partial sums, per block coefficients
   double* d_lans_part = nullptr;
+  // per-tensor units (unit_mode 1): per side, unit tables and totals
+  uint32_t *d_wufirst = nullptr, *d_wuns = nullptr, *d_sufirst = nullptr, *d_suns = nullptr;
+  double *d_wutotal = nullptr, *d_sutotal = nullptr;
+  uint32_t n_wunits = 0, n_sunits = 0;
   float2* d_lans_coef = nullptr;
   uint32_t* d_blk_tile = nullptr;
   int push_grid = 1, pull_grid = 1;
@@ -297,7 +306,9 @@ void free_ctx(bpc_ctx* ctx) {
   for (int r = 0; r < (int)ctx->peer_flags.size(); r++)
     if (ctx->peer_flags[r] && r != ctx->cfg.rank) cudaIpcCloseMemHandle(ctx->peer_flags[r]);
   if (ctx->d_xflags) cudaFree(ctx->d_xflags);
-  for (void* q : {(void*)ctx->d_lans_part, (void*)ctx->d_lans_coef, (void*)ctx->d_blk_tile})
+  for (void* q : {(void*)ctx->d_lans_part, (void*)ctx->d_lans_coef, (void*)ctx->d_blk_tile,
+                  (void*)ctx->d_wufirst, (void*)ctx->d_wuns, (void*)ctx->d_sufirst, (void*)ctx->d_suns,
+                  (void*)ctx->d_wutotal, (void*)ctx->d_sutotal})
     if (q) cudaFree(q);
   if (ctx->d_xdone) cudaFree(ctx->d_xdone);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
@@ -424,6 +435,33 @@ void set_signal(bpc_ctx* ctx, PeerSync* s, int which, uint32_t epoch) {
   for (int r = 0; r < n; r++) s->sflag[r] = r == rank ? nullptr : ctx->peer_flags[r];
   s->sslot = (uint32_t)(which * n + rank);
   s->sepoch = epoch;
+}
+
+// Streaming worker / server launch: one pass, or (per-tensor units) partials,
+// unit tree, then the emitting pass
+cudaError_t launch_stream_side(bpc_ctx* ctx, bool server, StreamParams& q) {
+  const int kind = ctx->cfg.comp.kind;
+  auto go = [&]() { return server ? launch_server_stream(kind, q, ctx->num_sms, ctx->stream)
+                                  : launch_worker_stream(kind, q, ctx->num_sms, ctx->stream); };
+  if (ctx->cfg.unit_mode != 1) {
+    q.pass = 0;
+    ctx->launches++;
+    return go();
+  }
+  UnitTreeParams ut = {};
+  ut.part = q.partials;
+  ut.first = server ? ctx->d_sufirst : ctx->d_wufirst;
+  ut.ns = server ? ctx->d_suns : ctx->d_wuns;
+  ut.nunits = server ? ctx->n_sunits : ctx->n_wunits;
+  ut.total = server ? ctx->d_sutotal : ctx->d_wutotal;
+  q.pass = 1;
+  cudaError_t e = go();
+  if (e == cudaSuccess) e = launch_unit_tree(ut, ctx->stream);
+  q.pass = 2;
+  q.unit_total = ut.total;
+  if (e == cudaSuccess) e = go();
+  ctx->launches += 3;
+  return e;
 }
 
 CompressParams base_params(bpc_ctx* ctx) {
@@ -598,6 +636,7 @@ bpc_status bpc_init(const bpc_config* cfg, bpc_ctx** out) {
   // (the server's: only the units this rank owns)
   for (int side = 0; side < 2; side++) {
     std::vector<Slice> sl;
+    std::vector<uint32_t> ufirst, uns;
     uint32_t units = 0, parts = 0;
     for (uint32_t c = 0; c < P.chunks.size(); c++) {
       const auto& ci = P.chunks[c];
@@ -609,6 +648,8 @@ bpc_status bpc_init(const bpc_config* cfg, bpc_ctx** out) {
         sl.push_back(x);
       }
       if (!ci.raw && ns > 1) {
+        ufirst.push_back(parts);
+        uns.push_back(ns);
         units++;
         parts += ns;
       }
@@ -620,6 +661,13 @@ bpc_status bpc_init(const bpc_config* cfg, bpc_ctx** out) {
     (side ? ctx->n_sslices : ctx->n_wslices) = (uint32_t)sl.size();
     if ((ce = alloc((void**)dp, 8ull * parts)) != cudaSuccess) return bail(cuda_fail(ctx, ce, "alloc partials"));
     if ((ce = alloc((void**)dc, 8ull * units)) != cudaSuccess) return bail(cuda_fail(ctx, ce, "alloc counters"));
+    if (cfg->unit_mode == 1) {
+      if ((s = upload(ctx, side ? &ctx->d_sufirst : &ctx->d_wufirst, ufirst)) != BPC_OK) return bail(s);
+      if ((s = upload(ctx, side ? &ctx->d_suns : &ctx->d_wuns, uns)) != BPC_OK) return bail(s);
+      if ((ce = alloc((void**)(side ? &ctx->d_sutotal : &ctx->d_wutotal), 8ull * units)) != cudaSuccess)
+        return bail(cuda_fail(ctx, ce, "alloc unit totals"));
+      (side ? ctx->n_sunits : ctx->n_wunits) = units;
+    }
   }
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cfg->device);
   // the cluster shape must be schedulable
@@ -679,7 +727,7 @@ bpc_status bpc_compress(bpc_ctx* ctx, const float* d_grad) {
         q.dst[r] = ctx->peer_recv[r] + (uint64_t)ctx->cfg.rank * P.seg_bytes[r];
       set_signal(ctx, &q.sync, 0, ++ctx->push_epoch);
     }
-    CK(launch_worker_stream(ctx->cfg.comp.kind, q, ctx->num_sms, ctx->stream), "worker stream launch");
+    CK(launch_stream_side(ctx, false, q), "worker stream launch");
   } else {
     CompressParams p = base_params(ctx);
     p.grad = d_grad;
@@ -691,9 +739,9 @@ bpc_status bpc_compress(bpc_ctx* ctx, const float* d_grad) {
     p.n_raw_tiles = ctx->n_wraw;
     p.stage = 0;
     CK(launch_compress(ctx->cfg.comp.kind, false, p, ctx->stream), "worker compress launch");
+    ctx->launches++;
   }
   timer_end(ctx, BPC_TIMER_COMPRESS, b);
-  ctx->launches++;
   ctx->phase = 1;
   return BPC_OK;
 }
@@ -797,7 +845,7 @@ bpc_status bpc_server(bpc_ctx* ctx) {
         CK(launch_p2p_copy(e, 1, ctx->stream), "pull signal launch");
       }
     }
-    CK(launch_server_stream(ctx->cfg.comp.kind, q, ctx->num_sms, ctx->stream), "server stream launch");
+    CK(launch_stream_side(ctx, true, q), "server stream launch");
   } else {
     CompressParams p = base_params(ctx);
     p.recv = ctx->recv;
@@ -810,9 +858,9 @@ bpc_status bpc_server(bpc_ctx* ctx) {
     p.n_raw_tiles = ctx->n_sraw;
     p.stage = 1;
     CK(launch_compress(ctx->cfg.comp.kind, true, p, ctx->stream), "server launch");
+    ctx->launches++;
   }
   timer_end(ctx, BPC_TIMER_SERVER, b);
-  ctx->launches++;
   ctx->phase = 3;
   return BPC_OK;
 }

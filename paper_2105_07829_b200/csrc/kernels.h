@@ -123,6 +123,11 @@ struct StreamParams {
   uint32_t piece_stride;    // server: bytes per staged piece
   uint32_t nstages, stage_a, stage_b;   // ring geometry (set by the launcher)
   uint32_t rk[20];          // Philox round keys of the seed (set by the launcher, R13)
+  // per-tensor units (NEXT #4): two passes.  pass 0: single pass
+  // (units <= 32 slices, cross-CTA unit totals); pass 1: produce + publish the
+  // slice partials only; pass 2: produce again and emit with unit_total[unit]
+  uint32_t pass;
+  const double* unit_total;
   // fused exchange (BPC_EXCHANGE_P2P, n > 1):
   //  worker: ndst = n, the payload of a chunk owned by r goes to dst[r] +
   //          chunk.recv (slot `rank` of r's RECV, IPC-mapped), then signals push;
@@ -163,6 +168,18 @@ struct LansCoefParams {
 };
 cudaError_t launch_lans_coef(const LansCoefParams& p, cudaStream_t s);
 constexpr uint32_t LANS_MAX_TILES = 8192;   // tiles per block (2^25 elements)
+
+// per-tensor units: unit u's total = pairwise tree over its slice partials
+// part[first[u] .. first[u] + ns[u]) padded to a power of two (R6)
+struct UnitTreeParams {
+  const double* part;
+  const uint32_t* first;
+  const uint32_t* ns;
+  uint32_t nunits;
+  double* total;
+};
+cudaError_t launch_unit_tree(const UnitTreeParams& p, cudaStream_t s);
+constexpr uint32_t UNIT_MAX_SLICES = 16384;   // 2^27 elements per unit
 
 // host launchers (return the launch error)
 cudaError_t launch_p2p_copy(const P2PParams& p, int grid, cudaStream_t s);

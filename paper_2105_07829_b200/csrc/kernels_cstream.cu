@@ -242,7 +242,11 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
       // needs this reducer's tready arrive for slice i first.
       mbar_wait_backoff(&hd.pready[hs], (i / NH) & 1, 200, 0x2000000u | i);
       const uint32_t ns = hd.desc[hs].nslices;
-      if (ns > 1) {
+      if (ns > 1 && p.pass == 1) {   // per-tensor units, pass 1: publish the partial only
+        if (lane == 0) p.partials[hd.desc[hs].unit_first + hd.desc[hs].sidx] = hd.part[hs];
+      } else if (ns > 1 && p.pass == 2) {   // pass 2: the unit's total from unit_tree_kernel
+        if (lane == 0) hd.total[hs] = __ldcg(p.unit_total + hd.desc[hs].unit);
+      } else if (ns > 1) {
         if (lane == 0) {
           // publish this slice's partial, then wait for the unit's other slices
           const CDesc& d = hd.desc[hs];
@@ -512,14 +516,19 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
       // recycled: keeps each mbarrier at most one phase ahead of its waiters
       mbar_wait(&hd.tready[hs], (ie / NH) & 1, 0x5000000u | ie);
       const double total = hd.total[hs];
-      if (d.len == CSL) emit(BoolC<true>{}, d, H(hs), pay, total);
-      else emit(BoolC<false>{}, d, H(hs), pay, total);
+      if (p.pass == 1) {
+        // per-tensor units, pass 1: nothing to emit (pass 2 re-produces the slice)
+      } else if (d.len == CSL) {
+        emit(BoolC<true>{}, d, H(hs), pay, total);
+      } else {
+        emit(BoolC<false>{}, d, H(hs), pay, total);
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive1(&hd.emptyH[hs]);   // this warp is done with held stage hs
     }
   }
   if (bad) atomicOr(p.flag, 1u);
-  if (FUSED) {   // fused exchange: release this step's payload bytes to the peers
+  if (FUSED && p.pass != 1) {   // fused exchange: release this step's payload bytes to the peers
     __threadfence_system();
     cons_sync();
     peer_signal(p.sync, threadIdx.x == 0);
@@ -586,6 +595,32 @@ static cudaError_t launch_cstream_t(int kind, StreamParams p, int grid, cudaStre
 }
 
 size_t cstream_smem() { return sizeof(CHead); }
+
+// per-tensor units: one CTA per unit sums its slice partials in pairwise order
+// over the slice count padded to a power of two (slices are 8192-aligned in the
+// unit, so this is R6's tree of the padded unit)
+__global__ void __launch_bounds__(1024) unit_tree_kernel(const __grid_constant__ UnitTreeParams p) {
+  extern __shared__ double acc[];   // [UNIT_MAX_SLICES]
+  const uint32_t u = blockIdx.x, first = p.first[u], T = p.ns[u];
+  uint32_t P = 1;
+  while (P < T) P <<= 1;
+  for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) acc[i] = i < T ? p.part[first + i] : 0.0;
+  __syncthreads();
+  for (uint32_t st = 1; st < P; st <<= 1) {
+    for (uint32_t i = threadIdx.x * 2 * st; i < P; i += blockDim.x * 2 * st) acc[i] = acc[i] + acc[i + st];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) p.total[u] = acc[0];
+}
+
+cudaError_t launch_unit_tree(const UnitTreeParams& p, cudaStream_t s) {
+  if (p.nunits == 0) return cudaSuccess;
+  const size_t smem = sizeof(double) * UNIT_MAX_SLICES;
+  cudaError_t e = cudaFuncSetAttribute(unit_tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  unit_tree_kernel<<<p.nunits, 1024, smem, s>>>(p);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_worker_stream(int kind, const StreamParams& p, int grid, cudaStream_t st) {
   return launch_cstream_t<false>(kind, p, grid, st);
