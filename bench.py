@@ -114,10 +114,11 @@ class Clocks:
 
 
 # ---------------------------------------------------------------- byte models
-def kernel_bytes(chunks, comp, n, rank, lans=False, nag=False):
+def kernel_bytes(chunks, comp, n, rank, lans=False, nag=False, per_tensor=False):
     """Algorithmic HBM bytes per launch of each kernel; LANS's
     update = pass 1 (m, v, x read, m, v written) + pass 2 (m, v, x read, x
-    written) + the payload read twice."""
+    written) + the payload read twice; per-tensor units read the worker's
+    g, e (server: e~ and the payloads) once more in their first pass."""
     ef = comp.use_ef
     w = s = u = 0
     for c in chunks:
@@ -128,9 +129,9 @@ def kernel_bytes(chunks, comp, n, rank, lans=False, nag=False):
                 s += 4 * n * L + 4 * L
             u += (36 * L + 8 * L) if lans else (16 * L + 4 * L) if nag else (24 * L + 4 * L)
         else:
-            w += (12 if ef else 4) * L + pb
+            w += (12 if ef else 4) * L + pb + ((8 if ef else 4) * L if per_tensor else 0)
             if c.owner == rank:
-                s += n * pb + (8 * L if ef else 0) + pb
+                s += n * pb + (8 * L if ef else 0) + pb + ((4 * L if ef else 0) + n * pb if per_tensor else 0)
             u += (36 * L + 2 * pb) if lans else (16 * L + pb) if nag else (24 * L + pb)
     return {"compress": w, "server": s, "update": u}
 
@@ -314,7 +315,8 @@ def run_ours(args):
     barrier()
     tim = ctx.timing()
     ctx.set_timing(False)
-    kb = kernel_bytes(chunks, w.comp, world, rank, lans=args.optimizer == "lans", nag=args.optimizer == "nag")
+    kb = kernel_bytes(chunks, w.comp, world, rank, lans=args.optimizer == "lans", nag=args.optimizer == "nag",
+                      per_tensor=args.units == "tensor")
     per = {k: (tim[k][0] / max(1, tim[k][1]), tim[k][1]) for k in ("compress", "server", "update", "push", "pull")}
     dom = max(("compress", "server", "update"), key=lambda k: per[k][0])
     peak, peak_src = peaks()
