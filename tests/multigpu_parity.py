@@ -25,6 +25,8 @@ CASES = {
     "ldither": Comp(LINEAR_DITHER, bits=7, use_ef=0),
     "lans_onebit": Comp(SCALED_SIGN, use_ef=1),   # + the LANS update (NEXT #1)
     "lans_topk": Comp(TOP_K, 1, 1000, use_ef=1),
+    "units_onebit": Comp(SCALED_SIGN, use_ef=1),   # per-tensor units (two-pass kernels)
+    "nag_topk": Comp(TOP_K, 1, 1000, use_ef=1, f16=1),
 }
 SHAPES = (1000, 300000, 70000, 262147, 5, 600000)
 
@@ -43,7 +45,8 @@ def main():
     exchange = sys.argv[2] if len(sys.argv) > 2 else "p2p"
     for name in names:
         w = Config("mg", "custom", CASES[name], numels=SHAPES, n=world,
-                   optimizer="lans" if name.startswith("lans") else "adam")
+                   optimizer="lans" if name.startswith("lans") else "nag" if name.startswith("nag") else "adam",
+                   chunk_elems=0 if name.startswith("units") else 1 << 18)
         offs, D = layout(w.tensor_numels())
         obj = [bpc.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
@@ -74,7 +77,7 @@ def main():
             slot = ctx.summary().recv_slot_bytes
             # the fused exchange (p2p, norm-based kinds) stores payloads straight into the
             # owners' RECV and never writes SEND
-            check_send = exchange == "nccl" or name in ("topk", "randk", "lans_topk")
+            check_send = exchange == "nccl" or name in ("topk", "randk", "lans_topk", "nag_topk")
             # ... and leaves p in its owner's P (the update kernels read it over NVLink)
             check_all_p = check_send
             pb = ctx.copy_state(bpc.BUF_P)

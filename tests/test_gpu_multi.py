@@ -34,5 +34,5 @@ def test_multi_parity(n, exchange):
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
     for rank in range(n):
-        for name in ("onebit", "topk", "randk", "ldither", "lans_onebit", "lans_topk"):
+        for name in ("onebit", "topk", "randk", "ldither", "lans_onebit", "lans_topk", "units_onebit", "nag_topk"):
             assert f"RANK {rank} {name} OK" in out, out[-4000:]
