@@ -417,6 +417,15 @@ def run_ours(args):
             "gpu_launches": launches,
             "clocks": clk,
         }
+        if world > 1:
+            # NVLink traffic of the exchange, per GPU and direction: the worker sends
+            # the other owners' segments (push), the update reads the other owners'
+            # p (pull); averaged over the step it is a small fraction of 900 GB/s
+            seg = [ctx.peer_segment(r)[1] for r in range(world)]
+            per_dir = sum(b for r, b in enumerate(seg) if r != rank)
+            line["nvlink"] = {"bytes_per_step_per_direction": per_dir,
+                              "avg_GBps_per_direction": round(per_dir / (ms * 1e-3) / 1e9, 3),
+                              "peak_GBps_per_direction": 900.0}
         print(json.dumps(line), flush=True)
     ctx.finalize()
     if world > 1:
