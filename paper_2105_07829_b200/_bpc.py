@@ -236,6 +236,10 @@ class Context:
         _check(lib().bpc_get_exchange(self.h, C.byref(m)), self.h)
         return EXCHANGE_NAMES[m.value]
 
+    def set_step(self, t: int):
+        """Resume at optimizer step t (after load_state of e, e~, m, v)."""
+        _check(lib().bpc_set_step(self.h, t), self.h)
+
     @property
     def t(self) -> int:
         t = C.c_uint32()
