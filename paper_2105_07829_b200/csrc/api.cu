@@ -670,12 +670,14 @@ bpc_status bpc_init(const bpc_config* cfg, bpc_ctx** out) {
     }
   }
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cfg->device);
-  // the cluster shape must be schedulable
-  int maxc = 0;
-  ce = compress_max_active_clusters(cfg->comp.kind, false, P.cs, &maxc);
-  if (ce != cudaSuccess || maxc < 1) {
-    ctx->err = "cluster of " + std::to_string(P.cs) + " CTAs is not schedulable";
-    return bail(BPC_ERR_CUDA);
+  // the sparse kinds' cluster shape must be schedulable
+  if (!stream_worker(cfg->comp.kind)) {
+    int maxc = 0;
+    ce = compress_max_active_clusters(cfg->comp.kind, false, P.cs, &maxc);
+    if (ce != cudaSuccess || maxc < 1) {
+      ctx->err = "cluster of " + std::to_string(P.cs) + " CTAs is not schedulable";
+      return bail(BPC_ERR_CUDA);
+    }
   }
   if ((ce = cudaDeviceSynchronize()) != cudaSuccess) return bail(cuda_fail(ctx, ce, "init sync"));
   // NCCL communicator (collective over all ranks)

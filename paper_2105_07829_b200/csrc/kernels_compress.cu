@@ -1,24 +1,24 @@
 // kernels_compress.cu — worker compress and server
-// decompress-sum-recompress (A5-A7) kernels for sm_100a.
+// decompress-sum-recompress (A5-A7) for the sparse kinds, top-k (R9) and
+// random-k (R10), on sm_100a.
 //
 // One thread-block cluster per compression unit (chunk of <= cs * 2^14
 // elements, R1): CTA r of the cluster owns slice
 // [r * 2^14, (r + 1) * 2^14) of the unit and keeps it on chip (64 KB of shared
-// memory) between the unit-wide reduction and the write-back, so every HBM
+// memory) between the unit-wide selection and the write-back, so every HBM
 // byte is read and written once:
 //   worker  q = g + e (Alg. 4 l.5) -> C(q) (l.6) -> e = q - dec (l.7)
 //   server  Delta = (1/n) sum_i dec(delta_i) + e~ (l.10)
 //           -> p = C(Delta) (l.11) -> e~ = Delta - dec(p) (l.13)
-// The unit-wide fp64 reduction (the ||.||_1 of the scaled sign, PAPER.md:318,
-// or the ||.||_2 of dithering) follows the pairwise tree of DESIGN.md R6:
-// lane -> warp butterfly -> CTA -> cluster over DSMEM.  Top-k / random-k run a
-// cluster-wide 4 x 8-bit radix select (R9, R10) and an ordered compaction.
-// Raw (below-threshold) units ride the same launch as plain tiles.
+// The exact selection of the k largest keys runs over the cluster through
+// DSMEM (histogram bins, candidate gather, tie cut), with a
+// 4 x 8-bit radix select as the fallback.  Raw (below-threshold) units ride the
+// same launch as plain tiles.  The norm-based kinds run in kernels_cstream.cu.
 #include "device.cuh"
 
 namespace bpc {
 
-enum { K_NONE = 0, K_SIGN = 2, K_TOPK = 3, K_RANDK = 4, K_LDITHER = 5, K_NDITHER = 6 };
+enum { K_TOPK = 3, K_RANDK = 4 };
 
 constexpr int FNB = 1024;   // bins of the sparse kinds' 10-bit key histogram
 constexpr int FCAP = FNB / 2;   // candidate capacity: CTA 0 keeps (key, index) pairs in fh
@@ -27,7 +27,6 @@ constexpr int SELCAP = 512;     // small-k emit: a CTA's selected (index, value)
 struct __align__(16) Smem {
   float4 q[SLICE / 4];      // the slice of q (worker) or Delta (server)
   union {
-    double red[128];        // dense kinds: warp subtree sums
     uint32_t fh[FNB];       // sparse kinds: 10-bit key histogram (DSMEM), then CTA 0's candidate
                             // keys [0, FCAP) and their indices [FCAP, 2 FCAP)
   };
@@ -38,8 +37,6 @@ struct __align__(16) Smem {
       uint32_t tot[256];
     };
   };
-  double part;              // this slice's subtree sum (read through DSMEM)
-  double total;             // unit total
   uint32_t cnt[2];          // (#key > T, #key == T) of this slice (DSMEM); small k: cnt[0] = #selected
   uint32_t scan[NWARP + 1];
   uint32_t info[8];
@@ -70,34 +67,6 @@ __device__ __forceinline__ void slice_wait(Smem& sm) {
 
 size_t compress_smem_bytes() { return sizeof(Smem); }
 
-// ---------------------------------------------------------------- reductions
-// The producers left in sm.red[m] the subtree sum of slice elements
-// [128 m, 128 m + 128) (m = it * NWARP + warp, see leaf_to_red).
-__device__ __forceinline__ double cluster_tree_total(Smem& sm, uint32_t cs) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __syncthreads();
-  if (warp == 0) {
-    double r = (sm.red[4 * lane] + sm.red[4 * lane + 1]) + (sm.red[4 * lane + 2] + sm.red[4 * lane + 3]);
-    r = warp_tree(r);
-    if (lane == 0) sm.part = r;
-  }
-  cluster_sync_all();   // publish every slice's sum to the cluster
-  if (threadIdx.x == 0) {
-    // tree over the cs slices, zero-padded to 16 (padding leaves the value unchanged)
-    double v[16];
-#pragma unroll
-    for (uint32_t r = 0; r < 16; r++) v[r] = r < cs ? *dsmem(&sm.part, r) : 0.0;
-#pragma unroll
-    for (uint32_t w = 1; w < 16; w <<= 1)
-#pragma unroll
-      for (uint32_t r = 0; r < 16; r += 2 * w) v[r] = v[r] + v[r + w];
-    sm.total = v[0];
-  }
-  __syncthreads();
-  cluster_arrive_relaxed();   // done with peers' smem; the matching wait is at kernel exit
-  return sm.total;
-}
-
 __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* scan, uint32_t& total) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t incl = v;
@@ -126,12 +95,6 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* scan, 
   return r;
 }
 
-// warp subtree of this iteration's 128 elements -> sm.red (all lanes call it)
-__device__ __forceinline__ void leaf_to_red(Smem& sm, int it, double leaf) {
-  const double a = warp_tree(leaf);
-  if ((threadIdx.x & 31) == 0) sm.red[it * NWARP + (threadIdx.x >> 5)] = a;
-}
-
 // key of an element for the "k largest keys, lowest index first" selection:
 // top-k: |q| bits (R9); random-k: ~Philox word (k smallest words, R10)
 template <int KIND>
@@ -150,10 +113,10 @@ __device__ __forceinline__ uint32_t getu(const uint4& v, int u) {
 }
 
 // ---------------------------------------------------------------- producers
-// worker: q = g + e (use_ef) or q = g; slice -> sm.q; leaf sums -> sm.red (LEAF);
-// HISTK (top-k / random-k): the round-0 10-bit key histogram of the selection
-// (emit_sparse) is built here, on the fly, instead of in a separate pass
-template <bool L2, bool LEAF, int HISTK = 0>
+// worker: q = g + e (use_ef) or q = g; slice -> sm.q; the round-0 10-bit key
+// histogram of the selection (emit_sparse) is built here, on the fly, instead
+// of in a separate pass
+template <int HISTK>
 __device__ __forceinline__ void produce_worker(const CompressParams& p, const DevChunk& c, Smem& sm,
                                                uint32_t s0) {
   const float* g = p.grad + c.off;
@@ -166,7 +129,6 @@ __device__ __forceinline__ void produce_worker(const CompressParams& p, const De
     const float4 q = p.use_ef ? make_float4(fadd(g4.x, e4.x), fadd(g4.y, e4.y), fadd(g4.z, e4.z), fadd(g4.w, e4.w))
                               : g4;
     sm.q[it * NT + threadIdx.x] = q;
-    if (LEAF) leaf_to_red(sm, it, L2 ? leaf4_sq(q) : leaf4_abs(q));
     if (HISTK) {
       constexpr int DSH = HISTK == K_TOPK ? 21 : 22;
       const uint32_t j = s0 + 4 * (it * NT + threadIdx.x);
@@ -212,83 +174,6 @@ __device__ __forceinline__ void produce_worker(const CompressParams& p, const De
     }
   }
   if (bad) atomicOr(p.flag, 1u);
-}
-
-// server, dense kinds: Delta_j = (float)(sum_i dec(delta_i)_j * (1/n) + e~_j)
-// Batches of B iterations: the e~ loads and each rank's code words are issued together.
-template <int KIND>
-__device__ __forceinline__ void produce_server_dense(const CompressParams& p, const DevChunk& c,
-                                                     Smem& sm, uint32_t s0) {
-  const uint32_t L = c.len;
-  const int b = (int)p.bits;
-  const float sl = (float)((1u << (b - 1)) - 1u);
-  const int cmax = (1 << (b - 1)) - 1;
-  const uint32_t cmask = (1u << b) - 1u;
-  const float* et = p.etl + c.etl;
-  const bool full = s0 + SLICE <= L;
-  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-  constexpr int B = 4;
-#pragma unroll 1
-  for (int it0 = 0; it0 < IT; it0 += B) {
-    uint32_t jj[B];
-    float4 e4[B];
-    double acc[B][4];
-#pragma unroll
-    for (int q = 0; q < B; q++) {
-      jj[q] = s0 + 4 * ((it0 + q) * NT + threadIdx.x);
-      e4[q] = z;
-      if (p.use_ef) e4[q] = full ? ld4(et + jj[q]) : (jj[q] < L ? load4_masked(et, jj[q], L) : z);
-#pragma unroll
-      for (int u = 0; u < 4; u++) acc[q][u] = 0.0;
-    }
-#pragma unroll 1
-    for (uint32_t r = 0; r < p.n; r++) {
-      const uint8_t* pl = p.recv + r * p.slot_bytes + c.recv;
-      const uint32_t* words = reinterpret_cast<const uint32_t*>(pl + 4);
-      const float hdr = *reinterpret_cast<const float*>(pl);
-      uint32_t f[B];
-#pragma unroll
-      for (int q = 0; q < B; q++) {
-        f[q] = 0;
-        if (jj[q] < L)
-          f[q] = KIND == K_SIGN ? ((words[jj[q] >> 5] >> (jj[q] & 31)) & 15u)
-                                : load_field(words, (uint64_t)b * jj[q], 4 * b);
-      }
-      const float unit = fdiv(hdr, sl);
-#pragma unroll
-      for (int q = 0; q < B; q++) {
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-          float dec;
-          if (KIND == K_SIGN) {
-            dec = ((f[q] >> u) & 1u) ? hdr : -hdr;
-          } else {
-            const uint32_t code = (f[q] >> (b * u)) & cmask;
-            float mag;
-            if (KIND == K_LDITHER) {
-              mag = fmul((float)(code >> 1), unit);
-            } else {
-              const uint32_t cl = code >> 1;
-              mag = fmul(cl == 0 ? 0.f : __uint_as_float((uint32_t)(127 - (cmax - (int)cl)) << 23), hdr);
-            }
-            dec = (code & 1u) ? mag : -mag;
-          }
-          if (jj[q] + u < L) acc[q][u] += (double)dec;
-        }
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < B; q++) {
-      const uint32_t j = jj[q];
-      float4 d = z;
-      if (j < L) d.x = mean_plus(acc[q][0], p.inv_n, (double)e4[q].x);
-      if (j + 1 < L) d.y = mean_plus(acc[q][1], p.inv_n, (double)e4[q].y);
-      if (j + 2 < L) d.z = mean_plus(acc[q][2], p.inv_n, (double)e4[q].z);
-      if (j + 3 < L) d.w = mean_plus(acc[q][3], p.inv_n, (double)e4[q].w);
-      sm.q[(it0 + q) * NT + threadIdx.x] = d;
-      leaf_to_red(sm, it0 + q, (KIND == K_SIGN) ? leaf4_abs(d) : leaf4_sq(d));
-    }
-  }
 }
 
 __device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* a, uint32_t n, uint32_t key) {
@@ -359,120 +244,6 @@ __device__ __forceinline__ void produce_server_sparse(const CompressParams& p, c
     }
   }
   __syncthreads();
-}
-
-// ---------------------------------------------------------------- emitters
-// scaled sign: s = (float)(||q||_1 / L), bit = q >= 0, err = q - dec
-__device__ __forceinline__ void emit_sign(const DevChunk& c, Smem& sm, uint32_t s0, uint32_t crank,
-                                          double total, uint8_t* pay, float* errp) {
-  const uint32_t L = c.len;
-  const float s = __double2float_rn(total / (double)L);
-  uint32_t* words = reinterpret_cast<uint32_t*>(pay + 4);
-  const int lane = threadIdx.x & 31;
-#pragma unroll 4
-  for (int it = 0; it < IT; it++) {
-    const uint32_t i4 = it * NT + threadIdx.x;
-    const uint32_t j = s0 + 4 * i4;
-    const float4 q = sm.q[i4];
-    uint32_t nib = 0;
-    float4 ev;
-#pragma unroll
-    for (int u = 0; u < 4; u++) {
-      const float qu = get(q, u);
-      const bool bit = !(qu < 0.f);
-      if (bit && j + u < L) nib |= 1u << u;
-      set(ev, u, bit ? fsub(qu, s) : fadd(qu, s));
-    }
-    if (errp && j < L) store4_masked(errp, j, L, ev);
-    uint32_t w = nib << (4 * (lane & 7));
-    w |= __shfl_xor_sync(0xffffffffu, w, 1);
-    w |= __shfl_xor_sync(0xffffffffu, w, 2);
-    w |= __shfl_xor_sync(0xffffffffu, w, 4);
-    if ((lane & 7) == 0 && j < L) words[j >> 5] = w;
-  }
-  if (crank == 0 && threadIdx.x == 0) *reinterpret_cast<float*>(pay) = s;
-}
-
-// linear dithering code (R11-R13)
-__device__ __forceinline__ uint32_t lin_code(float q, float N, float sl, float inv, uint32_t w) {
-  const uint32_t sign = !(q < 0.f);
-  uint32_t level = 0;
-  if (N != 0.f) {
-    const float r = fminf(fmul(fabsf(q), inv), sl);
-    const float l = floorf(r);
-    const float f = fsub(r, l);
-    const float u = (float)(w >> 8) * 0x1p-24f;
-    level = (uint32_t)l + (u < f ? 1u : 0u);
-  }
-  return sign | (level << 1);
-}
-// natural dithering code (R11-R13)
-__device__ __forceinline__ uint32_t nat_code(float q, float N, int cmax, float lmin, uint32_t w) {
-  const uint32_t sign = !(q < 0.f);
-  uint32_t code = 0;
-  if (N != 0.f) {
-    const float r = fminf(fdiv(fabsf(q), N), 1.0f);
-    const float u = (float)(w >> 8) * 0x1p-24f;
-    if (r >= lmin) {
-      const int eb = (int)(__float_as_uint(r) >> 23);        // r is normal and positive
-      const float lo = __uint_as_float((uint32_t)eb << 23);  // 2^floor(log2 r)
-      const float pup = fsub(fdiv(r, lo), 1.0f);
-      const int e_lev = (u < pup) ? eb - 127 + 1 : eb - 127;
-      code = (uint32_t)(cmax + e_lev);
-    } else {
-      code = (u < fdiv(r, lmin)) ? 1u : 0u;
-    }
-  }
-  return sign | (code << 1);
-}
-
-template <int KIND>
-__device__ __forceinline__ void emit_dither(const CompressParams& p, const DevChunk& c, Smem& sm,
-                                            uint32_t s0, uint32_t crank, double total, uint8_t* pay,
-                                            float* errp, uint32_t stage, uint32_t rrank) {
-  const uint32_t L = c.len;
-  const int b = (int)p.bits, nb = 4 * b;
-  const float N = __double2float_rn(sqrt(total));
-  const float sl = (float)((1u << (b - 1)) - 1u);
-  const float inv = N != 0.f ? fdiv(sl, N) : 0.f;
-  const float unit = fdiv(N, sl);
-  const int cmax = (1 << (b - 1)) - 1;
-  const float lmin = __uint_as_float((uint32_t)(127 - (cmax - 1)) << 23);
-  const uint32_t mask = (1u << b) - 1u;
-  uint32_t* words = reinterpret_cast<uint32_t*>(pay + 4);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint64_t nwords = ((uint64_t)b * L + 31) / 32;
-#pragma unroll 2
-  for (int it = 0; it < IT; it++) {
-    const uint32_t i4 = it * NT + threadIdx.x;
-    const uint32_t j = s0 + 4 * i4;
-    const float4 q = sm.q[i4];
-    uint32_t field = 0;
-    float4 ev = q;
-    if (j < L) {
-      const uint4 w4 = rng4(p.seed, j >> 2, c.id, p.t, stage, rrank);
-#pragma unroll
-      for (int u = 0; u < 4; u++) {
-        const uint32_t w = u == 0 ? w4.x : (u == 1 ? w4.y : (u == 2 ? w4.z : w4.w));
-        const float qu = get(q, u);
-        const uint32_t code = KIND == K_LDITHER ? lin_code(qu, N, sl, inv, w) : nat_code(qu, N, cmax, lmin, w);
-        if (j + u < L) field |= (code & mask) << (b * u);
-        float mag;
-        if (KIND == K_LDITHER) {
-          mag = fmul((float)(code >> 1), unit);
-        } else {
-          const uint32_t cl = code >> 1;
-          mag = fmul(cl == 0 ? 0.f : __uint_as_float((uint32_t)(127 - (cmax - (int)cl)) << 23), N);
-        }
-        set(ev, u, fsub(qu, (code & 1u) ? mag : -mag));
-      }
-      if (errp) store4_masked(errp, j, L, ev);
-    }
-    const uint32_t wd = warp_pack(field, nb);
-    const uint64_t wbase = (uint64_t)(s0 + 4 * (it * NT + 32 * warp)) / 32 * b;
-    if (lane < nb && wbase + lane < nwords) words[wbase + lane] = wd;
-  }
-  if (crank == 0 && threadIdx.x == 0) *reinterpret_cast<float*>(pay) = N;
 }
 
 template <int KIND>
@@ -905,31 +676,22 @@ __global__ void __launch_bounds__(NT, 3) compress_kernel(const __grid_constant__
     if (ti < p.n_raw_tiles) raw_tile<SERVER>(p, p.raw_tiles[ti]);
     return;
   }
-  if constexpr (KIND != K_NONE) {
+  {
     const DevChunk c = p.chunks[p.items[cid]];
     const uint32_t s0 = crank * SLICE;
     uint8_t* pay = p.out + c.pay;
     float* errp = p.use_ef ? (SERVER ? p.etl + c.etl : p.err + c.off) : nullptr;
     const uint32_t stage = SERVER ? 1u : 0u;
     const uint32_t rrank = SERVER ? 0u : p.rank;
-    if constexpr (KIND == K_SIGN || KIND == K_LDITHER || KIND == K_NDITHER) {
-      constexpr bool L2 = KIND != K_SIGN;
-      if (SERVER) produce_server_dense<KIND>(p, c, sm, s0);
-      else produce_worker<L2, true>(p, c, sm, s0);
-      const double total = cluster_tree_total(sm, p.cs);
-      if (KIND == K_SIGN) emit_sign(c, sm, s0, crank, total, pay, errp);
-      else emit_dither<KIND>(p, c, sm, s0, crank, total, pay, errp, stage, rrank);
+    if (SERVER) {
+      produce_server_sparse(p, c, sm, s0);
     } else {
-      if (SERVER) {
-        produce_server_sparse(p, c, sm, s0);
-      } else {
-        for (uint32_t b = threadIdx.x; b < (uint32_t)FNB; b += NT) sm.fh[b] = 0;
-        __syncthreads();
-        produce_worker<false, false, KIND>(p, c, sm, s0);
-      }
+      for (uint32_t b = threadIdx.x; b < (uint32_t)FNB; b += NT) sm.fh[b] = 0;
       __syncthreads();
-      emit_sparse<KIND>(p, c, sm, s0, crank, pay, errp, stage, rrank, !SERVER);
+      produce_worker<KIND>(p, c, sm, s0);
     }
+    __syncthreads();
+    emit_sparse<KIND>(p, c, sm, s0, crank, pay, errp, stage, rrank, !SERVER);
     cluster_wait();   // no CTA exits while a peer may still read its shared memory
   }
 }
@@ -983,15 +745,13 @@ static cudaError_t max_clusters_t(uint32_t cs, int* out) {
   return cudaOccupancyMaxActiveClusters(out, fn, &cfg);
 }
 
-#define BPC_DISPATCH(KIND_, SERVER_, CALL)                                   \
-  switch (KIND_) {                                                           \
-    case K_NONE: return SERVER_ ? CALL(K_NONE, true) : CALL(K_NONE, false);  \
-    case K_SIGN: return SERVER_ ? CALL(K_SIGN, true) : CALL(K_SIGN, false);  \
-    case K_TOPK: return SERVER_ ? CALL(K_TOPK, true) : CALL(K_TOPK, false);  \
+// the cluster kernels serve the sparse kinds (top-k, random-k) and their raw
+// units; the norm-based kinds run in the streaming kernels (kernels_cstream.cu)
+#define BPC_DISPATCH(KIND_, SERVER_, CALL)                                     \
+  switch (KIND_) {                                                             \
+    case K_TOPK: return SERVER_ ? CALL(K_TOPK, true) : CALL(K_TOPK, false);    \
     case K_RANDK: return SERVER_ ? CALL(K_RANDK, true) : CALL(K_RANDK, false); \
-    case K_LDITHER: return SERVER_ ? CALL(K_LDITHER, true) : CALL(K_LDITHER, false); \
-    case K_NDITHER: return SERVER_ ? CALL(K_NDITHER, true) : CALL(K_NDITHER, false); \
-  }                                                                          \
+  }                                                                            \
   return cudaErrorInvalidValue;
 
 cudaError_t launch_compress(int kind, bool server, const CompressParams& p, cudaStream_t s) {
