@@ -1,4 +1,4 @@
-"""The N>1 exchange path on CPU: two processes over torch.distributed (gloo)
+"""The N>1 exchange path on CPU: two and four processes over torch.distributed (gloo)
 run the sharded server with libbpc's host plan (owner map, per-peer segments,
 receive-slot offsets) and the oracle's per-unit operators, exchanging the
 payload bytes with a real all-to-all and all-gather.  The decoded g~ must equal
@@ -114,9 +114,10 @@ def _worker(rank, world, port, comp_t, steps, q):
         q.put((rank, traceback.format_exc()))
 
 
+@pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("comp", [Comp(SCALED_SIGN, use_ef=1), Comp(TOP_K, 1, 1000, use_ef=1),
                                   Comp(LINEAR_DITHER, bits=7, use_ef=0)], ids=["onebit", "topk", "ldither"])
-def test_two_rank_exchange_gloo(comp):
+def test_multi_rank_exchange_gloo(comp, world):
     import oracle
     oracle.build()
     from paper_2105_07829_b200 import build
@@ -125,10 +126,10 @@ def test_two_rank_exchange_gloo(comp):
     q = ctx.Queue()
     port = _free_port()
     comp_t = (comp.kind, comp.k_num, comp.k_den, comp.bits, comp.randk_scaled, comp.use_ef)
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, comp_t, 2, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, comp_t, 2, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=600) for _ in procs)
     for p in procs:
         p.join(timeout=60)
-    assert res == {0: "ok", 1: "ok"}, res
+    assert res == {r: "ok" for r in range(world)}, res
