@@ -1,5 +1,5 @@
 """Multi-GPU parity through the NVLink peer-store exchange and NCCL (bpc_aggregate): torchrun one process per GPU
-on 2 (and 4 when present) B200s; every rank's payloads, errors and parameters
+on 2 (and 4, 8 when present) B200s; every rank's payloads, errors and parameters
 are checked against the CPU oracle (tests/multigpu_parity.py).  Skips when the
 box has a single GPU (the loopback tests cover n > 1 there)."""
 import os
@@ -18,7 +18,7 @@ def _ngpus():
 
 
 @pytest.mark.parametrize("exchange", ["p2p", "nccl"])
-@pytest.mark.parametrize("n", [2, 4])
+@pytest.mark.parametrize("n", [2, 4, 8])
 def test_multi_parity(n, exchange):
     if _ngpus() < n:
         pytest.skip(f"needs {n} GPUs")
