@@ -52,6 +52,9 @@ def parse():
     ap.add_argument("--units", choices=["chunk", "tensor"], default="chunk",
                     help="compression unit: 2^18-element chunks (R1) or whole tensors (PAPER.md:505, "
                          "two-pass kernels; norm-based compressors only)")
+    ap.add_argument("--threshold-bytes", type=int, default=None,
+                    help="size threshold (PAPER.md:504-505): tensors below it stay raw; default: the config's 1 MiB "
+                         "(tools/threshold_search.py sweeps it)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -193,7 +196,8 @@ def run_reference(args):
     import oracle
     from workloads import config, gen_grad, gen_params, layout
     n = args.gpus
-    full = config(args.config, n=n)
+    full = config(args.config, n=n,
+                  **({"threshold_bytes": args.threshold_bytes} if args.threshold_bytes is not None else {}))
     d_full = sum(full.tensor_numels())
     # Each step is one oracle round (n simulated workers) over a miniature of the
     # workload: every tensor, the size threshold and the unit size divided by s,
@@ -257,7 +261,8 @@ def run_ours(args):
     from workloads import config, gen_grad_torch, gen_params, layout
 
     w = config(args.config, n=world, optimizer=args.optimizer,
-               **({"chunk_elems": 0} if args.units == "tensor" else {}))
+               **({"chunk_elems": 0} if args.units == "tensor" else {}),
+               **({"threshold_bytes": args.threshold_bytes} if args.threshold_bytes is not None else {}))
     numels = w.tensor_numels()
     offs, D = layout(numels)
     d = sum(numels)
@@ -406,7 +411,8 @@ def run_ours(args):
                        "l2": "inputs larger than L2 (g, e, m, v, x = %.0f MB per rank)" % (20 * D / 1e6),
                        "parallelism": f"dp{world} (sharded server: all-to-all + all-gather)",
                        "exchange": ctx.exchange if world > 1 else None,
-                       "optimizer": args.optimizer, "units": args.units},
+                       "optimizer": args.optimizer, "units": args.units,
+                       "threshold_bytes": w.threshold_bytes},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                          "traffic_source": traffic_src, "peak_source": peak_src,
