@@ -112,7 +112,7 @@ typedef struct {
 
 /* The update of bpc_step (A9).
  * BPC_OPT_ADAM: Alg. 5 lines 12-16 and x = x - lr (r + weight_decay x)
- *   (R15, R21), one fused pass (24 B/element + payload).
+ *   (R15, R16), one fused pass (24 B/element + payload).
  * BPC_OPT_LANS: CLAN proper, Alg. 5 lines 12-18 (Alg. 2
  *   PAPER.md:157-163): per block G_b = one tensor,
  *   d = phi(||x_b||) [beta1 (r + lambda x)/||r + lambda x|| + (1 - beta1)(c + lambda x)/||c + lambda x||],

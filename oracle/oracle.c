@@ -391,19 +391,19 @@ void orc_adam(uint64_t L, const float* gt, float* m, float* v, float* x, uint32_
               float lr, float beta1, float beta2, float eps, float wd) {
   /* Alg. 5 lines 12-16 and the x update with the
    * direction r + lambda x (PAPER.md:292-295 with the LANS normalisation
-   * left to NEXT #1): reading R15. The bias corrections 1/(1 - beta^t) are
-   * formed once per step in fp64 and rounded to fp32 (R16); lines 14-15 then
-   * multiply by them (R21: same real-number formula as the division). */
+   * left to NEXT #1): reading R15. The bias corrections (1 - beta^t) are
+   * formed once per step in fp64 and rounded to fp32 (R16); lines 14-15
+   * divide by them, as the paper writes. */
   float omb1 = (float)(1.0 - (double)beta1);
   float omb2 = (float)(1.0 - (double)beta2);
-  float ibc1 = (float)(1.0 / (1.0 - pow((double)beta1, (double)t)));
-  float ibc2 = (float)(1.0 / (1.0 - pow((double)beta2, (double)t)));
+  float bc1 = (float)(1.0 - pow((double)beta1, (double)t));
+  float bc2 = (float)(1.0 - pow((double)beta2, (double)t));
   for (uint64_t j = 0; j < L; j++) {
     float g = gt[j];
     m[j] = beta1 * m[j] + omb1 * g;                 /* line 12 */
     v[j] = beta2 * v[j] + omb2 * (g * g);           /* line 13 */
-    float mh = m[j] * ibc1;                         /* line 14: m / (1 - beta1^t) */
-    float vh = v[j] * ibc2;                         /* line 15: v / (1 - beta2^t) */
+    float mh = m[j] / bc1;                          /* line 14: m / (1 - beta1^t) */
+    float vh = v[j] / bc2;                          /* line 15: v / (1 - beta2^t) */
     float r = mh / (sqrtf(vh) + eps);               /* line 16 */
     x[j] = x[j] - lr * (r + wd * x[j]);             /* line 18 (Adam core) */
   }
@@ -424,7 +424,7 @@ void orc_nag(uint64_t L, const float* gt, float* vel, float* x, float lr, float 
 
 /* LANS block update (CLAN, Alg. 5 lines 12-18; the same
  * step as Alg. 2 lines 8-14), in the paper's order:
- *   m, v, m~, v~ as in orc_adam (lines 12-15, R16/R21);
+ *   m, v, m~, v~ as in orc_adam (lines 12-15, R16);
  *   line 16: r = m~ / (sqrt(v~) + eps),  c = g~ / (sqrt(v~) + eps);
  *   line 17: d~ = phi(||x_b||) [ beta1 (r + lambda x)/||r + lambda x||
  *                               + (1 - beta1)(c + lambda x)/||c + lambda x|| ];
@@ -441,8 +441,8 @@ void orc_lans_block(uint64_t L, const float* gt, float* m, float* v, float* x, u
                     float alpha_u) {
   float omb1 = (float)(1.0 - (double)beta1);
   float omb2 = (float)(1.0 - (double)beta2);
-  float ibc1 = (float)(1.0 / (1.0 - pow((double)beta1, (double)t)));
-  float ibc2 = (float)(1.0 / (1.0 - pow((double)beta2, (double)t)));
+  float bc1 = (float)(1.0 - pow((double)beta1, (double)t));
+  float bc2 = (float)(1.0 - pow((double)beta2, (double)t));
   float* u = (float*)malloc(sizeof(float) * (size_t)(L ? L : 1));
   float* w = (float*)malloc(sizeof(float) * (size_t)(L ? L : 1));
   double* sq = (double*)malloc(sizeof(double) * (size_t)(L ? L : 1));
@@ -450,8 +450,8 @@ void orc_lans_block(uint64_t L, const float* gt, float* m, float* v, float* x, u
     float g = gt[j];
     m[j] = beta1 * m[j] + omb1 * g;                 /* line 12 */
     v[j] = beta2 * v[j] + omb2 * (g * g);           /* line 13 */
-    float mh = m[j] * ibc1;                         /* line 14 */
-    float vh = v[j] * ibc2;                         /* line 15 */
+    float mh = m[j] / bc1;                          /* line 14 */
+    float vh = v[j] / bc2;                          /* line 15 */
     float den = sqrtf(vh) + eps;
     float r = mh / den;                             /* line 16: r */
     float c = g / den;                              /* line 16: c */

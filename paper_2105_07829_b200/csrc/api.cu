@@ -936,9 +936,9 @@ bpc_status bpc_step(bpc_ctx* ctx, float* d_params, float lr) {
   p.beta2 = c.beta2;
   p.omb1 = (float)(1.0 - (double)c.beta1);
   p.omb2 = (float)(1.0 - (double)c.beta2);
-  // reciprocal bias corrections, fp64 then one rounding (R16, R21)
-  p.bc1 = (float)(1.0 / (1.0 - std::pow((double)c.beta1, (double)ctx->t)));
-  p.bc2 = (float)(1.0 / (1.0 - std::pow((double)c.beta2, (double)ctx->t)));
+  // bias corrections 1 - beta^t, fp64 then one rounding (R16); the kernels divide
+  p.bc1 = (float)(1.0 - std::pow((double)c.beta1, (double)ctx->t));
+  p.bc2 = (float)(1.0 - std::pow((double)c.beta2, (double)ctx->t));
   p.eps = c.eps;
   p.lr = lr;
   p.wd = c.weight_decay;

@@ -76,7 +76,7 @@ struct UpdateParams {
   float* m;
   float* v;
   float* x;
-  float beta1, beta2, omb1, omb2, bc1, bc2, eps, lr, wd;   // bc = 1 / (1 - beta^t), R21
+  float beta1, beta2, omb1, omb2, bc1, bc2, eps, lr, wd;   // bc = fl32(1 - beta^t), R16
   uint32_t bits;
   int32_t mode;           // 0 Adam core; LANS (R22): 1 = pass 1 (m, v, block sums), 2 = pass 2 (x);
                           // 3 NAG (R24, velocity in m)

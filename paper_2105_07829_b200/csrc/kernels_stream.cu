@@ -7,7 +7,7 @@
 // reads in flight per SM.
 //
 // update_stream: g~ = dec(p) from the staged payload bytes,
-// then Alg. 5 lines 12-16 + x update (R15/R21)
+// then Alg. 5 lines 12-16 + x update (R15/R16)
 // on the staged m, v, x tile; results stored straight to HBM.
 //
 // worker_stream (A1-A3 for the norm-based compressors: scaled sign, linear /
@@ -69,8 +69,8 @@ struct __align__(128) USmem {
 __device__ __forceinline__ void adam1s(float g, float& m, float& v, float& x, const UpdateParams& p) {
   m = fadd(fmul(p.beta1, m), fmul(p.omb1, g));                 // line 12
   v = fadd(fmul(p.beta2, v), fmul(p.omb2, fmul(g, g)));        // line 13
-  const float mh = fmul(m, p.bc1);                             // line 14 (R21)
-  const float vh = fmul(v, p.bc2);                             // line 15
+  const float mh = fdiv(m, p.bc1);                             // line 14: m / (1 - beta1^t)
+  const float vh = fdiv(v, p.bc2);                             // line 15: v / (1 - beta2^t)
   const float r = fdiv(mh, fadd(__fsqrt_rn(vh), p.eps));       // line 16
   x = fsub(x, fmul(p.lr, fadd(r, fmul(p.wd, x))));             // x update (Adam core)
 }
@@ -79,8 +79,8 @@ __device__ __forceinline__ void adam1s(float g, float& m, float& v, float& x, co
 // c = g~/(sqrt(v~)+eps), from the already-updated m, v (the oracle's order)
 __device__ __forceinline__ void lans_uw(float g, float m, float v, float x, const UpdateParams& p, float& u,
                                         float& w) {
-  const float den = fadd(__fsqrt_rn(fmul(v, p.bc2)), p.eps);
-  u = fadd(fdiv(fmul(m, p.bc1), den), fmul(p.wd, x));
+  const float den = fadd(__fsqrt_rn(fdiv(v, p.bc2)), p.eps);
+  u = fadd(fdiv(fdiv(m, p.bc1), den), fmul(p.wd, x));
   w = fadd(fdiv(g, den), fmul(p.wd, x));
 }
 

@@ -11,8 +11,8 @@ enum { U_NONE = 0, U_SIGN = 2, U_TOPK = 3, U_RANDK = 4, U_LDITHER = 5, U_NDITHER
 __device__ __forceinline__ void adam1(float g, float& m, float& v, float& x, const UpdateParams& p) {
   m = fadd(fmul(p.beta1, m), fmul(p.omb1, g));                 // line 12
   v = fadd(fmul(p.beta2, v), fmul(p.omb2, fmul(g, g)));        // line 13
-  const float mh = fmul(m, p.bc1);                             // line 14 (bc1 = fl32(1/(1-b1^t)), R21)
-  const float vh = fmul(v, p.bc2);                             // line 15
+  const float mh = fdiv(m, p.bc1);                             // line 14: m / (1 - beta1^t) (R16)
+  const float vh = fdiv(v, p.bc2);                             // line 15: v / (1 - beta2^t)
   const float r = fdiv(mh, fadd(__fsqrt_rn(vh), p.eps));       // line 16
   x = fsub(x, fmul(p.lr, fadd(r, fmul(p.wd, x))));             // x update (Adam core)
 }
@@ -20,8 +20,8 @@ __device__ __forceinline__ void adam1(float g, float& m, float& v, float& x, con
 // LANS (R22): u = r + lambda x, w = c + lambda x from the updated m, v
 __device__ __forceinline__ void lans_uw1(float g, float m, float v, float x, const UpdateParams& p, float& u,
                                          float& w) {
-  const float den = fadd(__fsqrt_rn(fmul(v, p.bc2)), p.eps);
-  u = fadd(fdiv(fmul(m, p.bc1), den), fmul(p.wd, x));
+  const float den = fadd(__fsqrt_rn(fdiv(v, p.bc2)), p.eps);
+  u = fadd(fdiv(fdiv(m, p.bc1), den), fmul(p.wd, x));
   w = fadd(fdiv(g, den), fmul(p.wd, x));
 }
 

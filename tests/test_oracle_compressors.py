@@ -291,3 +291,36 @@ def test_dither_code_packing(orc):
         sign = code & 1
         assert sign == (0 if x[j] < 0 else 1)
         assert dec[j] == (1 if sign else -1) * np.float32(np.float32(code >> 1) * unit)
+
+
+# ---------------------------------------------------------------- dithering: bit-exact vectors
+def test_dither_golden_vectors(orc):
+    # SURVEY.md:566-573 (tests/golden/dither_vectors.json): Philox words, codes and
+    # packed bytes derived outside this repo; a change to the counter layout, the
+    # word selection, u = (w >> 8) * 2^-24 or the code packing fails here even when
+    # the output stays uniform / unbiased (which the statistical pins above allow).
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "dither_vectors.json")))
+    s = g["stream"]
+    words = [orc.rng_word(s["seed"], j, s["chunk"], s["t"], s["stage"], s["rank"]) for j in range(8)]
+    assert ["%08x" % w for w in words] == g["philox_words_w0_w7"]
+    for case in g["cases"]:
+        kind = LINEAR_DITHER if case["kind"] == "linear" else NATURAL_DITHER
+        b = case["bits"]
+        comp = C(orc, kind, bits=b, use_ef=0)
+        x = np.array(case["x"], np.float32)
+        p = orc.compress(comp, x, seed=s["seed"], chunk=s["chunk"], t=s["t"], stage=s["stage"], rank=s["rank"])
+        assert p[:4].hex() == case["norm_f32_le"], case
+        assert p[4:].hex() == case["packed"], case
+        body = int.from_bytes(p[4:], "little")
+        codes = [(body >> (b * j)) & ((1 << b) - 1) for j in range(len(x))]
+        assert codes == case["codes"], case
+        if "levels" in case and kind == LINEAR_DITHER:
+            assert [c >> 1 for c in codes] == case["levels"]
+        if kind == NATURAL_DITHER:
+            cmax = (1 << (b - 1)) - 1
+            lev = [0.0 if (c >> 1) == 0 else 2.0 ** -(cmax - (c >> 1)) for c in codes]
+            assert lev == case["levels"]
+        if "dec" in case:
+            assert list(orc.decompress(comp, p, len(x))) == case["dec"]
