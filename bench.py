@@ -23,6 +23,7 @@ import subprocess
 import sys
 import tempfile
 import time
+from dataclasses import replace
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -43,7 +44,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C5",
+                    help="workload (BASELINE.json configs): C5 BERT-large = the largest single-GPU config, the "
+                         "metric's default; C2 ResNet-50, C3 VGG16, C4 BERT-base, C1 d=4096")
     ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
                     help="N>1 transport of the push/pull exchange: NVLink peer stores or NCCL send/recv")
     ap.add_argument("--optimizer", choices=["adam", "lans", "nag"], default="adam",
@@ -57,7 +60,8 @@ def parse():
                          "(tools/threshold_search.py sweeps it)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="CPU work per cpu_baseline leg (1 core, then all host cores)")
     return ap.parse_args()
 
 
@@ -163,28 +167,51 @@ def peaks():
 
 
 # ---------------------------------------------------------------- CPU oracle leg
-def oracle_sample(wcfg, n, seconds):
-    """Time the oracle as it stands (single host core) on a bounded sample of the
-    workload: whole rounds of the full config at n simulated workers, repeated
-    until `seconds` of CPU work; returns gradient GB/s (n x 4d / s)."""
+def host_cpu():
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return model, len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+
+
+def oracle_sample(wcfg, n, seconds, threads):
+    """Time the oracle as it stands on `threads` host cores (OpenMP over units,
+    bit-identical to 1 thread) on a bounded sample of the workload: the config
+    with every tensor, the size threshold and the unit size divided by s (tensor
+    count and raw / compressed mix kept), s chosen for ~seconds/3 per round,
+    rounds repeated until `seconds` of wall time; gradient GB/s = n x 4 d_sample / s."""
     import numpy as np
 
     import oracle
     from workloads import gen_grad, gen_params, layout
     oracle.build()
-    numels = wcfg.tensor_numels()
+    d_full = sum(wcfg.tensor_numels())
+    rate = 12e6 * threads / max(1, n)              # oracle elements / s (measured ~15e6 per core, n = 1)
+    s = max(1, int(np.ceil(d_full / (rate * seconds / 3))))
+    w = wcfg if s == 1 else replace(wcfg, scale=s, threshold_bytes=wcfg.threshold_bytes // s,
+                                     chunk_elems=max(1, wcfg.chunk_elems // s) if wcfg.chunk_elems else 0)
+    numels = w.tensor_numels()
     offs, D = layout(numels)
     d = sum(numels)
-    cfg = oracle.Cfg.from_workload(wcfg, n=n)
-    st = oracle.State(n, D, gen_params(wcfg))
-    grads = [np.stack([gen_grad(wcfg, i, s) for i in range(n)]) for s in (1, 2)]
+    cfg = oracle.Cfg.from_workload(w, n=n)
+    st = oracle.State(n, D, gen_params(w))
+    grads = [np.stack([gen_grad(w, i, k) for i in range(n)]) for k in (1, 2)]
+    oracle.set_threads(threads)
     steps, busy = 0, 0.0
-    while busy < seconds or steps == 0:
-        t0 = time.perf_counter()
-        oracle.round_(cfg, st, grads[steps % 2], wcfg.lr, want_payloads=False)
-        busy += time.perf_counter() - t0
-        steps += 1
-    return n * 4 * d * steps / busy / 1e9, steps, busy
+    try:
+        while busy < seconds or steps == 0:
+            t0 = time.perf_counter()
+            oracle.round_(cfg, st, grads[steps % 2], w.lr, want_payloads=False)
+            busy += time.perf_counter() - t0
+            steps += 1
+    finally:
+        oracle.set_threads(1)
+    return n * 4 * d * steps / busy / 1e9, steps, busy, s, d
 
 
 def run_reference(args):
@@ -203,7 +230,7 @@ def run_reference(args):
     # workload: every tensor, the size threshold and the unit size divided by s,
     # so the tensor count and the raw / compressed mix are kept; s is chosen so
     # the whole --warmup + --steps run takes about a minute on one core.
-    rate = 15e6                                    # oracle elements / s / core (measured)
+    rate = 12e6 * host_cpu()[1]                    # oracle elements / s on all cores (~15e6 per core)
     budget = max(4096.0, 60.0 * rate / max(1, args.steps + args.warmup) / n)
     s = max(1, int(np.ceil(d_full / budget)))
     w = config(args.config, n=n, scale=s, threshold_bytes=full.threshold_bytes // s,
@@ -215,6 +242,8 @@ def run_reference(args):
     cfg = oracle.Cfg.from_workload(w, n=n)
     st = oracle.State(n, D, gen_params(w))
     grads = [np.stack([gen_grad(w, i, k) for i in range(n)]) for k in (1, 2)]
+    model, ncores = host_cpu()
+    oracle.set_threads(ncores)               # the oracle on all host cores (OpenMP over units)
     for i in range(args.warmup):
         oracle.round_(cfg, st, grads[i % 2], w.lr, want_payloads=False)
     t0 = time.perf_counter()
@@ -230,9 +259,11 @@ def run_reference(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{args.config}: {DESCR[args.config]}", "ranks_simulated": n, "d": d_full,
                    "sample_scale": s, "sample_d": d},
-        "cpu_baseline": {"value": round(val, 6), "unit": "GB/s", "cores": 1, "kind": "oracle",
+        "cpu_baseline": {"value": round(val, 6), "unit": "GB/s", "cores": ncores, "kind": "oracle",
+                         "cpu_model": model,
                          "sample": f"each step: one oracle round of {args.config} with every tensor, the threshold "
-                                   f"and the unit size divided by {s} ({d} elements), {n} simulated workers"},
+                                   f"and the unit size divided by {s} ({d} elements), {n} simulated workers, "
+                                   f"OpenMP over units on {ncores} host cores"},
         "e2e": {"value": round(val, 6), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -328,7 +359,16 @@ def run_ours(args):
     achieved = kb[dom] / (per[dom][0] * 1e-3) / 1e9
     traffic, traffic_src = ncu_traffic(args.config, dom) if world == 1 else (None, None)
     kern = {k: {"ms": round(per[k][0], 5), "GB/s": round(kb[k] / max(per[k][0], 1e-9) / 1e6, 1) if k in kb else None,
+                "frac": round(kb[k] / max(per[k][0], 1e-9) / 1e6 / peak, 4) if k in kb else None,
                 "alg_bytes": kb.get(k)} for k in per if per[k][1]}
+    # step roofline: t_roof = max(sum of the kernels' algorithmic HBM
+    # bytes / HBM peak, exchange bytes per direction / 900 GB/s) against the step time
+    step_bytes = sum(kb.values())
+    nvl_bytes = 0
+    if world > 1:
+        nvl_bytes = sum(ctx.peer_segment(r)[1] for r in range(world) if r != rank)   # per direction, push or pull
+    t_roof = max(step_bytes / (peak * 1e9), 2 * nvl_bytes / 900e9 if world > 1 else 0.0)
+    t_roof8 = max(step_bytes / 8000e9, 2 * nvl_bytes / 900e9 if world > 1 else 0.0)
 
     # end to end through the public API: pinned host gradient -> device, step, params -> host
     e2e = None
@@ -393,9 +433,15 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        val, steps, busy = oracle_sample(w, 1, args.cpu_seconds)
-        cpu = {"value": round(val, 6), "unit": "GB/s", "cores": 1, "kind": "oracle",
-               "sample": f"{steps} full oracle rounds of {args.config} (n=1), {busy:.1f} s on 1 host core"}
+        model, ncores = host_cpu()
+        legs = {}
+        for th in sorted({1, ncores}):
+            val, steps, busy, sc, ds = oracle_sample(w, 1, args.cpu_seconds, th)
+            legs[th] = {"value": round(val, 6), "unit": "GB/s", "cores": th,
+                        "sample": f"{steps} oracle rounds of {args.config} with every tensor, the threshold and "
+                                  f"the unit size divided by {sc} ({ds} elements, n=1), {busy:.1f} s on {th} "
+                                  f"host core(s)"}
+        cpu = dict(legs[ncores], kind="oracle", cpu_model=model, nproc=ncores, single_core=legs[1])
 
     if rank == 0:
         s = ctx.summary()
@@ -416,7 +462,12 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                          "traffic_source": traffic_src, "peak_source": peak_src,
-                         "alg_bytes_per_launch": kb[dom]},
+                         "alg_bytes_per_launch": kb[dom],
+                         "step_bytes": step_bytes, "step_frac": round(t_roof * 1e3 / ms, 4),
+                         "step_frac_8tbs": round(t_roof8 * 1e3 / ms, 4),
+                         "step_note": "step_frac = max(sum of algorithmic HBM bytes of the step / peak, "
+                                      "exchange bytes / 900 GB/s) / ms_per_step; step_frac_8tbs uses the north "
+                                      "star's 8 TB/s"},
             "kernels": kern,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -139,7 +139,8 @@ typedef enum { BPC_OPT_ADAM = 0, BPC_OPT_LANS = 1, BPC_OPT_NAG = 2 } bpc_optimiz
  *     launch nothing; P holds valid bytes for the owned segment only.
  *   - sparse kinds (top-k, random-k): bpc_exchange_push/pull run a copy
  *     kernel that stores the segments into the peers' RECV / P over NVLink and
- *     releases the flags, then a wait kernel (SEND and P fully valid).
+ *     releases the flags; bpc_server / bpc_step start with a one-warp kernel
+ *     that waits for the peers' flags (SEND and P fully valid).
  *   If the peer mappings cannot be opened on every rank, init falls back to
  *   BPC_EXCHANGE_NCCL (bpc_get_exchange reports what is in use).
  * BPC_EXCHANGE_NCCL: grouped ncclSend/ncclRecv (all-to-all, all-gather). */
@@ -195,6 +196,28 @@ bpc_status bpc_init(const bpc_config* cfg, bpc_ctx** out);
 bpc_status bpc_plan(const bpc_config* cfg, bpc_plan_summary* summary, bpc_chunk_info* infos,
                     uint32_t cap);
 
+/* Single-process exchange group: wires n contexts of THIS process (index r =
+ * rank r, world_size n, created with nccl_unique_id = NULL, before their first
+ * step) into one BPC_EXCHANGE_P2P group with direct device pointers instead of
+ * CUDA IPC.  Contexts on distinct devices get peer access enabled (both
+ * directions; BPC_ERR_CUDA if the devices cannot reach each other).  The
+ * kernels then run exactly the multi-process P2P exchange (fused stores into
+ * the owners' RECV, release / acquire flags, bulk reads of the owners' P).
+ * Issue order: every rank's call of one phase before any rank's next phase
+ * (compress x n, exchange_push x n, server x n, exchange_pull x n, step x n),
+ * because a phase's kernels wait on flags released by the previous phase of
+ * every rank; contexts that share a device must also share one stream, or a
+ * persistent kernel spinning on a flag can hold the SMs its producer needs.
+ * bpc_aggregate on one context is then invalid (it would wait on peers'
+ * later phases).  Finalize only after every context's stream has drained.
+ * Errors: BPC_ERR_INVALID_ARGUMENT (NULL, n < 2 or n > 64), BPC_ERR_BAD_STATE
+ * (wrong world size / rank order, NCCL id given, already stepped),
+ * BPC_ERR_SIZE_MISMATCH (plans differ). */
+bpc_status bpc_connect_local(bpc_ctx* const* ctxs, int32_t n);
+
+/* d_grad / d_params: device memory of cfg.device (or managed), 16-byte aligned,
+ * >= plan flat_elems fp32 values; otherwise BPC_ERR_INVALID_ARGUMENT before
+ * anything is enqueued. */
 bpc_status bpc_compress(bpc_ctx* ctx, const float* d_grad);          /* A1-A3 */
 bpc_status bpc_aggregate(bpc_ctx* ctx);                              /* A4-A8 */
 bpc_status bpc_exchange_push(bpc_ctx* ctx);                          /* A4 all-to-all */
@@ -202,6 +225,9 @@ bpc_status bpc_server(bpc_ctx* ctx);                                 /* A5-A7 */
 bpc_status bpc_exchange_pull(bpc_ctx* ctx);                          /* A8 all-gather */
 bpc_status bpc_step(bpc_ctx* ctx, float* d_params, float lr);        /* A9, t += 1 */
 bpc_status bpc_sync(bpc_ctx* ctx);   /* drain the stream; surface async CUDA/NCCL/non-finite */
+/* Frees the context.  With the multi-process P2P exchange this is collective
+ * (an NCCL all-reduce orders every rank's frees after all peers' last reads of
+ * its buffers): every rank must call it. */
 bpc_status bpc_finalize(bpc_ctx* ctx);
 
 bpc_status bpc_get_plan(const bpc_ctx* ctx, bpc_plan_summary* out);

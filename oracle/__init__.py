@@ -15,7 +15,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "liboracle.so")
 SRC = os.path.join(HERE, "oracle.c")
-CFLAGS = ["-std=c11", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-Wall"]
+CFLAGS = ["-std=c11", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared", "-Wall"]
 
 
 def build(force: bool = False) -> str:
@@ -71,6 +71,8 @@ def lib():
                                 C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_float,
                                 C.c_void_p, C.c_void_p, C.c_void_p]
         L.orc_push_pull.argtypes = [C.c_uint32, C.c_uint64, C.c_void_p, C.c_void_p]
+        L.orc_set_threads.argtypes = [C.c_int]
+        L.orc_get_threads.restype = C.c_int
         L.orc_adam.argtypes = [C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                C.c_uint32, C.c_float, C.c_float, C.c_float, C.c_float, C.c_float]
         L.orc_nag.argtypes = [C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_float, C.c_float, C.c_float]
@@ -214,6 +216,15 @@ def round_(cfg: Cfg, st: State, grads: np.ndarray, lr: float, want_payloads=True
         raise RuntimeError("orc_round failed")
     st.t += 1
     return delta, p, gt
+
+
+def set_threads(n: int) -> None:
+    """Host threads of round_ (OpenMP over units; results identical for any n)."""
+    lib().orc_set_threads(int(n))
+
+
+def get_threads() -> int:
+    return lib().orc_get_threads()
 
 
 def push_pull(grads: np.ndarray) -> np.ndarray:

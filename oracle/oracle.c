@@ -477,6 +477,14 @@ void orc_lans_block(uint64_t L, const float* gt, float* m, float* v, float* x, u
 }
 
 /* ------------------------------------------------------------------------ */
+/* Host threads for orc_round (OpenMP over units; 1 = plain serial). Units are
+ * independent in Alg. 3/4 (each worker compresses each unit on its own, the
+ * server aggregates each unit on its own, the update is per element / per
+ * block), so the result does not depend on the thread count. */
+static int g_threads = 1;
+void orc_set_threads(int n) { g_threads = n < 1 ? 1 : n; }
+int orc_get_threads(void) { return g_threads; }
+
 int orc_round(const orc_cfg* cfg, uint64_t D, const float* grads, float* e, float* et,
               float* m, float* v, float* x, uint32_t t, float lr,
               uint8_t* delta_out, uint8_t* p_out, float* gtilde_out) {
@@ -487,47 +495,49 @@ int orc_round(const orc_cfg* cfg, uint64_t D, const float* grads, float* e, floa
   const orc_comp* C = &cfg->comp;
   uint32_t n = cfg->n;
 
-  uint64_t total = 0, maxL = 1, maxP = 1;
-  for (int64_t c = 0; c < nc; c++) {
-    uint64_t pb = orc_payload_bytes(C, ch[c].raw, ch[c].len);
-    total += pb;
-    if (ch[c].len > maxL) maxL = ch[c].len;
-    if (pb > maxP) maxP = pb;
-  }
+  /* payload stream: chunk c at byte offset poff[c], no padding */
+  uint64_t* poff = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(nc + 1));
+  poff[0] = 0;
+  for (int64_t c = 0; c < nc; c++) poff[c + 1] = poff[c] + orc_payload_bytes(C, ch[c].raw, ch[c].len);
+  uint64_t total = poff[nc];
   uint8_t* delta = (uint8_t*)malloc((size_t)((n * total) > 0 ? n * total : 1));
   uint8_t* pbuf = (uint8_t*)malloc((size_t)(total ? total : 1));
-  float* q = (float*)malloc(sizeof(float) * maxL);
-  float* dec = (float*)malloc(sizeof(float) * maxL);
-  double* acc = (double*)malloc(sizeof(double) * maxL);
-  float* gt = (float*)malloc(sizeof(float) * maxL);
   float* gall = cfg->optimizer == 1 ? (float*)calloc((size_t)(D ? D : 1), sizeof(float)) : NULL;
   int err = 0;
 
-  /* ---- workers (Alg. 4 lines 5-7; Alg. 3 line 4) */
-  for (uint32_t i = 0; i < n && !err; i++) {
+  /* ---- workers (Alg. 4 lines 5-7; Alg. 3 line 4),
+   * every (worker i, unit c) on its own */
+#pragma omp parallel for schedule(dynamic, 1) num_threads(g_threads) reduction(|: err)
+  for (int64_t w = 0; w < (int64_t)n * nc; w++) {
+    uint32_t i = (uint32_t)(w / nc);
+    int64_t c = w % nc;
     const float* g = grads + (uint64_t)i * D;
     float* ei = e + (uint64_t)i * D;
-    uint64_t off = 0;
-    for (int64_t c = 0; c < nc && !err; c++) {
-      uint64_t L = ch[c].len, o = ch[c].offset;
-      int ef = C->use_ef && !ch[c].raw;     /* raw units carry no EF (R3) */
-      for (uint64_t j = 0; j < L; j++) q[j] = ef ? g[o + j] + ei[o + j] : g[o + j];  /* q = g + e */
-      uint8_t* d = delta + (uint64_t)i * total + off;
-      err |= orc_compress(C, ch[c].raw, q, L, cfg->seed, (uint32_t)c, t, 0, i, d);  /* delta = C(q) */
-      if (ef) {
-        err |= orc_decompress(C, 0, d, L, dec);
-        for (uint64_t j = 0; j < L; j++) ei[o + j] = q[j] - dec[j];                  /* e = q - delta */
-      }
-      off += orc_payload_bytes(C, ch[c].raw, L);
+    uint64_t L = ch[c].len, o = ch[c].offset;
+    int ef = C->use_ef && !ch[c].raw;     /* raw units carry no EF (R3) */
+    float* q = (float*)malloc(sizeof(float) * L);
+    float* dec = (float*)malloc(sizeof(float) * L);
+    for (uint64_t j = 0; j < L; j++) q[j] = ef ? g[o + j] + ei[o + j] : g[o + j];  /* q = g + e */
+    uint8_t* d = delta + (uint64_t)i * total + poff[c];
+    err |= orc_compress(C, ch[c].raw, q, L, cfg->seed, (uint32_t)c, t, 0, i, d);  /* delta = C(q) */
+    if (ef) {
+      err |= orc_decompress(C, 0, d, L, dec);
+      for (uint64_t j = 0; j < L; j++) ei[o + j] = q[j] - dec[j];                  /* e = q - delta */
     }
+    free(q); free(dec);
   }
 
-  /* ---- server (Alg. 4 lines 10-13; Alg. 3 lines 7-8) */
-  uint64_t off = 0;
-  for (int64_t c = 0; c < nc && !err; c++) {
-    uint64_t L = ch[c].len, o = ch[c].offset;
+  /* ---- server (Alg. 4 lines 10-13; Alg. 3 lines 7-8), every unit
+   * on its own, then the workers' g~ = dec(p) and the adaptive update (Alg. 5 l.12-18) */
+#pragma omp parallel for schedule(dynamic, 1) num_threads(g_threads) reduction(|: err)
+  for (int64_t c = 0; c < nc; c++) {
+    if (err) continue;
+    uint64_t L = ch[c].len, o = ch[c].offset, off = poff[c];
     int ef = C->use_ef && !ch[c].raw;
-    uint64_t pb = orc_payload_bytes(C, ch[c].raw, L);
+    float* q = (float*)malloc(sizeof(float) * L);
+    float* dec = (float*)malloc(sizeof(float) * L);
+    float* gt = (float*)malloc(sizeof(float) * L);
+    double* acc = (double*)malloc(sizeof(double) * L);
     for (uint64_t j = 0; j < L; j++) acc[j] = 0.0;
     for (uint32_t i = 0; i < n; i++) {              /* pull delta_i, sum in rank order (R5) */
       err |= orc_decompress(C, ch[c].raw, delta + (uint64_t)i * total + off, L, dec);
@@ -547,18 +557,20 @@ int orc_round(const orc_cfg* cfg, uint64_t D, const float* grads, float* e, floa
     else
       orc_adam(L, gt, m + o, v + o, x + o, t, lr, cfg->beta1, cfg->beta2, cfg->eps, cfg->weight_decay);
     if (gtilde_out) memcpy(gtilde_out + o, gt, sizeof(float) * L);
-    off += pb;
+    free(q); free(dec); free(gt); free(acc);
   }
 
-  if (!err && cfg->optimizer == 1)                  /* LANS: one block per tensor */
-    for (uint32_t b = 0; b < cfg->num_tensors; b++) {
+  if (!err && cfg->optimizer == 1) {                /* LANS: one block per tensor */
+#pragma omp parallel for schedule(dynamic, 1) num_threads(g_threads)
+    for (int64_t b = 0; b < (int64_t)cfg->num_tensors; b++) {
       uint64_t o = cfg->offset[b], L = cfg->numel[b];
       orc_lans_block(L, gall + o, m + o, v + o, x + o, t, lr, cfg->beta1, cfg->beta2, cfg->eps,
                      cfg->weight_decay, cfg->alpha_l, cfg->alpha_u);
     }
+  }
   free(gall);
   if (!err && delta_out) memcpy(delta_out, delta, (size_t)(n * total));
   if (!err && p_out) memcpy(p_out, pbuf, (size_t)total);
-  free(delta); free(pbuf); free(q); free(dec); free(acc); free(gt); free(ch);
+  free(delta); free(pbuf); free(poff); free(ch);
   return err;
 }

@@ -95,6 +95,11 @@ int orc_round(const orc_cfg* cfg, uint64_t D, const float* grads, float* e, floa
               float* m, float* v, float* x, uint32_t t, float lr,
               uint8_t* delta_out, uint8_t* p_out, float* gtilde_out);
 
+/* Host threads of orc_round (OpenMP over units, default 1); the result is the
+ * same for every thread count (units are independent). */
+void orc_set_threads(int n);
+int orc_get_threads(void);
+
 /* Alg. 1 push_pull: p = (1/n) sum_i g_i with fp64 accumulation. */
 void orc_push_pull(uint32_t n, uint64_t D, const float* grads, float* out);
 

@@ -6,9 +6,10 @@ kernels + NCCL.  This package is its thin Python binding.  See DESIGN.md.
 from __future__ import annotations
 
 from ._bpc import (BUF_M, BUF_P, BUF_RECV, BUF_SEND, BUF_SERVER_ERR, BUF_V, BUF_WORKER_ERR, BpcError,
-                   ChunkInfo, Config, Context, EXPORTS, PlanSummary, lib, make_config, plan, unique_id)
+                   ChunkInfo, Config, Context, EXPORTS, PlanSummary, connect_local, lib, make_config, plan,
+                   unique_id)
 
-__all__ = ["Context", "make_config", "plan", "unique_id", "context_for", "BpcError", "lib", "EXPORTS",
+__all__ = ["Context", "make_config", "plan", "unique_id", "connect_local", "context_for", "BpcError", "lib", "EXPORTS",
            "BUF_SEND", "BUF_RECV", "BUF_P", "BUF_WORKER_ERR", "BUF_SERVER_ERR", "BUF_M", "BUF_V",
            "ChunkInfo", "Config", "PlanSummary"]
 

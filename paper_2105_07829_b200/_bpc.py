@@ -60,7 +60,7 @@ class PlanSummary(C.Structure):
                 ("recv_slot_bytes", C.c_uint64), ("server_err_elems", C.c_uint64), ("payload_total", C.c_uint64)]
 
 
-EXPORTS = ["bpc_get_unique_id", "bpc_init", "bpc_plan", "bpc_compress", "bpc_aggregate", "bpc_exchange_push",
+EXPORTS = ["bpc_get_unique_id", "bpc_init", "bpc_plan", "bpc_connect_local", "bpc_compress", "bpc_aggregate", "bpc_exchange_push",
            "bpc_server", "bpc_exchange_pull", "bpc_step", "bpc_sync", "bpc_finalize", "bpc_get_plan",
            "bpc_get_chunk", "bpc_peer_segment", "bpc_buffer", "bpc_copy_state", "bpc_load_state",
            "bpc_get_exchange", "bpc_get_step", "bpc_set_step", "bpc_set_timing", "bpc_get_timing", "bpc_launch_count",
@@ -78,6 +78,7 @@ def lib():
         P = C.c_void_p
         sigs = {
             "bpc_get_unique_id": [P], "bpc_init": [C.POINTER(Config), C.POINTER(C.c_void_p)],
+            "bpc_connect_local": [P, C.c_int32],
             "bpc_plan": [C.POINTER(Config), C.POINTER(PlanSummary), C.POINTER(ChunkInfo), C.c_uint32],
             "bpc_compress": [P, P], "bpc_aggregate": [P], "bpc_exchange_push": [P], "bpc_server": [P],
             "bpc_exchange_pull": [P], "bpc_step": [P, P, C.c_float], "bpc_sync": [P], "bpc_finalize": [P],
@@ -139,6 +140,28 @@ def plan(cfg: Config):
     return s, list(arr[:s.num_chunks])
 
 
+def connect_local(contexts) -> None:
+    """bpc_connect_local: one process's contexts (rank r at index r) as one P2P
+    exchange group with direct device pointers (see bpc.h for the issue order)."""
+    arr = (C.c_void_p * len(contexts))(*[c.h.value for c in contexts])
+    _check(lib().bpc_connect_local(arr, len(contexts)), contexts[0].h)
+
+
+def _device_f32(t, name, numel, device):
+    """Marshalling check of a caller buffer: contiguous fp32 on the context's
+    device with at least the plan's flat_elems values (libbpc checks alignment)."""
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if t.dtype != torch.float32 or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous float32 tensor")
+    if t.device.type != "cuda" or t.device.index != device:
+        raise ValueError(f"{name} must live on cuda:{device} (got {t.device})")
+    if t.numel() < numel:
+        raise ValueError(f"{name} has {t.numel()} elements, the plan needs {numel}")
+    return C.c_void_p(t.data_ptr())
+
+
 class _CAI:
     """Wraps a device pointer for torch.as_tensor (zero copy)."""
 
@@ -155,10 +178,11 @@ class Context:
         h = C.c_void_p()
         _check(lib().bpc_init(C.byref(cfg), C.byref(h)))
         self.h = h
+        self._flat = self.summary().flat_elems
 
     # ---- the hot path
     def compress(self, grad):
-        _check(lib().bpc_compress(self.h, C.c_void_p(grad.data_ptr())), self.h)
+        _check(lib().bpc_compress(self.h, _device_f32(grad, "grad", self._flat, self.cfg.device)), self.h)
 
     def aggregate(self):
         _check(lib().bpc_aggregate(self.h), self.h)
@@ -173,7 +197,8 @@ class Context:
         _check(lib().bpc_exchange_pull(self.h), self.h)
 
     def step(self, params, lr: float):
-        _check(lib().bpc_step(self.h, C.c_void_p(params.data_ptr()), C.c_float(lr)), self.h)
+        _check(lib().bpc_step(self.h, _device_f32(params, "params", self._flat, self.cfg.device), C.c_float(lr)),
+               self.h)
 
     def sync(self):
         _check(lib().bpc_sync(self.h), self.h)

@@ -239,6 +239,7 @@ struct bpc_ctx {
   std::vector<uint8_t*> peer_recv, peer_p;
   std::vector<unsigned long long*> peer_flags;
   uint32_t push_epoch = 0, pull_epoch = 0;
+  bool local_group = false;   // bpc_connect_local: peers are contexts of this process (direct pointers)
   // LANS (BPC_OPT_LANS): per update tile partial sums, per block coefficients
   double* d_lans_part = nullptr;
   // per-tensor units (unit_mode 1): per side, unit tables and totals
@@ -276,6 +277,47 @@ bpc_status cuda_fail(bpc_ctx* c, cudaError_t e, const char* what) {
     }                                                               \
   } while (0)
 
+// Every entry point runs on the context's device and restores the caller's
+// current device on return (a process may drive contexts on several GPUs).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// A caller buffer handed to the kernels: device memory of the context's device
+// (or managed), 16-byte aligned (the kernels bulk-copy it with cp.async.bulk).
+bpc_status check_user_ptr(bpc_ctx* ctx, const void* p, const char* what) {
+  if (!p) {
+    ctx->err = std::string(what) + " is NULL";
+    return BPC_ERR_INVALID_ARGUMENT;
+  }
+  if (reinterpret_cast<uintptr_t>(p) & 15u) {
+    ctx->err = std::string(what) + " is not 16-byte aligned";
+    return BPC_ERR_INVALID_ARGUMENT;
+  }
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    (void)cudaGetLastError();
+    ctx->err = std::string(what) + " is not a CUDA pointer";
+    return BPC_ERR_INVALID_ARGUMENT;
+  }
+  const bool ok = a.type == cudaMemoryTypeManaged || (a.type == cudaMemoryTypeDevice && a.device == ctx->cfg.device);
+  if (!ok) {
+    ctx->err = std::string(what) + " is not device memory of the context's device";
+    return BPC_ERR_INVALID_ARGUMENT;
+  }
+  return BPC_OK;
+}
+
 void timer_begin(bpc_ctx* ctx, int id, cudaEvent_t* ev) {
   if (!ctx->timing) return;
   cudaEventCreate(ev);
@@ -300,6 +342,11 @@ bpc_status upload(bpc_ctx* ctx, T** dst, const std::vector<T>& src) {
 
 void free_ctx(bpc_ctx* ctx) {
   if (!ctx) return;
+  if (ctx->local_group) {   // direct pointers into the other contexts: nothing to close
+    ctx->peer_recv.clear();
+    ctx->peer_p.clear();
+    ctx->peer_flags.clear();
+  }
   for (auto* v : {&ctx->peer_recv, &ctx->peer_p})
     for (int r = 0; r < (int)v->size(); r++)
       if ((*v)[r] && r != ctx->cfg.rank) cudaIpcCloseMemHandle((*v)[r]);
@@ -324,6 +371,23 @@ void free_ctx(bpc_ctx* ctx) {
     cudaEventDestroy(ev.second.second);
   }
   delete ctx;
+}
+
+// The peer arrays are filled (peers' RECV / P / flags): switch to the P2P
+// exchange and size the copy grids of the sparse kinds' exchange kernels.
+void finish_p2p(bpc_ctx* ctx) {
+  const int n = ctx->cfg.world_size, rank = ctx->cfg.rank;
+  const Plan& P = ctx->plan;
+  ctx->exchange = BPC_EXCHANGE_P2P;
+  ctx->peer_recv[rank] = ctx->recv;
+  ctx->peer_p[rank] = ctx->pbuf;
+  ctx->peer_flags[rank] = ctx->d_xflags;
+  // copy grids: one 32 KB round (512 threads x 4 x 16 B) per CTA, <= 2 CTAs per SM
+  auto grid_for = [&](uint64_t bytes) {
+    return (int)std::max<uint64_t>(1, std::min<uint64_t>(2ull * ctx->num_sms, (bytes + 32767) / 32768));
+  };
+  ctx->push_grid = grid_for(P.send_bytes);
+  ctx->pull_grid = grid_for((uint64_t)(n - 1) * P.seg_bytes[rank]);
 }
 
 // BPC_EXCHANGE_P2P setup (collective over all ranks, after the communicator
@@ -402,18 +466,7 @@ bpc_status setup_p2p(bpc_ctx* ctx) {
   cudaFree(d_all);
   cudaFree(d_ok);
   if (st != BPC_OK) return st;
-  if (ok) {
-    ctx->exchange = BPC_EXCHANGE_P2P;
-    ctx->peer_recv[rank] = ctx->recv;
-    ctx->peer_p[rank] = ctx->pbuf;
-    ctx->peer_flags[rank] = ctx->d_xflags;
-    // copy grids: one 32 KB round (512 threads x 4 x 16 B) per CTA, <= 2 CTAs per SM
-    auto grid_for = [&](uint64_t bytes) {
-      return (int)std::max<uint64_t>(1, std::min<uint64_t>(2ull * ctx->num_sms, (bytes + 32767) / 32768));
-    };
-    ctx->push_grid = grid_for(P.send_bytes);
-    ctx->pull_grid = grid_for((uint64_t)(n - 1) * P.seg_bytes[rank]);
-  }
+  if (ok) finish_p2p(ctx);
   return BPC_OK;
 }
 
@@ -549,7 +602,11 @@ bpc_status bpc_init(const bpc_config* cfg, bpc_ctx** out) {
   // device: must be sm_100 (no CPU fallback)
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || cfg->device < 0 || cfg->device >= ndev) return bail(BPC_ERR_CUDA);
-  if (cudaSetDevice(cfg->device) != cudaSuccess) return bail(BPC_ERR_CUDA);
+  DeviceGuard dg(cfg->device);   // restores the caller's device on return
+  {
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess || cur != cfg->device) return bail(BPC_ERR_CUDA);
+  }
   cudaDeviceProp prop;
   if (cudaGetDeviceProperties(&prop, cfg->device) != cudaSuccess || prop.major != 10) return bail(BPC_ERR_CUDA);
   const Plan& P = ctx->plan;
@@ -695,9 +752,76 @@ bpc_status bpc_init(const bpc_config* cfg, bpc_ctx** out) {
   return BPC_OK;
 }
 
+bpc_status bpc_connect_local(bpc_ctx* const* ctxs, int32_t n) {
+  if (!ctxs || n < 2 || n > P2P_MAXJ) return BPC_ERR_INVALID_ARGUMENT;
+  for (int r = 0; r < n; r++) {
+    bpc_ctx* c = ctxs[r];
+    if (!c) return BPC_ERR_INVALID_ARGUMENT;
+    if (c->cfg.world_size != n || c->cfg.rank != r || c->comm || c->local_group || c->phase != 0 ||
+        c->t != 1) {
+      c->err = "bpc_connect_local: needs fresh contexts of world_size n, rank r at index r, no NCCL id";
+      return BPC_ERR_BAD_STATE;
+    }
+    const Plan& a = c->plan;
+    const Plan& b = ctxs[0]->plan;
+    if (a.chunks.size() != b.chunks.size() || a.send_bytes != b.send_bytes || a.seg_bytes != b.seg_bytes) {
+      c->err = "bpc_connect_local: the contexts' plans differ";
+      return BPC_ERR_SIZE_MISMATCH;
+    }
+  }
+  // peer access between distinct devices (both directions)
+  for (int a = 0; a < n; a++)
+    for (int b = 0; b < n; b++) {
+      const int da = ctxs[a]->cfg.device, db = ctxs[b]->cfg.device;
+      if (da == db) continue;
+      int can = 0;
+      if (cudaDeviceCanAccessPeer(&can, da, db) != cudaSuccess || !can) {
+        ctxs[a]->err = "bpc_connect_local: no peer access between the contexts' devices";
+        return BPC_ERR_CUDA;
+      }
+      DeviceGuard dg(da);
+      const cudaError_t e = cudaDeviceEnablePeerAccess(db, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return cuda_fail(ctxs[a], e, "peer access");
+      (void)cudaGetLastError();
+    }
+  for (int r = 0; r < n; r++) {
+    bpc_ctx* ctx = ctxs[r];
+    DeviceGuard dg(ctx->cfg.device);
+    if (!ctx->d_xflags) {
+      CK(cudaMalloc((void**)&ctx->d_xflags, 16ull * n), "alloc exchange flags");
+      CK(cudaMemset(ctx->d_xflags, 0, 16ull * n), "zero exchange flags");
+    }
+    if (!ctx->d_xdone) {
+      CK(cudaMalloc((void**)&ctx->d_xdone, 16), "alloc exchange counters");
+      CK(cudaMemset(ctx->d_xdone, 0, 16), "zero exchange counters");
+    }
+  }
+  for (int r = 0; r < n; r++) {
+    bpc_ctx* ctx = ctxs[r];
+    ctx->peer_recv.assign(n, nullptr);
+    ctx->peer_p.assign(n, nullptr);
+    ctx->peer_flags.assign(n, nullptr);
+    for (int q = 0; q < n; q++) {
+      ctx->peer_recv[q] = ctxs[q]->recv;
+      ctx->peer_p[q] = ctxs[q]->pbuf;
+      ctx->peer_flags[q] = ctxs[q]->d_xflags;
+    }
+    ctx->local_group = true;
+    finish_p2p(ctx);
+  }
+  for (int r = 0; r < n; r++) {
+    DeviceGuard dg(ctxs[r]->cfg.device);
+    bpc_ctx* ctx = ctxs[r];
+    CK(cudaDeviceSynchronize(), "connect sync");
+  }
+  return BPC_OK;
+}
+
 bpc_status bpc_compress(bpc_ctx* ctx, const float* d_grad) {
-  if (!ctx || !d_grad) return BPC_ERR_INVALID_ARGUMENT;
+  if (!ctx) return BPC_ERR_INVALID_ARGUMENT;
   if (ctx->phase != 0) return BPC_ERR_BAD_STATE;
+  DeviceGuard dg(ctx->cfg.device);
+  if (bpc_status st = check_user_ptr(ctx, d_grad, "d_grad")) return st;
   cudaEvent_t b = nullptr;
   timer_begin(ctx, BPC_TIMER_COMPRESS, &b);
   if (stream_worker(ctx->cfg.comp.kind)) {
@@ -751,14 +875,17 @@ bpc_status bpc_compress(bpc_ctx* ctx, const float* d_grad) {
 bpc_status bpc_exchange_push(bpc_ctx* ctx) {
   if (!ctx) return BPC_ERR_INVALID_ARGUMENT;
   if (ctx->phase != 1) return BPC_ERR_BAD_STATE;
+  DeviceGuard dg(ctx->cfg.device);
   const int n = ctx->cfg.world_size, rank = ctx->cfg.rank;
-  if (n > 1 && ctx->comm && !fused_exchange(ctx)) {
+  if (n > 1 && (ctx->comm || ctx->local_group) && !fused_exchange(ctx)) {
     const Plan& P = ctx->plan;
     cudaEvent_t b = nullptr;
     timer_begin(ctx, BPC_TIMER_PUSH, &b);
     const uint64_t slot = P.seg_bytes[rank];
     if (ctx->exchange == BPC_EXCHANGE_P2P) {
-      // segment r of SEND -> slot `rank` of owner r's RECV (the local one included)
+      // segment r of SEND -> slot `rank` of owner r's RECV (the local one included),
+      // then release the push flag on every peer; bpc_server waits for the peers'
+      // flags before its first read of RECV
       P2PParams q = {};
       for (int r = 0; r < n; r++) {
         if (!P.seg_bytes[r]) continue;
@@ -766,19 +893,13 @@ bpc_status bpc_exchange_push(bpc_ctx* ctx) {
         q.dst[q.njobs] = ctx->peer_recv[r] + (uint64_t)rank * P.seg_bytes[r];
         q.len[q.njobs++] = P.seg_bytes[r];
       }
-      P2PWait w = {};
-      for (int r = 0; r < n; r++) {
-        if (r == rank) continue;
-        q.peer_flag[q.npeers++] = ctx->peer_flags[r];
-        w.slots[w.nslots++] = r;
-      }
+      for (int r = 0; r < n; r++)
+        if (r != rank) q.peer_flag[q.npeers++] = ctx->peer_flags[r];
       q.slot = rank;
-      q.epoch = w.epoch = ++ctx->push_epoch;
+      q.epoch = ++ctx->push_epoch;
       q.done = ctx->d_xdone;
-      w.flags = ctx->d_xflags;
       CK(launch_p2p_copy(q, ctx->push_grid, ctx->stream), "push copy launch");
-      CK(launch_p2p_wait(w, ctx->stream), "push wait launch");
-      ctx->launches += 2;
+      ctx->launches += 1;
     } else {
       NK(ncclGroupStart(), "group start");
       for (int r = 0; r < n; r++) {
@@ -798,9 +919,26 @@ bpc_status bpc_exchange_push(bpc_ctx* ctx) {
   return BPC_OK;
 }
 
+// sparse kinds over the P2P exchange: one warp waits for every peer's release of
+// flag slots [slot0, slot0 + n) at `epoch` before the consumer kernel reads
+static bpc_status launch_flag_wait(bpc_ctx* ctx, int slot0, uint32_t epoch, const char* what) {
+  P2PWait w = {};
+  for (int r = 0; r < ctx->cfg.world_size; r++)
+    if (r != ctx->cfg.rank) w.slots[w.nslots++] = slot0 + r;
+  w.flags = ctx->d_xflags;
+  w.epoch = epoch;
+  CK(launch_p2p_wait(w, ctx->stream), what);
+  ctx->launches++;
+  return BPC_OK;
+}
+static bool sparse_p2p(const bpc_ctx* ctx) {
+  return ctx->cfg.world_size > 1 && ctx->exchange == BPC_EXCHANGE_P2P && !fused_exchange(ctx);
+}
+
 bpc_status bpc_server(bpc_ctx* ctx) {
   if (!ctx) return BPC_ERR_INVALID_ARGUMENT;
   if (ctx->phase != 2) return BPC_ERR_BAD_STATE;
+  DeviceGuard dg(ctx->cfg.device);
   // n == 1: RECV aliases SEND, recv offsets equal payload offsets (one segment)
   const uint64_t slot = ctx->cfg.world_size == 1 ? 0 : ctx->plan.seg_bytes[ctx->cfg.rank];
   cudaEvent_t b = nullptr;
@@ -849,6 +987,9 @@ bpc_status bpc_server(bpc_ctx* ctx) {
     }
     CK(launch_stream_side(ctx, true, q), "server stream launch");
   } else {
+    if (sparse_p2p(ctx)) {   // every rank's delta has landed in RECV
+      if (bpc_status st = launch_flag_wait(ctx, 0, ctx->push_epoch, "push wait launch")) return st;
+    }
     CompressParams p = base_params(ctx);
     p.recv = ctx->recv;
     p.slot_bytes = slot;
@@ -870,15 +1011,16 @@ bpc_status bpc_server(bpc_ctx* ctx) {
 bpc_status bpc_exchange_pull(bpc_ctx* ctx) {
   if (!ctx) return BPC_ERR_INVALID_ARGUMENT;
   if (ctx->phase != 3) return BPC_ERR_BAD_STATE;
+  DeviceGuard dg(ctx->cfg.device);
   const int n = ctx->cfg.world_size, rank = ctx->cfg.rank;
-  if (n > 1 && ctx->comm && !fused_exchange(ctx)) {
+  if (n > 1 && (ctx->comm || ctx->local_group) && !fused_exchange(ctx)) {
     const Plan& P = ctx->plan;
     cudaEvent_t b = nullptr;
     timer_begin(ctx, BPC_TIMER_PULL, &b);
     if (ctx->exchange == BPC_EXCHANGE_P2P) {
-      // my segment of P -> the same offset of every peer's P
+      // my segment of P -> the same offset of every peer's P, then release the pull
+      // flag on every peer; bpc_step waits for the peers' flags before it decodes
       P2PParams q = {};
-      P2PWait w = {};
       for (int r = 0; r < n; r++) {
         if (r == rank) continue;
         if (P.seg_bytes[rank]) {
@@ -887,15 +1029,12 @@ bpc_status bpc_exchange_pull(bpc_ctx* ctx) {
           q.len[q.njobs++] = P.seg_bytes[rank];
         }
         q.peer_flag[q.npeers++] = ctx->peer_flags[r];
-        w.slots[w.nslots++] = n + r;
       }
       q.slot = n + rank;
-      q.epoch = w.epoch = ++ctx->pull_epoch;
+      q.epoch = ++ctx->pull_epoch;
       q.done = ctx->d_xdone + 1;
-      w.flags = ctx->d_xflags;
       CK(launch_p2p_copy(q, ctx->pull_grid, ctx->stream), "pull copy launch");
-      CK(launch_p2p_wait(w, ctx->stream), "pull wait launch");
-      ctx->launches += 2;
+      ctx->launches += 1;
     } else {
       NK(ncclGroupStart(), "group start");
       for (int r = 0; r < n; r++) {
@@ -913,7 +1052,7 @@ bpc_status bpc_exchange_pull(bpc_ctx* ctx) {
 
 bpc_status bpc_aggregate(bpc_ctx* ctx) {
   if (!ctx) return BPC_ERR_INVALID_ARGUMENT;
-  if (ctx->cfg.world_size > 1 && !ctx->comm) return BPC_ERR_BAD_STATE;
+  if (ctx->cfg.world_size > 1 && !ctx->comm && !ctx->local_group) return BPC_ERR_BAD_STATE;
   bpc_status s = bpc_exchange_push(ctx);
   if (s != BPC_OK) return s;
   if ((s = bpc_server(ctx)) != BPC_OK) return s;
@@ -921,8 +1060,10 @@ bpc_status bpc_aggregate(bpc_ctx* ctx) {
 }
 
 bpc_status bpc_step(bpc_ctx* ctx, float* d_params, float lr) {
-  if (!ctx || !d_params) return BPC_ERR_INVALID_ARGUMENT;
+  if (!ctx) return BPC_ERR_INVALID_ARGUMENT;
   if (ctx->phase != 4) return BPC_ERR_BAD_STATE;
+  DeviceGuard dg(ctx->cfg.device);
+  if (bpc_status st = check_user_ptr(ctx, d_params, "d_params")) return st;
   const bpc_config& c = ctx->cfg;
   UpdateParams p = {};
   p.pbuf = ctx->pbuf;
@@ -954,6 +1095,9 @@ bpc_status bpc_step(bpc_ctx* ctx, float* d_params, float lr) {
   }
   cudaEvent_t b = nullptr;
   timer_begin(ctx, BPC_TIMER_UPDATE, &b);
+  if (sparse_p2p(ctx)) {   // every owner's p has landed in P
+    if (bpc_status st = launch_flag_wait(ctx, c.world_size, ctx->pull_epoch, "pull wait launch")) return st;
+  }
   const bool sparse = c.comp.kind == BPC_TOP_K || c.comp.kind == BPC_RANDOM_K;
   auto pass = [&](int mode) -> cudaError_t {
     p.mode = mode;
@@ -988,6 +1132,7 @@ bpc_status bpc_step(bpc_ctx* ctx, float* d_params, float lr) {
 
 bpc_status bpc_sync(bpc_ctx* ctx) {
   if (!ctx) return BPC_ERR_INVALID_ARGUMENT;
+  DeviceGuard dg(ctx->cfg.device);
   CK(cudaStreamSynchronize(ctx->stream), "stream sync");
   if (ctx->comm) {
     ncclResult_t ar;
@@ -1008,9 +1153,25 @@ bpc_status bpc_sync(bpc_ctx* ctx) {
 
 bpc_status bpc_finalize(bpc_ctx* ctx) {
   if (!ctx) return BPC_ERR_INVALID_ARGUMENT;
+  DeviceGuard dg(ctx->cfg.device);
+  bpc_status st = BPC_OK;
   cudaStreamSynchronize(ctx->stream);
+  if (ctx->comm && ctx->exchange == BPC_EXCHANGE_P2P) {
+    // Collective teardown: a peer's last update may still be reading this
+    // rank's P (or its last push writing this rank's RECV) over NVLink after
+    // this rank's stream drained.  An all-reduce over the communicator, run
+    // after every rank's stream drained, orders the frees after all of them.
+    int32_t* d = nullptr;
+    if (cudaMalloc((void**)&d, 4) == cudaSuccess && cudaMemsetAsync(d, 0, 4, ctx->stream) == cudaSuccess &&
+        ncclAllReduce(d, d, 1, ncclInt32, ncclSum, ctx->comm, ctx->stream) == ncclSuccess) {
+      if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) st = BPC_ERR_CUDA;
+    } else {
+      st = BPC_ERR_NCCL;
+    }
+    if (d) cudaFree(d);
+  }
   free_ctx(ctx);
-  return BPC_OK;
+  return st;
 }
 
 bpc_status bpc_get_plan(const bpc_ctx* ctx, bpc_plan_summary* out) {
@@ -1055,6 +1216,7 @@ bpc_status bpc_copy_state(bpc_ctx* ctx, int32_t which, void* host_dst, uint64_t 
   void* p;
   uint64_t b;
   if (!ctx || !host_dst || !buffer_of(ctx, which, &p, &b)) return BPC_ERR_INVALID_ARGUMENT;
+  DeviceGuard dg(ctx->cfg.device);
   if (bytes != b) return BPC_ERR_SIZE_MISMATCH;
   CK(cudaStreamSynchronize(ctx->stream), "sync");
   if (b) CK(cudaMemcpy(host_dst, p, b, cudaMemcpyDeviceToHost), "copy state");
@@ -1065,6 +1227,7 @@ bpc_status bpc_load_state(bpc_ctx* ctx, int32_t which, const void* host_src, uin
   void* p;
   uint64_t b;
   if (!ctx || !host_src || !buffer_of(ctx, which, &p, &b)) return BPC_ERR_INVALID_ARGUMENT;
+  DeviceGuard dg(ctx->cfg.device);
   if (bytes != b) return BPC_ERR_SIZE_MISMATCH;
   CK(cudaStreamSynchronize(ctx->stream), "sync");
   if (b) CK(cudaMemcpy(p, host_src, b, cudaMemcpyHostToDevice), "load state");
@@ -1091,6 +1254,7 @@ bpc_status bpc_set_step(bpc_ctx* ctx, uint32_t t) {
 
 bpc_status bpc_set_timing(bpc_ctx* ctx, int32_t enable) {
   if (!ctx) return BPC_ERR_INVALID_ARGUMENT;
+  DeviceGuard dg(ctx->cfg.device);
   cudaStreamSynchronize(ctx->stream);
   for (auto& ev : ctx->events) {
     cudaEventDestroy(ev.second.first);
@@ -1103,6 +1267,7 @@ bpc_status bpc_set_timing(bpc_ctx* ctx, int32_t enable) {
 
 bpc_status bpc_get_timing(bpc_ctx* ctx, float ms[BPC_NUM_TIMERS], uint32_t count[BPC_NUM_TIMERS]) {
   if (!ctx || !ms || !count) return BPC_ERR_INVALID_ARGUMENT;
+  DeviceGuard dg(ctx->cfg.device);
   for (int i = 0; i < BPC_NUM_TIMERS; i++) {
     ms[i] = 0.f;
     count[i] = 0;

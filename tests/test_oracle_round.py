@@ -245,3 +245,22 @@ def test_round_deterministic_and_c1_fast(orc):
     assert time.time() - t0 < 10.0   # "CPU oracle in seconds" (BASELINE.json configs[0])
     for a, b in zip(*runs):
         assert a.tobytes() == b.tobytes()
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C4"])
+def test_round_thread_count_invariant(orc, name):
+    # the OpenMP build (bench.py's all-cores cpu_baseline) must give the serial
+    # result bit for bit: units are independent in Alg. 3/4 and the update
+    w = config(name, n=2, scale=64)
+    cfg = orc.Cfg.from_workload(w)
+    offs, D = layout(w.tensor_numels())
+    outs = []
+    for threads in (1, 4):
+        orc.set_threads(threads)
+        st = orc.State(w.n, D, gen_params(w))
+        for step in (1, 2):
+            g = np.stack([gen_grad(w, i, step) for i in range(w.n)])
+            d, p, _ = orc.round_(cfg, st, g, w.lr)
+        outs.append((d.tobytes(), p.tobytes(), st.e.tobytes(), st.et.tobytes(), st.m.tobytes(), st.x.tobytes()))
+    orc.set_threads(1)
+    assert outs[0] == outs[1]
