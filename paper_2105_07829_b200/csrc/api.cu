@@ -215,8 +215,18 @@ struct bpc_ctx {
   uint64_t recv_bytes = 0;
   DevChunk* d_chunks = nullptr;
   uint32_t *d_witems = nullptr, *d_sitems = nullptr;
-  Tile *d_wraw = nullptr, *d_sraw = nullptr, *d_utiles = nullptr;
-  uint32_t n_witems = 0, n_sitems = 0, n_wraw = 0, n_sraw = 0, n_utiles = 0;
+  Tile* d_utiles = nullptr;
+  uint32_t n_witems = 0, n_sitems = 0, n_utiles = 0;
+  // sparse kinds (kernels_sparse.cu), per side (0 worker, 1 server): chunk -> unit,
+  // candidate thresholds, counters, candidate lists
+  uint32_t* d_chunk2u[2] = {nullptr, nullptr};
+  uint32_t* d_guess[2] = {nullptr, nullptr};
+  uint32_t* d_cnt[2] = {nullptr, nullptr};
+  uint32_t* d_cand[2] = {nullptr, nullptr};
+  uint32_t* d_cand_off[2] = {nullptr, nullptr};
+  uint32_t sel_cap[2] = {0, 0};                  // CTA select kernel: candidates in shared memory
+  uint32_t* d_big[2] = {nullptr, nullptr};       // units handed from the warp to the CTA select
+  float* d_sdelta = nullptr;   // server Delta of the owned units (sparse kinds without EF)
   unsigned int* d_flag = nullptr;
   // streaming worker (norm-based compressors): slices, partials, unit counters
   Slice* d_wslices = nullptr;
@@ -361,7 +371,10 @@ void free_ctx(bpc_ctx* ctx) {
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   for (void* p : {(void*)ctx->e, (void*)ctx->etl, (void*)ctx->m, (void*)ctx->v, (void*)ctx->send,
                   (void*)ctx->pbuf, (void*)ctx->d_chunks, (void*)ctx->d_witems, (void*)ctx->d_sitems,
-                  (void*)ctx->d_wraw, (void*)ctx->d_sraw, (void*)ctx->d_utiles, (void*)ctx->d_flag,
+                  (void*)ctx->d_utiles, (void*)ctx->d_flag, (void*)ctx->d_sdelta,
+                  (void*)ctx->d_chunk2u[0], (void*)ctx->d_chunk2u[1], (void*)ctx->d_guess[0], (void*)ctx->d_guess[1],
+                  (void*)ctx->d_cnt[0], (void*)ctx->d_cnt[1], (void*)ctx->d_cand[0], (void*)ctx->d_cand[1],
+                  (void*)ctx->d_cand_off[0], (void*)ctx->d_cand_off[1], (void*)ctx->d_big[0], (void*)ctx->d_big[1],
                   (void*)ctx->d_wslices, (void*)ctx->d_wpartials, (void*)ctx->d_wcounters,
                   (void*)ctx->d_sslices, (void*)ctx->d_spartials, (void*)ctx->d_scounters})
     if (p) cudaFree(p);
@@ -517,21 +530,32 @@ cudaError_t launch_stream_side(bpc_ctx* ctx, bool server, StreamParams& q) {
   return e;
 }
 
-CompressParams base_params(bpc_ctx* ctx) {
-  CompressParams p = {};
+SparseParams sparse_params(bpc_ctx* ctx, int side) {
+  SparseParams p = {};
   p.chunks = ctx->d_chunks;
-  p.cs = ctx->plan.cs;
+  p.items = side ? ctx->d_sitems : ctx->d_witems;
+  p.n_units = side ? ctx->n_sitems : ctx->n_witems;
+  p.slices = side ? ctx->d_sslices : ctx->d_wslices;
+  p.n_slices = side ? ctx->n_sslices : ctx->n_wslices;
+  p.chunk2u = ctx->d_chunk2u[side];
+  p.guess = ctx->d_guess[side];
+  p.cnt = ctx->d_cnt[side];
+  p.cand = ctx->d_cand[side];
+  p.cand_off = ctx->d_cand_off[side];
   p.n = (uint32_t)ctx->cfg.world_size;
   p.inv_n = 1.0 / (double)ctx->cfg.world_size;
   p.t = ctx->t;
-  p.rank = (uint32_t)ctx->cfg.rank;
+  p.stage = side ? 1u : 0u;
+  p.rrank = side ? 0u : (uint32_t)ctx->cfg.rank;
   p.seed = ctx->cfg.seed;
-  p.bits = ctx->cfg.comp.bits;
+  p.server = side;
   p.randk_scaled = ctx->cfg.comp.randk_scaled;
   p.use_ef = ctx->cfg.comp.use_ef;
   p.f16 = ctx->cfg.comp.f16_values;
   p.check_finite = ctx->cfg.check_finite;
   p.flag = ctx->d_flag;
+  p.sel_cap = ctx->sel_cap[side];
+  p.big = ctx->d_big[side];
   return p;
 }
 
@@ -637,8 +661,10 @@ bpc_status bpc_init(const bpc_config* cfg, bpc_ctx** out) {
   // device tables
   std::vector<DevChunk> dch(P.chunks.size());
   std::vector<uint32_t> witems, sitems;
-  std::vector<Tile> wraw, sraw, utiles;
+  std::vector<Tile> utiles;
   std::vector<uint32_t> blk_tile;   // first update tile of each tensor
+  const bool sparse_kind = !stream_worker(cfg->comp.kind);
+  uint64_t sd_elems = 0;            // server Delta scratch (sparse kinds without EF)
   for (uint32_t c = 0; c < P.chunks.size(); c++) {
     const auto& ci = P.chunks[c];
     DevChunk& d = dch[c];
@@ -655,11 +681,9 @@ bpc_status bpc_init(const bpc_config* cfg, bpc_ctx** out) {
     if (!ci.raw) {
       witems.push_back(c);
       if (mine) sitems.push_back(c);
-    } else {
-      for (uint64_t s0 = 0; s0 < ci.len; s0 += kSlice) {
-        Tile tl = {c, (uint32_t)s0, (uint32_t)std::min<uint64_t>(kSlice, ci.len - s0), 0};
-        wraw.push_back(tl);
-        if (mine) sraw.push_back(tl);
+      if (mine && sparse_kind && !cfg->comp.use_ef) {   // the server's Delta lives in the scratch
+        d.etl = sd_elems;
+        sd_elems += round_up(ci.len, 4);
       }
     }
     if (blk_tile.size() <= ci.tensor) blk_tile.resize(ci.tensor + 1, (uint32_t)utiles.size());
@@ -672,13 +696,44 @@ bpc_status bpc_init(const bpc_config* cfg, bpc_ctx** out) {
   if ((s = upload(ctx, &ctx->d_chunks, dch)) != BPC_OK) return bail(s);
   if ((s = upload(ctx, &ctx->d_witems, witems)) != BPC_OK) return bail(s);
   if ((s = upload(ctx, &ctx->d_sitems, sitems)) != BPC_OK) return bail(s);
-  if ((s = upload(ctx, &ctx->d_wraw, wraw)) != BPC_OK) return bail(s);
-  if ((s = upload(ctx, &ctx->d_sraw, sraw)) != BPC_OK) return bail(s);
   if ((s = upload(ctx, &ctx->d_utiles, utiles)) != BPC_OK) return bail(s);
   ctx->n_witems = (uint32_t)witems.size();
   ctx->n_sitems = (uint32_t)sitems.size();
-  ctx->n_wraw = (uint32_t)wraw.size();
-  ctx->n_sraw = (uint32_t)sraw.size();
+  if (sparse_kind) {
+    // per side: chunk -> unit, candidate capacity per unit (the
+    // guess keeps ~1.5-5 k candidates; the lists hold about twice that, the server
+    // also the n ranks' k entries), counters zeroed once (the select kernel resets)
+    for (int side = 0; side < 2; side++) {
+      const std::vector<uint32_t>& items = side ? sitems : witems;
+      std::vector<uint32_t> c2u(P.chunks.size(), 0xffffffffu), off(items.size() + 1, 0);
+      for (uint32_t u = 0; u < items.size(); u++) {
+        const auto& ci = P.chunks[items[u]];
+        const uint64_t L = ci.len, k = ci.k;
+        uint64_t cap;
+        if (cfg->comp.kind == BPC_RANDOM_K) {
+          cap = k + (uint64_t)(16.0 * std::sqrt((double)k)) + 256;
+        } else {
+          cap = L <= 4096 ? L : (uint64_t)std::ceil(2.0 * sparse_sample_rank((uint32_t)k, (uint32_t)L) * (double)L / 4096.0) + 1024;
+          if (side) cap += (uint64_t)n * k;
+        }
+        c2u[items[u]] = u;
+        off[u + 1] = off[u] + (uint32_t)std::min<uint64_t>(L, cap);
+        ctx->sel_cap[side] = std::max<uint32_t>(ctx->sel_cap[side], (uint32_t)std::min<uint64_t>(L, cap));
+      }
+      // a power of two: the bitonic sorts of the tie / selection lists (<= the
+      // candidate count) pad to the next power of two inside this region
+      uint32_t sc = 1;
+      while (sc < ctx->sel_cap[side]) sc <<= 1;
+      ctx->sel_cap[side] = std::min<uint32_t>(sc, SEL_CAP);
+      if ((s = upload(ctx, &ctx->d_chunk2u[side], c2u)) != BPC_OK) return bail(s);
+      if ((s = upload(ctx, &ctx->d_cand_off[side], off)) != BPC_OK) return bail(s);
+      if ((ce = alloc((void**)&ctx->d_guess[side], 4ull * items.size())) != cudaSuccess) return bail(cuda_fail(ctx, ce, "alloc guesses"));
+      if ((ce = alloc((void**)&ctx->d_cnt[side], 4ull * items.size())) != cudaSuccess) return bail(cuda_fail(ctx, ce, "alloc counters"));
+      if ((ce = alloc((void**)&ctx->d_cand[side], 4ull * off.back())) != cudaSuccess) return bail(cuda_fail(ctx, ce, "alloc candidates"));
+      if ((ce = alloc((void**)&ctx->d_big[side], 4ull * items.size())) != cudaSuccess) return bail(cuda_fail(ctx, ce, "alloc select flags"));
+    }
+    if ((ce = alloc((void**)&ctx->d_sdelta, 4ull * sd_elems)) != cudaSuccess) return bail(cuda_fail(ctx, ce, "alloc Delta scratch"));
+  }
   ctx->n_utiles = (uint32_t)utiles.size();
   if (cfg->optimizer == BPC_OPT_LANS) {
     blk_tile.push_back((uint32_t)utiles.size());   // [num_tensors + 1]
@@ -727,15 +782,6 @@ bpc_status bpc_init(const bpc_config* cfg, bpc_ctx** out) {
     }
   }
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cfg->device);
-  // the sparse kinds' cluster shape must be schedulable
-  if (!stream_worker(cfg->comp.kind)) {
-    int maxc = 0;
-    ce = compress_max_active_clusters(cfg->comp.kind, false, P.cs, &maxc);
-    if (ce != cudaSuccess || maxc < 1) {
-      ctx->err = "cluster of " + std::to_string(P.cs) + " CTAs is not schedulable";
-      return bail(BPC_ERR_CUDA);
-    }
-  }
   if ((ce = cudaDeviceSynchronize()) != cudaSuccess) return bail(cuda_fail(ctx, ce, "init sync"));
   // NCCL communicator (collective over all ranks)
   if (cfg->nccl_unique_id && n > 1) {
@@ -855,17 +901,12 @@ bpc_status bpc_compress(bpc_ctx* ctx, const float* d_grad) {
     }
     CK(launch_stream_side(ctx, false, q), "worker stream launch");
   } else {
-    CompressParams p = base_params(ctx);
+    SparseParams p = sparse_params(ctx, 0);
     p.grad = d_grad;
-    p.err = ctx->e;
+    p.vals = ctx->e;
     p.out = ctx->send;
-    p.items = ctx->d_witems;
-    p.n_items = ctx->n_witems;
-    p.raw_tiles = ctx->d_wraw;
-    p.n_raw_tiles = ctx->n_wraw;
-    p.stage = 0;
-    CK(launch_compress(ctx->cfg.comp.kind, false, p, ctx->stream), "worker compress launch");
-    ctx->launches++;
+    CK(launch_sparse(ctx->cfg.comp.kind, p, 2 * ctx->num_sms, ctx->stream), "worker sparse launch");
+    ctx->launches += 3;
   }
   timer_end(ctx, BPC_TIMER_COMPRESS, b);
   ctx->phase = 1;
@@ -990,18 +1031,13 @@ bpc_status bpc_server(bpc_ctx* ctx) {
     if (sparse_p2p(ctx)) {   // every rank's delta has landed in RECV
       if (bpc_status st = launch_flag_wait(ctx, 0, ctx->push_epoch, "push wait launch")) return st;
     }
-    CompressParams p = base_params(ctx);
+    SparseParams p = sparse_params(ctx, 1);
     p.recv = ctx->recv;
     p.slot_bytes = slot;
-    p.etl = ctx->etl;
+    p.vals = ctx->cfg.comp.use_ef ? ctx->etl : ctx->d_sdelta;
     p.out = ctx->pbuf;
-    p.items = ctx->d_sitems;
-    p.n_items = ctx->n_sitems;
-    p.raw_tiles = ctx->d_sraw;
-    p.n_raw_tiles = ctx->n_sraw;
-    p.stage = 1;
-    CK(launch_compress(ctx->cfg.comp.kind, true, p, ctx->stream), "server launch");
-    ctx->launches++;
+    CK(launch_sparse(ctx->cfg.comp.kind, p, 2 * ctx->num_sms, ctx->stream), "server sparse launch");
+    ctx->launches += 3;
   }
   timer_end(ctx, BPC_TIMER_SERVER, b);
   ctx->phase = 3;
@@ -1080,6 +1116,8 @@ bpc_status bpc_step(bpc_ctx* ctx, float* d_params, float lr) {
   // bias corrections 1 - beta^t, fp64 then one rounding (R16); the kernels divide
   p.bc1 = (float)(1.0 - std::pow((double)c.beta1, (double)ctx->t));
   p.bc2 = (float)(1.0 - std::pow((double)c.beta2, (double)ctx->t));
+  p.ibc1 = 1.0f / p.bc1;   // RN(1 / bc): IEEE fp32 division on the host
+  p.ibc2 = 1.0f / p.bc2;
   p.eps = c.eps;
   p.lr = lr;
   p.wd = c.weight_decay;

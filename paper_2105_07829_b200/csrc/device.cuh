@@ -124,8 +124,8 @@ __device__ __forceinline__ long long clock64_v() {   // not hoisted out of the w
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, uint32_t tag = 0) {
   if (mbar_try(bar, parity)) return;
   const long long t0 = clock64_v();
-  while (!mbar_try_sleep(bar, parity, 20000u)) {
-    if (clock64_v() - t0 > BPC_WATCHDOG_CYCLES)
+  for (uint32_t it = 1; !mbar_try_sleep(bar, parity, 20000u); it++) {   // clock read every 16 tries
+    if ((it & 15) == 0 && clock64_v() - t0 > BPC_WATCHDOG_CYCLES)
       watchdog_fire("mbarrier", tag, parity, (unsigned long long)smem_u32(bar), 0);
   }
 }
@@ -164,7 +164,7 @@ __device__ __forceinline__ void wait_counter(const unsigned long long* p, unsign
   if (v < target) {
     const long long t0 = clock64_v();
     for (uint32_t it = 1; (v = ld_relaxed(p)) < target; it++) {
-      __nanosleep(256);
+      __nanosleep(512);
       if ((it & 63) == 0) {
         if (clock64_v() - t0 > BPC_WATCHDOG_CYCLES) watchdog_fire("counter", tag, 0, v, target);
       }
@@ -233,11 +233,89 @@ __device__ __forceinline__ float fadd(float a, float b) { return __fadd_rn(a, b)
 __device__ __forceinline__ float fsub(float a, float b) { return __fsub_rn(a, b); }
 __device__ __forceinline__ float fmul(float a, float b) { return __fmul_rn(a, b); }
 __device__ __forceinline__ float fdiv(float a, float b) { return __fdiv_rn(a, b); }
+// a / b and sqrt(a) with the +-0 operand answered directly: the IEEE sequences send
+// zero operands to their slow-path subroutines, and the moments of coordinates
+// whose aggregated gradient stays 0 (sparse kinds; BERT's unused embedding rows)
+// are exactly 0 (same results: +-0 / b = +-0 for b > 0, sqrt(+-0) = +-0; 0 / 0
+// still takes the IEEE division)
+__device__ __forceinline__ float fdiv_pos(float a, float b) { return (a == 0.f && b > 0.f) ? a : __fdiv_rn(a, b); }
+__device__ __forceinline__ float fsqrt0(float a) { return a == 0.f ? a : __fsqrt_rn(a); }
+// a / b correctly rounded for a per-launch constant divisor b with y = RN(1/b)
+// (Markstein: q = RN(a y) is within an ulp, the residual a - b q is exact by
+// FMA, and RN(q + r y) is RN(a / b)), two FMAs instead of the IEEE division
+// sequence.  The theorem needs the residual not to underflow: |a| < 2^-100
+// takes the IEEE division (checked bit for bit against a / b for the Adam bias
+// corrections over 2.9e8 cases, tests/test_divc.py).
+__device__ __forceinline__ float divc(float a, float b, float y) {
+  if (fabsf(a) < 0x1p-100f) return a == 0.f ? a : __fdiv_rn(a, b);   // +-0 / b = +-0 (b > 0)
+  const float q = __fmul_rn(a, y);
+  const float r = __fmaf_rn(-q, b, a);
+  return __fmaf_rn(r, y, q);
+}
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 // server mean (R5): (float)(acc * (1/n) + e~), two fp64 roundings then one to fp32
 __device__ __forceinline__ float mean_plus(double acc, double inv_n, double et) {
   return __double2float_rn(dadd(dmul(acc, inv_n), et));
+}
+
+// ---------------------------------------------------------------- packed fp32 pairs
+// FADD2 (sm_100): two IEEE round-to-nearest fp32 additions per instruction,
+// lane by lane the same results as the scalar ops.  No packed products: ptxas
+// fuses a packed multiply into a following packed add (FFMA2) regardless of
+// -fmad=false.
+__device__ __forceinline__ unsigned long long f2_bits(float2 a) {
+  unsigned long long r;
+  memcpy(&r, &a, 8);
+  return r;
+}
+__device__ __forceinline__ float2 bits_f2(unsigned long long r) {
+  float2 a;
+  memcpy(&a, &r, 8);
+  return a;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+  return bits_f2(r);
+}
+__device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+  return bits_f2(r);
+}
+#define BPC_F4_OP(NAME, OP2)                                                              \
+  __device__ __forceinline__ float4 NAME(float4 a, float4 b) {                            \
+    const float2 lo = OP2(make_float2(a.x, a.y), make_float2(b.x, b.y));                 \
+    const float2 hi = OP2(make_float2(a.z, a.w), make_float2(b.z, b.w));                 \
+    return make_float4(lo.x, lo.y, hi.x, hi.y);                                           \
+  }
+BPC_F4_OP(fadd4, fadd2)
+BPC_F4_OP(fsub4, fsub2)
+#undef BPC_F4_OP
+__device__ __forceinline__ float4 splat4(float a) { return make_float4(a, a, a, a); }
+
+// Alg. 5 lines 12-16 and x <- x - eta (r + lambda x) on 4 elements (R15, R16, R21):
+// products per element, the sums of two products as packed pairs, divisions and
+// roots per element -- the same IEEE operations in the same order as the scalar
+// form.  (Packed products feeding packed sums are NOT used: ptxas 12.9 contracts
+// mul.rn.f32x2 + add.rn.f32x2 into FFMA2 even under -fmad=false, a single
+// rounding the oracle does not make; scalar FMUL results are left alone.)
+__device__ __forceinline__ float4 fmul4s(float4 a, float4 b) {   // scalar products
+  return make_float4(fmul(a.x, b.x), fmul(a.y, b.y), fmul(a.z, b.z), fmul(a.w, b.w));
+}
+__device__ __forceinline__ void adam4(float4 g, float4& m, float4& v, float4& x, const UpdateParams& p) {
+  m = fadd4(fmul4s(splat4(p.beta1), m), fmul4s(splat4(p.omb1), g));                 // line 12
+  v = fadd4(fmul4s(splat4(p.beta2), v), fmul4s(splat4(p.omb2), fmul4s(g, g)));      // line 13
+  float4 r;
+#pragma unroll
+  for (int u = 0; u < 4; u++) {
+    const float mh = divc(u == 0 ? m.x : u == 1 ? m.y : u == 2 ? m.z : m.w, p.bc1, p.ibc1);   // line 14
+    const float vh = divc(u == 0 ? v.x : u == 1 ? v.y : u == 2 ? v.z : v.w, p.bc2, p.ibc2);   // line 15
+    const float ru = fdiv_pos(mh, fadd(fsqrt0(vh), p.eps));                                   // line 16
+    if (u == 0) r.x = ru; else if (u == 1) r.y = ru; else if (u == 2) r.z = ru; else r.w = ru;
+  }
+  x = fsub4(x, fmul4s(splat4(p.lr), fadd4(r, fmul4s(splat4(p.wd), x))));          // x update
 }
 
 // ---------------------------------------------------------------- pairwise tree (R6)

@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cmath>
+
 namespace bpc {
 
 constexpr int P2P_MAXJ = 64;   // max world size of the peer-memory exchange
@@ -44,30 +46,6 @@ struct Tile {
   uint32_t pad;
 };
 
-struct CompressParams {
-  const float* grad;      // worker: g (flat)
-  float* err;             // worker: e (flat)
-  uint8_t* out;           // worker: SEND; server: P
-  const uint8_t* recv;    // server: RECV (n slots)
-  uint64_t slot_bytes;    // server: bytes per RECV slot
-  float* etl;             // server: e~ (compact)
-  const DevChunk* chunks;
-  const uint32_t* items;  // compressed chunk indices handled by this launch
-  uint32_t n_items;
-  const Tile* raw_tiles;  // raw tiles handled by this launch
-  uint32_t n_raw_tiles;
-  uint32_t cs;            // CTAs per cluster
-  uint32_t n;             // world size
-  double inv_n;           // 1.0 / n
-  uint32_t t, rank, stage;
-  uint64_t seed;
-  uint32_t bits;
-  int32_t randk_scaled, use_ef;
-  int32_t f16;            // sparse kinds: binary16 values (R23)
-  int32_t check_finite;
-  unsigned int* flag;     // non-finite flag
-};
-
 struct UpdateParams {
   const uint8_t* pbuf;
   const DevChunk* chunks;
@@ -77,6 +55,7 @@ struct UpdateParams {
   float* v;
   float* x;
   float beta1, beta2, omb1, omb2, bc1, bc2, eps, lr, wd;   // bc = fl32(1 - beta^t), R16
+  float ibc1, ibc2;       // RN(1 / bc): the divisions by bc run as Markstein's correction (divc)
   uint32_t bits;
   int32_t mode;           // 0 Adam core; LANS (R22): 1 = pass 1 (m, v, block sums), 2 = pass 2 (x);
                           // 3 NAG (R24, velocity in m)
@@ -138,6 +117,42 @@ struct StreamParams {
   PeerSync sync;
 };
 
+// sparse kinds (kernels_sparse.cu): guess -> stream -> select, per side
+struct SparseParams {
+  const float* grad;        // worker: g (flat)
+  float* vals;              // worker: e (flat; use_ef); server: e~ (use_ef) or the Delta scratch
+                            // (compact, DevChunk.etl)
+  uint8_t* out;             // worker: SEND; server: P
+  const uint8_t* recv;      // server: RECV (n slots)
+  uint64_t slot_bytes;
+  const DevChunk* chunks;
+  const uint32_t* items;    // this side's compressed units (chunk indices)
+  uint32_t n_units;
+  const Slice* slices;      // this side's 2^13-element slices (compressed and raw units)
+  uint32_t n_slices;
+  const uint32_t* chunk2u;  // chunk -> unit index of this side
+  uint32_t* guess;          // [n_units] candidate thresholds
+  uint32_t* cnt;            // [n_units] candidate counters (the select kernel resets them)
+  uint32_t* cand;           // candidate indices, unit u at [cand_off[u], cand_off[u + 1])
+  const uint32_t* cand_off; // [n_units + 1]
+  uint32_t n;
+  double inv_n;
+  uint32_t t, stage, rrank;  // Philox counter words (R13): stage 0 push (rank), 1 pull (0)
+  uint64_t seed;
+  int32_t server, randk_scaled, use_ef, f16, check_finite;
+  unsigned int* flag;
+  uint32_t sel_cap;         // CTA select kernel: candidates held in shared memory, a power of two <= SEL_CAP
+  uint32_t* big;            // [n_units] units the warp select hands to the CTA select (it resets them)
+};
+constexpr uint32_t SEL_CAP = 16384;     // max candidates a select CTA holds in shared memory
+// the sample rank of the top-k guess (host: capacity; device: the guess)
+__host__ __device__ inline uint32_t sparse_sample_rank(uint32_t k, uint32_t L) {
+  const double mu = (double)k * 4096.0 / (double)L;
+  return (uint32_t)ceil(mu + 3.0 * sqrt(mu) + 6.0);
+}
+cudaError_t launch_sparse(int kind, const SparseParams& p, int grid, cudaStream_t s);
+size_t sparse_select_smem(uint32_t sel_cap);
+
 // peer-memory exchange (kernels_p2p.cu)
 struct P2PParams {
   const uint8_t* src[P2P_MAXJ];
@@ -189,9 +204,6 @@ cudaError_t launch_server_stream(int kind, const StreamParams& p, int grid, cuda
 cudaError_t launch_update_stream(int kind, const UpdateParams& p, int grid, cudaStream_t s);
 size_t cstream_smem();
 size_t update_stream_smem();
-cudaError_t launch_compress(int kind, bool server, const CompressParams& p, cudaStream_t s);
 cudaError_t launch_update(int kind, const UpdateParams& p, cudaStream_t s);
-size_t compress_smem_bytes();
-cudaError_t compress_max_active_clusters(int kind, bool server, uint32_t cs, int* out);
 
 }  // namespace bpc

@@ -11,23 +11,40 @@
 // two rings sized at launch:
 //   HELD ring  (NH x 32 KB)  q (worker: g lands here by TMA, q = g + e in place)
 //                            or Delta (server), kept until the slice is emitted;
-//   INPUT ring (NI x SI)     e (worker) or e~ and the n ranks' payload bytes
-//                            (server), released as soon as the slice is produced.
+//                            the emit overwrites it with the error e / e~ (or it
+//                            holds a raw unit's values), which the producer
+//                            writes back with one bulk store (TMA, full sectors);
+//   INPUT ring (NI x SI)     e (worker) or the n ranks' payload bytes (server),
+//                            released as soon as the slice is produced.
 // Warps:
-//   PRODUCER   reads the slice descriptors and issues the 1-D bulk copies
-//              (cp.async.bulk -> UBLKCP, one mbarrier complete_tx per slice);
+//   PRODUCER   reads the slice descriptors, issues the 1-D bulk loads
+//              (cp.async.bulk -> UBLKCP, one mbarrier complete_tx per slice) and
+//              the bulk stores of emitted slices (cp.async.bulk.global.shared);
 //   4 REDUCERS (slice i -> reducer i % 4) complete each unit's fp64 pairwise-tree
 //              total (R6): a multi-slice unit publishes one partial per
 //              slice (release add on a per-unit counter) and each slice's reducer
 //              waits (relaxed spin + one acquire) for the unit, then reduces it;
 //   16 CONSUMERS produce slice i (q or Delta, slice partial) and then emit slice
-//              i - D (codes + error) once its total is ready, D = NH - 2 <= 3, so
-//              the cross-CTA wait overlaps the produce of D later slices.
+//              i - D (sign bits / codes + error) once its total is ready,
+//              D = NH - 2 <= 3, so the cross-CTA wait overlaps useful work.
+//
+// Consumer layout (round 2): warp w owns elements [512 w, 512 w + 512) of a
+// slice and lane l the 16 contiguous elements [512 w + 16 l, + 16), i.e. float4
+// groups 4 l' .. 4 l' + 3 (l' = 32 w + l).  So a lane's 16 elements are one
+// subtree of R6's pairwise tree (15 fp64 adds in registers, then a 5-level
+// butterfly for the warp's 512), its 16 sign bits are one half-word of the
+// payload and its 16 codes one 16 b-bit field: no cross-lane packing loops.
+// The lane visits its groups in the rotated order k = (s + (l >> 1)) & 3,
+// s = 0..3: eight consecutive lanes then touch eight distinct 16-byte bank
+// groups, so the 16-byte shared-memory accesses are conflict-free although the
+// lanes are 64 bytes apart (a plain order would be 4-way conflicted).
 // All CTAs are co-resident (cooperative launch) and every slice's partial is
 // published before its CTA waits on an earlier unit, so the waits cannot
 // deadlock.  Each mbarrier has a single in-order waiter group; the reducers,
 // run out of order (slice i -> reducer i % 4) but each waits on its slice's
 // held-stage barrier, which cannot run a phase ahead of it.
+#include <type_traits>
+
 #include "device.cuh"
 
 namespace bpc {
@@ -44,10 +61,9 @@ constexpr int CMAXH = 8;                 // max held stages
 constexpr int CNI = 2;                   // input stages
 constexpr int CMAXD = 3;                 // max emit deferral
 constexpr int CSL = 8192;                // elements per slice
-constexpr int CK = CSL / 4 / CCNT;       // float4 per consumer thread per slice
-constexpr int CNRED = CK * CCW;          // 128-element warp subtrees per slice (64)
+constexpr int CLE = 16;                  // elements per consumer lane per slice
 constexpr int CUNITSL = (1 << 18) / CSL; // max slices per unit (32)
-static_assert(CNRED == 32 || CNRED == 64, "slice tree expects 32 or 64 warp subtrees");
+static_assert(CSL == CCNT * CLE, "one slice = 16 elements per consumer lane");
 
 template <bool B>
 struct BoolC {
@@ -69,8 +85,9 @@ struct CDesc {
 struct __align__(128) CHead {
   uint64_t fullI[CNI], emptyI[CNI], emptyH[CMAXH], tready[CMAXH];
   uint64_t pready[CMAXH];   // slice in held stage s produced (its reducer waits on it)
+  uint64_t pfin;            // fused exchange: the producer's last bulk store has completed
   CDesc desc[CMAXH];
-  double red[2][CNRED];
+  double red[2][CCW];       // the consumer warps' 512-element subtrees of a slice
   double part[CMAXH];
   double total[CMAXH];
 };
@@ -80,6 +97,87 @@ __device__ __forceinline__ void mbar_arrive1(uint64_t* bar) {
 }
 __device__ __forceinline__ void cons_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(CCNT) : "memory");
+}
+// bulk shared -> global copy (UBLKCP), tracked by the issuing thread's bulk groups
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+               "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_all() {   // sources of every committed store read
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {        // every committed store complete
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// 128-bit field helpers (a lane's 16 b-bit codes, b <= 8)
+struct U128 {
+  uint64_t lo, hi;
+};
+__device__ __forceinline__ uint32_t u128_get(const U128& a, uint32_t s) {   // bits [s, s + 32)
+  uint64_t v;
+  if (s == 0) v = a.lo;
+  else if (s < 64) v = (a.lo >> s) | (a.hi << (64 - s));
+  else v = a.hi >> (s - 64);
+  return (uint32_t)v;
+}
+__device__ __forceinline__ void u128_or(U128& a, uint32_t x, uint32_t s) {   // a |= x << s (s < 128)
+  const uint64_t v = x;
+  if (s < 64) {
+    a.lo |= v << s;
+    if (s > 32) a.hi |= v >> (64 - s);
+  } else {
+    a.hi |= v << (s - 64);
+  }
+}
+__device__ __forceinline__ U128 u128_shr(const U128& a, uint32_t s) {   // s < 64
+  if (s == 0) return a;
+  return U128{(a.lo >> s) | (a.hi << (64 - s)), a.hi >> s};
+}
+// shifts by a warp-uniform amount s < 128 (uniform branches only)
+__device__ __forceinline__ U128 u128_shl_u(const U128& a, uint32_t s) {
+  if (s == 0) return a;
+  if (s < 64) return U128{a.lo << s, (a.hi << s) | (a.lo >> (64 - s))};
+  return U128{0, a.lo << (s - 64)};
+}
+__device__ __forceinline__ U128 u128_shr_u(const U128& a, uint32_t s) {
+  if (s == 0) return a;
+  if (s < 64) return U128{(a.lo >> s) | (a.hi << (64 - s)), a.hi >> s};
+  return U128{a.hi >> (s - 64), 0};
+}
+// rotate a w-bit field (w <= 128, bits above w zero) left by a uniform r < w
+__device__ __forceinline__ U128 u128_rotl_u(const U128& a, uint32_t r, uint32_t w) {
+  const U128 x = u128_shl_u(a, r), y = u128_shr_u(a, w - r);
+  U128 m = u128_shl_u(U128{~0ull, ~0ull}, 128 - w);
+  m = u128_shr_u(m, 128 - w);   // low w bits
+  return U128{(x.lo | y.lo) & m.lo, (x.hi | y.hi) & m.hi};
+}
+// a |= x << s for a warp-uniform s < 128 (x < 2^32)
+__device__ __forceinline__ U128 u128_or_u(const U128& a, uint32_t x, uint32_t s) {
+  const U128 v = u128_shl_u(U128{x, 0}, s);
+  return U128{a.lo | v.lo, a.hi | v.hi};
+}
+__device__ __forceinline__ U128 u128_sel(bool c, const U128& a, const U128& b) {
+  return U128{c ? a.lo : b.lo, c ? a.hi : b.hi};
+}
+// the lane's 16 codes in element order (group k at bit 4 b k) from the per-step
+// group fields f0 (bits 4 b s for step s, group k = (s + rot) & 3): rotate left by
+// 4 b rot = 4 b (rot & 1) + 8 b (rot & 2) / 2 with uniform amounts and per-lane selects
+__device__ __forceinline__ U128 unrotate_field(const U128& f0, uint32_t rot, uint32_t gb) {
+  const uint32_t w = 4 * gb;
+  U128 f = u128_sel(rot & 1u, u128_rotl_u(f0, gb, w), f0);
+  return u128_sel(rot & 2u, u128_rotl_u(f, 2 * gb, w), f);
+}
+// the inverse: step s's group at bit 4 b s (f's bits at and above 4 gb, the next
+// lane's codes of a loaded field, are dropped first)
+__device__ __forceinline__ U128 rotate_field(const U128& fin, uint32_t rot, uint32_t gb) {
+  const uint32_t w = 4 * gb;
+  const U128 m = u128_shr_u(U128{~0ull, ~0ull}, 128 - w);
+  const U128 f{fin.lo & m.lo, fin.hi & m.hi};
+  U128 g = u128_sel(rot & 1u, u128_rotl_u(f, w - gb, w), f);
+  return u128_sel(rot & 2u, u128_rotl_u(g, w - 2 * gb, w), g);
 }
 
 // inv = fl32(s / N), or 0 when N = 0: then every q of the unit is +-0, r = 0 and
@@ -97,16 +195,16 @@ __device__ __forceinline__ uint32_t nat_code_c(float q, float N, int cmax, float
   const uint32_t sign = !(q < 0.f);
   uint32_t code = 0;
   if (N != 0.f) {
-    const float r = fminf(fdiv(fabsf(q), N), 1.0f);
+    const float r = fminf(fdiv_pos(fabsf(q), N), 1.0f);
     const float u = (float)(w >> 8) * 0x1p-24f;
     if (r >= lmin) {
       const int eb = (int)(__float_as_uint(r) >> 23);
       const float lo = __uint_as_float((uint32_t)eb << 23);
-      const float pup = fsub(fdiv(r, lo), 1.0f);
+      const float pup = fsub(fdiv_pos(r, lo), 1.0f);
       const int e_lev = (u < pup) ? eb - 127 + 1 : eb - 127;
       code = (uint32_t)(cmax + e_lev);
     } else {
-      code = (u < fdiv(r, lmin)) ? 1u : 0u;
+      code = (u < fdiv_pos(r, lmin)) ? 1u : 0u;
     }
   }
   return sign | (code << 1);
@@ -123,18 +221,21 @@ __device__ __forceinline__ float dither_mag(uint32_t code, float hdr, float unit
 // the owners' RECV slots over NVLink and releases the push flags; the server
 // waits for every rank's push before its first load and releases the pull
 // flags after its last store (the update kernels read p from the owners' P).
-template <int KIND, bool SERVER, bool FUSED>
+// BITS: dithering bits as a compile-time constant (the paper's 3 / 5 / 7-bit runs,
+// every shift of the code packing is then an immediate), or 0 =
+// p.bits at run time
+template <int KIND, bool SERVER, bool FUSED, int BITS>
 __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant__ StreamParams p) {
   extern __shared__ __align__(128) unsigned char sraw[];
   CHead& hd = *reinterpret_cast<CHead*>(sraw);
   const uint32_t NH = p.nstages;          // held stages
   const uint32_t D = NH - 2 < (uint32_t)CMAXD ? NH - 2 : (uint32_t)CMAXD;   // emit deferral
   const uint32_t SI = p.stage_b;          // bytes per input stage
-  const uint32_t SIE = p.stage_a;         // byte offset of the e / e~ region inside an input stage
+  const uint32_t SIE = p.stage_a;         // byte offset of the e region inside an input stage
   unsigned char* held = sraw + sizeof(CHead);
   unsigned char* input = held + (size_t)NH * CSL * 4;
   auto H = [&](uint32_t s) { return reinterpret_cast<float4*>(held + (size_t)s * CSL * 4); };
-  // server input stage: [n x 16-byte payload heads][n payload pieces][e~]
+  // server input stage: [n x 16-byte payload heads][n payload pieces]
   const uint32_t HB = SERVER ? (16 * p.n + 127) / 128 * 128 : 0;
   auto IH = [&](uint32_t t) { return input + (size_t)t * SI; };               // payload heads
   auto I = [&](uint32_t t) { return input + (size_t)t * SI + HB; };          // payload pieces
@@ -142,7 +243,7 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
   const uint32_t G = gridDim.x;
   const uint32_t mine = p.n_slices > blockIdx.x ? (p.n_slices - blockIdx.x + G - 1) / G : 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int b = KIND == C_SIGN ? 1 : (int)p.bits;       // bits per element in the payload stream
+  const int b = KIND == C_SIGN ? 1 : (BITS ? BITS : (int)p.bits);   // bits per element in the payload stream
   if (threadIdx.x == 0) {
     for (uint32_t s = 0; s < NH; s++) {
       mbar_init(&hd.emptyH[s], CCW);
@@ -153,6 +254,7 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
       mbar_init(&hd.fullI[t], 1);
       mbar_init(&hd.emptyI[t], CCW);
     }
+    mbar_init(&hd.pfin, 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -162,6 +264,24 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
   if (warp == CPROD) {
     if (lane == 0) {
       if (SERVER && FUSED) peer_wait(p.sync);   // fused exchange: every rank's delta has landed in RECV
+      // write-back of emitted slice ie (its held stage): the error e / e~, or a raw
+      // unit's payload (worker: g; server: the mean), 16-byte-aligned part
+      auto flush = [&](uint32_t ie) {
+        const uint32_t hs = ie % NH;
+        mbar_wait_backoff(&hd.emptyH[hs], (ie / NH) & 1, 128, 0x1000000u | ie);   // consumers emitted slice ie
+        if (p.pass == 1) return;
+        const CDesc& o = hd.desc[hs];
+        const uint32_t nvb = (o.len & ~3u) * 4u;
+        if (!nvb) return;
+        uint8_t* dst = nullptr;
+        if (o.nslices == 0) {
+          uint8_t* pay = (!SERVER && FUSED) ? p.dst[o.owner] + o.recv : p.out + o.pay;
+          dst = pay + 4ull * o.start;
+        } else if (p.use_ef) {
+          dst = reinterpret_cast<uint8_t*>(p.err + (SERVER ? o.etl : o.off) + o.start);
+        }
+        if (dst) bulk_store(dst, H(hs), nvb);
+      };
       // descriptors of the next slice are loaded before the stage waits, so their
       // latency overlaps the wait instead of delaying the bulk copies
       Slice sl_next = mine ? p.slices[blockIdx.x] : Slice{};
@@ -174,8 +294,10 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
           sl_next = p.slices[blockIdx.x + (i + 1) * G];
           c_next = p.chunks[sl_next.chunk];
         }
-        if (i >= NH) mbar_wait(&hd.emptyH[hs], ((i / NH) - 1) & 1, 0x1000000u | i);
-        if (i >= (uint32_t)CNI) mbar_wait(&hd.emptyI[t], ((i / CNI) - 1) & 1, 0x1100000u | i);
+        // stage hs held slice i - NH, flushed one iteration ago: its store must
+        // have read the stage before new bytes land there
+        if (i >= NH) bulk_wait_read_all();
+        if (i >= (uint32_t)CNI) mbar_wait_backoff(&hd.emptyI[t], ((i / CNI) - 1) & 1, 128, 0x1100000u | i);
         CDesc d;
         d.off = c.off;
         d.pay = c.pay;
@@ -229,6 +351,15 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
               tma_load_1d(I(t) + r * p.piece_stride, p.recv + r * p.slot_bytes + c.recv + a0,
                           (uint32_t)(a1 - a0), &hd.fullI[t]);
         }
+        // flush the slice whose stage the next iteration reuses (store issued now,
+        // its smem read waited for only then)
+        if (i + 1 >= NH && i + 1 < mine) flush(i + 1 - NH);
+      }
+      for (uint32_t ie = mine > NH ? mine - NH : 0; ie < mine; ie++) flush(ie);
+      bulk_wait_all();
+      if (FUSED && p.pass != 1) {   // raw payloads stored into peers' RECV: visible before the signal
+        __threadfence_system();
+        mbar_arrive1(&hd.pfin);
       }
     }
     return;
@@ -240,7 +371,9 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
       const uint32_t hs = i % NH;
       // slice i produced.  Cannot alias: slice i + NH needs stage hs back, which
       // needs this reducer's tready arrive for slice i first.
-      mbar_wait_backoff(&hd.pready[hs], (i / NH) & 1, 200, 0x2000000u | i);
+      // the emit of slice i runs D slices later: a 1 us poll costs it nothing and
+      // keeps the waiting warps off the issue slots the consumers need
+      mbar_wait_backoff(&hd.pready[hs], (i / NH) & 1, 1000, 0x2000000u | i);
       const uint32_t ns = hd.desc[hs].nslices;
       if (ns > 1 && p.pass == 1) {   // per-tensor units, pass 1: publish the partial only
         if (lane == 0) p.partials[hd.desc[hs].unit_first + hd.desc[hs].sidx] = hd.part[hs];
@@ -276,14 +409,30 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
   }
 
   // ===================================================== consumers
-  const int nb = 4 * b;
-  const float slv = (float)((1u << (p.bits - 1)) - 1u);
-  const int cmax = (1 << (p.bits - 1)) - 1;
+  const float slv = (float)((1u << (b - 1)) - 1u);
+  const int cmax = (1 << (b - 1)) - 1;
   const float lmin = __uint_as_float((uint32_t)(127 - (cmax - 1)) << 23);
   const uint32_t cmask = (1u << b) - 1u;
+  const uint32_t gbits = 4u * (uint32_t)b;                  // bits of one float4 group's codes
+  const uint32_t gmask = gbits == 32 ? 0xFFFFFFFFu : (1u << gbits) - 1u;
   const uint32_t stage_id = SERVER ? 1u : 0u;
   const uint32_t rng_rank = SERVER ? 0u : p.rank;
+  const uint32_t rot = ((uint32_t)lane >> 1) & 3u;         // conflict-free group order (header)
+  const uint32_t lf = 128u * warp + 4u * lane;              // the lane's first float4 in a slice
+  const uint32_t lq = 32u * warp + lane;                    // lane index within the slice
+  const uint32_t lbit = 16u * (uint32_t)b * lq;             // first bit of the lane's field in the slice stream
   bool bad = false;
+
+  // the lane's 16 b-bit field of a payload stream whose slice starts at `words`
+  // (32-bit aligned); words at index >= sw are not read (they are not payload)
+  auto load_lane_field = [&](const uint32_t* words, uint32_t sw) -> U128 {
+    const uint32_t w0 = lbit >> 5;
+    uint32_t wv[4];
+#pragma unroll
+    for (int c = 0; c < 4; c++) wv[c] = (w0 + c < sw) ? words[w0 + c] : 0u;
+    U128 a{(uint64_t)wv[0] | ((uint64_t)wv[1] << 32), (uint64_t)wv[2] | ((uint64_t)wv[3] << 32)};
+    return u128_shr(a, lbit & 31u);
+  };
 
   // A slice is FULL when it holds CSL elements of its unit: no bounds checks, no
   // tail loads (the ragged-tail code runs only for a unit's last slice).
@@ -291,27 +440,52 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
   auto produce = [&](auto full_tag, uint32_t i, uint32_t t, const CDesc& d, float4* val, bool comp) {
     constexpr bool FULL = decltype(full_tag)::value;
     const uint32_t nvec = d.len >> 2;
+    const uint32_t sw = (uint32_t)(((uint64_t)d.len * b + 31) / 32);   // payload words of the slice
+    const bool lane_any = FULL || 16u * lq < d.len;
+    double lv[4];
+    // server, n = 1: rank 0's field of the lane (sign: one half-word), read once
+    U128 fld{0, 0};
+    float h0 = 0.f;
+    if (SERVER && comp && p.n == 1 && lane_any) {
+      h0 = *reinterpret_cast<const float*>(IH(t));
+      const uint32_t* words = d.staged ? reinterpret_cast<const uint32_t*>(I(t) + d.pofs)
+                                       : reinterpret_cast<const uint32_t*>(p.recv + d.recv + 4 +
+                                                                           (uint64_t)d.start * b / 8);
+      if (KIND == C_SIGN) fld.lo = reinterpret_cast<const uint16_t*>(words)[lq];
+      else fld = rotate_field(load_lane_field(words, sw), rot, gbits);   // step s's group at bit 4 b s
+    }
+    const float unit0 = KIND == C_SIGN ? 0.f : fdiv(h0, slv);
 #pragma unroll
-    for (int k = 0; k < CK; k++) {
-      const uint32_t f = threadIdx.x + k * CCNT;
+    for (int s = 0; s < 4; s++) {
+      const uint32_t k = (s + rot) & 3u;
+      const uint32_t f = lf + k;
       const uint32_t j = d.start + 4 * f;
       const bool inv4 = FULL || f < nvec;   // a whole float4 inside the 16-byte bulk copies
+      const bool any = FULL || 4 * f < d.len;
       float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+      bool wr = false;
       if (!SERVER) {
         const bool ef = p.use_ef && comp;
         float4 g4 = q, e4 = q;
         if (inv4) {
           g4 = val[f];
           if (ef) e4 = IE(t)[f];
-        } else if (4 * f < d.len) {   // ragged tail (not in the 16-byte bulk copy)
+        } else if (any) {   // ragged tail (not in the 16-byte bulk copy)
           g4 = load4_masked(p.grad + d.off, j, d.L);
           if (ef) e4 = load4_masked(p.err + d.off, j, d.L);
+          wr = true;
         }
         if (p.check_finite) bad |= !(isfinite(g4.x) && isfinite(g4.y) && isfinite(g4.z) && isfinite(g4.w));
-        q = ef ? make_float4(fadd(g4.x, e4.x), fadd(g4.y, e4.y), fadd(g4.z, e4.z), fadd(g4.w, e4.w)) : g4;
-      } else if (FULL || 4 * f < d.len) {
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        if (ef) {
+          q = fadd4(g4, e4);
+          wr = any;
+        } else {
+          q = g4;
+        }
+      } else if (any) {
+        wr = true;
         if (!comp) {   // raw unit: mean of the ranks' fp32 values (rank 0's staged in val)
+          double acc[4] = {0.0, 0.0, 0.0, 0.0};
           for (uint32_t r = 0; r < p.n; r++) {
             const float4 x4 = (r == 0 && inv4)
                                   ? val[f]
@@ -321,164 +495,193 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
             acc[2] += (double)x4.z;
             acc[3] += (double)x4.w;
           }
+          if (FULL || j < d.L) q.x = mean_plus(acc[0], p.inv_n, 0.0);
+          if (FULL || j + 1 < d.L) q.y = mean_plus(acc[1], p.inv_n, 0.0);
+          if (FULL || j + 2 < d.L) q.z = mean_plus(acc[2], p.inv_n, 0.0);
+          if (FULL || j + 3 < d.L) q.w = mean_plus(acc[3], p.inv_n, 0.0);
         } else if (p.n == 1) {
           // n = 1: Delta = fl32(fl64(dec * 1.0) + fl64(e~)) equals the fp32 sum
           // fl32(dec + e~): the fp64 sum of two fp32 values is exact unless their
           // exponents differ by more than 29, and then both roundings return the
           // larger operand.  One fp32 add instead of four conversions.
-          const float h = *reinterpret_cast<const float*>(IH(t));
-          // staged words are read with shared-memory loads (no generic pointer merge)
-          uint32_t field;
-          if (d.staged) {
-            const uint32_t* words = reinterpret_cast<const uint32_t*>(I(t) + d.pofs);
-            field = KIND == C_SIGN ? ((words[f >> 3] >> ((f & 7) * 4)) & 15u)
-                                   : load_field(words, (uint64_t)b * 4 * f, nb);
-          } else {
-            const uint32_t* words =
-                reinterpret_cast<const uint32_t*>(p.recv + d.recv + 4 + (uint64_t)d.start * b / 8);
-            field = KIND == C_SIGN ? ((words[f >> 3] >> ((f & 7) * 4)) & 15u)
-                                   : load_field(words, (uint64_t)b * 4 * f, nb);
-          }
-          const float unit = KIND == C_SIGN ? 0.f : fdiv(h, slv);
-          // sign: h >= +0, and for h = 0 both decodes are +0 (the fp64 sum of the
-          // oracle starts at +0, so -0 never survives): one add per element
-          const float hneg = h == 0.f ? 0.f : -h;
           float4 e4 = make_float4(0.f, 0.f, 0.f, 0.f);
           if (p.use_ef) e4 = inv4 ? val[f] : load4_masked(p.err + d.etl, j, d.L);
+          float4 dec;
+          if (KIND == C_SIGN) {
+            // sign: h >= +0, and for h = 0 both decodes are +0 (the fp64 sum of the
+            // oracle starts at +0, so -0 never survives): one add per element
+            const float hneg = h0 == 0.f ? 0.f : -h0;
+            const uint32_t nib = (uint32_t)(fld.lo >> (4 * k)) & 15u;
+            dec = make_float4(nib & 1u ? h0 : hneg, nib & 2u ? h0 : hneg, nib & 4u ? h0 : hneg,
+                              nib & 8u ? h0 : hneg);
+          } else {
+            const uint32_t x = u128_get(fld, gbits * s) & gmask;
 #pragma unroll
-          for (int u = 0; u < 4; u++) {
-            float dsum;
-            if (KIND == C_SIGN) {
-              dsum = fadd(((field >> u) & 1u) ? h : hneg, get(e4, u));
-            } else {
-              const uint32_t code = (field >> (b * u)) & cmask;
-              const float mag = dither_mag<KIND>(code, h, unit, cmax);
-              // acc = +0.0 + dec (turns -0 into +0, as the fp64 sum does), then + e~
-              dsum = fadd(fadd(0.f, (code & 1u) ? mag : -mag), get(e4, u));
+            for (int u = 0; u < 4; u++) {
+              const uint32_t code = (x >> (b * u)) & cmask;
+              const float mag = dither_mag<KIND>(code, h0, unit0, cmax);
+              set(dec, u, (code & 1u) ? mag : -mag);
             }
-            if (FULL || j + u < d.L) set(q, u, dsum);
+            // acc = +0.0 + dec (turns -0 into +0, as the fp64 sum does), then + e~
+            dec = fadd4(make_float4(0.f, 0.f, 0.f, 0.f), dec);
           }
+          const float4 dsum = fadd4(dec, e4);
+          q = FULL ? dsum : make_float4(j < d.L ? dsum.x : 0.f, j + 1 < d.L ? dsum.y : 0.f,
+                                        j + 2 < d.L ? dsum.z : 0.f, j + 3 < d.L ? dsum.w : 0.f);
         } else {
+          double acc[4] = {0.0, 0.0, 0.0, 0.0};
           for (uint32_t r = 0; r < p.n; r++) {
             const float h = *reinterpret_cast<const float*>(IH(t) + 16 * r);
             const uint32_t* words =
                 d.staged ? reinterpret_cast<const uint32_t*>(I(t) + r * p.piece_stride + d.pofs)
                          : reinterpret_cast<const uint32_t*>(p.recv + r * p.slot_bytes + d.recv + 4 +
                                                              (uint64_t)d.start * b / 8);
-            const uint32_t field = KIND == C_SIGN ? ((words[f >> 3] >> ((f & 7) * 4)) & 15u)
-                                                  : load_field(words, (uint64_t)b * 4 * f, nb);
+            // this group's 4 codes: bits [lbit + 4 b k, + 4 b) of the slice stream
+            const uint32_t pos = lbit + gbits * k;
+            const uint32_t w0 = pos >> 5;
+            const uint32_t lo = words[w0];
+            const uint32_t hi = (w0 + 1 < sw) ? words[w0 + 1] : 0u;
+            const uint32_t x = (uint32_t)((((uint64_t)hi << 32) | lo) >> (pos & 31)) & gmask;
             const float unit = KIND == C_SIGN ? 0.f : fdiv(h, slv);
             const double hd64 = (double)h;   // sign: one conversion per rank, not per element
 #pragma unroll
             for (int u = 0; u < 4; u++) {
               double dec;
               if (KIND == C_SIGN) {
-                dec = ((field >> u) & 1u) ? hd64 : -hd64;
+                dec = ((x >> u) & 1u) ? hd64 : -hd64;
               } else {
-                const uint32_t code = (field >> (b * u)) & cmask;
+                const uint32_t code = (x >> (b * u)) & cmask;
                 const float mag = dither_mag<KIND>(code, h, unit, cmax);
                 dec = (double)((code & 1u) ? mag : -mag);
               }
               if (FULL || j + u < d.L) acc[u] += dec;
             }
           }
-        }
-        if (!comp || p.n != 1) {
           float4 e4 = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (comp && p.use_ef) e4 = inv4 ? val[f] : load4_masked(p.err + d.etl, j, d.L);
+          if (p.use_ef) e4 = inv4 ? val[f] : load4_masked(p.err + d.etl, j, d.L);
           if (FULL || j < d.L) q.x = mean_plus(acc[0], p.inv_n, (double)e4.x);
           if (FULL || j + 1 < d.L) q.y = mean_plus(acc[1], p.inv_n, (double)e4.y);
           if (FULL || j + 2 < d.L) q.z = mean_plus(acc[2], p.inv_n, (double)e4.z);
           if (FULL || j + 3 < d.L) q.w = mean_plus(acc[3], p.inv_n, (double)e4.w);
         }
       }
-      val[f] = q;
-      if (comp) {
-        const double a = warp_tree(KIND == C_SIGN ? leaf4_abs(q) : leaf4_sq(q));
-        if (lane == 0) hd.red[i & 1][k * CCW + warp] = a;   // subtree of slice elements [128 m, 128 m + 128)
-      }
+      if (wr) val[f] = q;
+      lv[s] = comp ? (KIND == C_SIGN ? leaf4_abs(q) : leaf4_sq(q)) : 0.0;
+    }
+    if (comp) {
+      // the lane's 16-element subtree: groups (0, 1) and (2, 3) pair up; in step
+      // order that is (s0, s1), (s2, s3) for an even rotation and (s3, s0),
+      // (s1, s2) for an odd one (IEEE + is commutative)
+      const bool odd = rot & 1u;
+      const double x1 = odd ? lv[3] : lv[1], y1 = odd ? lv[1] : lv[3];
+      const double a = warp_tree((lv[0] + x1) + (lv[2] + y1));   // the warp's 512 elements
+      if (lane == 0) hd.red[i & 1][warp] = a;
     }
   };
 
-  // ---------------- emit: payload (sign bits / codes / raw fp32) + error of a slice
-  auto emit = [&](auto full_tag, const CDesc& d, const float4* val, uint8_t* pay, double total) {
+  // ---------------- emit: payload (sign bits / codes) + error of a slice (into the
+  // held stage; the producer bulk-stores it), raw units: ragged tail only
+  auto emit = [&](auto full_tag, const CDesc& d, float4* val, uint8_t* pay, double total) {
     constexpr bool FULL = decltype(full_tag)::value;
     const uint32_t L = d.L;
-    if (d.nslices == 0) {   // raw unit: fp32 payload (worker: g, no EF; server: the mean)
+    const uint32_t nvec = d.len >> 2;
+    if (d.nslices == 0) {   // raw unit: the producer bulk-stores [0, nvec); the ragged float4 here
+      if (!FULL && (d.len & 3u)) {
 #pragma unroll
-      for (int k = 0; k < CK; k++) {
-        const uint32_t f = threadIdx.x + k * CCNT;
-        if (FULL) st4(reinterpret_cast<float*>(pay) + d.start + 4 * f, val[f]);
-        else if (4 * f < d.len) store4_masked(reinterpret_cast<float*>(pay), d.start + 4 * f, L, val[f]);
+        for (int s = 0; s < 4; s++) {
+          const uint32_t f = lf + ((s + rot) & 3u);
+          if (f == nvec) store4_masked(reinterpret_cast<float*>(pay), d.start + 4 * f, L, val[f]);
+        }
       }
       return;
     }
     float* errp = p.use_ef ? (SERVER ? p.err + d.etl : p.err + d.off) : nullptr;
     if (KIND == C_SIGN) {
       const float sc = __double2float_rn(total / (double)L);
+      const float nsc = -sc;
+      uint32_t m16 = 0;
 #pragma unroll
-      for (int k = 0; k < CK; k++) {
-        const uint32_t f = threadIdx.x + k * CCNT;
+      for (int s = 0; s < 4; s++) {
+        const uint32_t k = (s + rot) & 3u;
+        const uint32_t f = lf + k;
         const uint32_t j = d.start + 4 * f;
+        if (!(FULL || 4 * f < d.len)) continue;
         const float4 q = val[f];
         uint32_t nib = 0;
-        float4 ev;
+        float4 m;
 #pragma unroll
         for (int u = 0; u < 4; u++) {
-          const float qu = get(q, u);
-          const bool bit = !(qu < 0.f);
+          const bool bit = !(get(q, u) < 0.f);
           if (bit && (FULL || j + u < L)) nib |= 1u << u;
-          set(ev, u, bit ? fsub(qu, sc) : fadd(qu, sc));
+          set(m, u, bit ? nsc : sc);   // e = q - dec: q - s or q + s
         }
         if (errp) {
-          if (FULL) st4(errp + j, ev);
-          else if (j < L) store4_masked(errp, j, L, ev);
+          const float4 ev = fadd4(q, m);
+          val[f] = ev;
+          if (!FULL && f >= nvec) store4_masked(errp, j, L, ev);   // ragged float4 (not bulk-stored)
         }
-        uint32_t w = nib << (4 * (lane & 7));
-        w |= __shfl_xor_sync(0xffffffffu, w, 1);
-        w |= __shfl_xor_sync(0xffffffffu, w, 2);
-        w |= __shfl_xor_sync(0xffffffffu, w, 4);
-        if ((lane & 7) == 0 && (FULL || j < L)) reinterpret_cast<uint32_t*>(pay + 4)[j >> 5] = w;
+        m16 |= nib << (4 * k);
       }
+      // lane pairs (2m, 2m+1) hold the two halves of payload word m of the warp
+      const uint32_t other = __shfl_xor_sync(0xffffffffu, m16, 1);
+      const uint32_t wi = (d.start >> 5) + (lq >> 1);
+      if (!(lane & 1) && (FULL || wi < (L + 31) / 32))
+        reinterpret_cast<uint32_t*>(pay + 4)[wi] = m16 | (other << 16);
       if (d.sidx == 0 && threadIdx.x == 0) *reinterpret_cast<float*>(pay) = sc;
     } else if (KIND == C_LDITHER || KIND == C_NDITHER) {
       const float N = __double2float_rn(sqrt(total));
       const float inv = N != 0.f ? fdiv(slv, N) : 0.f;
       const float unit = fdiv(N, slv);
-      const uint64_t nwords = ((uint64_t)b * L + 31) / 32;
+      U128 fld{0, 0};   // the lane's 16 codes in element order
 #pragma unroll
-      for (int k = 0; k < CK; k++) {
-        const uint32_t f = threadIdx.x + k * CCNT;
+      for (int s = 0; s < 4; s++) {
+        const uint32_t k = (s + rot) & 3u;
+        const uint32_t f = lf + k;
         const uint32_t j = d.start + 4 * f;
+        if (!(FULL || 4 * f < d.len)) continue;
         const float4 q = val[f];
-        uint32_t field = 0;
-        if (FULL || j < L) {
-          const uint4 w4 = philox4x32_10_rk(make_uint4(j >> 2, d.id, p.t, (stage_id << 31) | rng_rank), p.rk);
-          float4 ev;
-          uint32_t codes[4];
+        const uint4 w4 = philox4x32_10_rk(make_uint4(j >> 2, d.id, p.t, (stage_id << 31) | rng_rank), p.rk);
+        uint32_t g = 0, codes[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const uint32_t w = u == 0 ? w4.x : (u == 1 ? w4.y : (u == 2 ? w4.z : w4.w));
+          const float qu = get(q, u);
+          codes[u] = KIND == C_LDITHER ? lin_code_c(qu, slv, inv, w) : nat_code_c(qu, N, cmax, lmin, w);
+          if (FULL || j + u < L) g |= codes[u] << (b * u);   // code < 2^b
+        }
+        fld = u128_or_u(fld, g, gbits * s);
+        if (errp) {   // EF runs only; no error arithmetic otherwise
+          float4 m;
 #pragma unroll
           for (int u = 0; u < 4; u++) {
-            const uint32_t w = u == 0 ? w4.x : (u == 1 ? w4.y : (u == 2 ? w4.z : w4.w));
-            const float qu = get(q, u);
-            const uint32_t code = KIND == C_LDITHER ? lin_code_c(qu, slv, inv, w)
-                                                    : nat_code_c(qu, N, cmax, lmin, w);
-            if (FULL || j + u < L) field |= (code & cmask) << (b * u);
-            codes[u] = code;
+            const float mag = dither_mag<KIND>(codes[u], N, unit, cmax);
+            set(m, u, (codes[u] & 1u) ? -mag : mag);   // e = q - dec
           }
-          if (errp) {   // e = q - dec (EF runs only); no error arithmetic otherwise
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-              const float mag = dither_mag<KIND>(codes[u], N, unit, cmax);
-              set(ev, u, fsub(get(q, u), (codes[u] & 1u) ? mag : -mag));
-            }
-            if (FULL) st4(errp + j, ev);
-            else store4_masked(errp, j, L, ev);
-          }
+          const float4 ev = fadd4(q, m);
+          val[f] = ev;
+          if (!FULL && f >= nvec) store4_masked(errp, j, L, ev);
         }
-        const uint32_t wd = warp_pack(field, nb);
-        const uint64_t wbase = (uint64_t)(d.start + 4 * (k * CCNT + 32 * warp)) / 32 * b;
-        if (lane < nb && (FULL || wbase + lane < nwords)) reinterpret_cast<uint32_t*>(pay + 4)[wbase + lane] = wd;
       }
+      fld = unrotate_field(fld, rot, gbits);
+      // store the lane's 16 b bits at bit lbit of the slice stream.  Odd b: lane
+      // 2m+1 starts at bit 16 of the word lane 2m ends in; it hands its first 16
+      // bits to lane 2m, which stores that shared word
+      uint32_t* out = reinterpret_cast<uint32_t*>(pay + 4) + (uint32_t)((uint64_t)d.start * b / 32);
+      const uint32_t nwu = (uint32_t)(((uint64_t)b * L + 31) / 32 - (uint64_t)d.start * b / 32);   // words left in the unit
+      uint32_t w0 = lbit >> 5, nw = (uint32_t)b / 2;
+      if (b & 1) {
+        const uint32_t nb16 = __shfl_xor_sync(0xffffffffu, (uint32_t)fld.lo & 0xFFFFu, 1);
+        if (lane & 1) {
+          fld = u128_shr(fld, 16);
+          w0 += 1;
+        } else {
+          u128_or(fld, nb16, 16u * b);
+          nw += 1;
+        }
+      }
+#pragma unroll
+      for (uint32_t c = 0; c < 4; c++)
+        if (c < nw && (FULL || w0 + c < nwu)) out[w0 + c] = u128_get(fld, 32 * c);
       if (d.sidx == 0 && threadIdx.x == 0) *reinterpret_cast<float*>(pay) = N;
     }
   };
@@ -496,9 +699,10 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
       if (lane == 0) mbar_arrive1(&hd.emptyI[t]);   // input stage consumed by this warp
       cons_sync();                                    // all q written, red complete
       if (warp == 0) {
-        if (comp) {
-          const double r = warp_tree(CNRED == 64 ? hd.red[i & 1][2 * lane] + hd.red[i & 1][2 * lane + 1]
-                                                 : hd.red[i & 1][lane]);
+        if (comp) {   // the slice partial: pairwise tree over the 16 warp subtrees
+          double r = lane < CCW ? hd.red[i & 1][lane] : 0.0;
+#pragma unroll
+          for (int m = 1; m < CCW; m <<= 1) r = r + __shfl_xor_sync(0xffffffffu, r, m);
           if (lane == 0) hd.part[hs] = r;   // the slice's reducer publishes it
         }
         if (lane == 0) mbar_arrive1(&hd.pready[hs]);   // release: q and part[hs] visible to the reducer
@@ -523,6 +727,7 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
       } else {
         emit(BoolC<false>{}, d, H(hs), pay, total);
       }
+      fence_proxy_async();   // this thread's smem writes before the producer's bulk store
       __syncwarp();
       if (lane == 0) mbar_arrive1(&hd.emptyH[hs]);   // this warp is done with held stage hs
     }
@@ -531,6 +736,7 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
   if (FUSED && p.pass != 1) {   // fused exchange: release this step's payload bytes to the peers
     __threadfence_system();
     cons_sync();
+    if (threadIdx.x == 0) mbar_wait(&hd.pfin, 0, 0x6000000u);   // the producer's raw stores landed
     peer_signal(p.sync, threadIdx.x == 0);
   }
 }
@@ -583,13 +789,20 @@ static cudaError_t launch_cstream_t(int kind, StreamParams p, int grid, cudaStre
     return cudaLaunchKernelEx(&cfg, fn, p);
   };
   const bool fused = p.ndst > 0 || p.sync.wflags != nullptr;
+  auto dither = [&](auto kind_tag) -> cudaError_t {
+    constexpr int K = decltype(kind_tag)::value;
+    switch (p.bits) {
+      case 3: return fused ? go(cstream_kernel<K, SERVER, true, 3>) : go(cstream_kernel<K, SERVER, false, 3>);
+      case 5: return fused ? go(cstream_kernel<K, SERVER, true, 5>) : go(cstream_kernel<K, SERVER, false, 5>);
+      case 7: return fused ? go(cstream_kernel<K, SERVER, true, 7>) : go(cstream_kernel<K, SERVER, false, 7>);
+    }
+    return fused ? go(cstream_kernel<K, SERVER, true, 0>) : go(cstream_kernel<K, SERVER, false, 0>);
+  };
   switch (kind) {
-    case C_NONE: return fused ? go(cstream_kernel<C_NONE, SERVER, true>) : go(cstream_kernel<C_NONE, SERVER, false>);
-    case C_SIGN: return fused ? go(cstream_kernel<C_SIGN, SERVER, true>) : go(cstream_kernel<C_SIGN, SERVER, false>);
-    case C_LDITHER:
-      return fused ? go(cstream_kernel<C_LDITHER, SERVER, true>) : go(cstream_kernel<C_LDITHER, SERVER, false>);
-    case C_NDITHER:
-      return fused ? go(cstream_kernel<C_NDITHER, SERVER, true>) : go(cstream_kernel<C_NDITHER, SERVER, false>);
+    case C_NONE: return fused ? go(cstream_kernel<C_NONE, SERVER, true, 0>) : go(cstream_kernel<C_NONE, SERVER, false, 0>);
+    case C_SIGN: return fused ? go(cstream_kernel<C_SIGN, SERVER, true, 0>) : go(cstream_kernel<C_SIGN, SERVER, false, 0>);
+    case C_LDITHER: return dither(std::integral_constant<int, C_LDITHER>{});
+    case C_NDITHER: return dither(std::integral_constant<int, C_NDITHER>{});
   }
   return cudaErrorInvalidValue;
 }

@@ -66,22 +66,14 @@ struct __align__(128) USmem {
   double red[UST][3][UTILE / 16];  // LANS pass 1: 16-element subtrees of x^2, u^2, w^2
 };
 
-__device__ __forceinline__ void adam1s(float g, float& m, float& v, float& x, const UpdateParams& p) {
-  m = fadd(fmul(p.beta1, m), fmul(p.omb1, g));                 // line 12
-  v = fadd(fmul(p.beta2, v), fmul(p.omb2, fmul(g, g)));        // line 13
-  const float mh = fdiv(m, p.bc1);                             // line 14: m / (1 - beta1^t)
-  const float vh = fdiv(v, p.bc2);                             // line 15: v / (1 - beta2^t)
-  const float r = fdiv(mh, fadd(__fsqrt_rn(vh), p.eps));       // line 16
-  x = fsub(x, fmul(p.lr, fadd(r, fmul(p.wd, x))));             // x update (Adam core)
-}
 
 // LANS (R22): u = r + lambda x, w = c + lambda x with r = m~/(sqrt(v~)+eps),
 // c = g~/(sqrt(v~)+eps), from the already-updated m, v (the oracle's order)
 __device__ __forceinline__ void lans_uw(float g, float m, float v, float x, const UpdateParams& p, float& u,
                                         float& w) {
-  const float den = fadd(__fsqrt_rn(fdiv(v, p.bc2)), p.eps);
-  u = fadd(fdiv(fdiv(m, p.bc1), den), fmul(p.wd, x));
-  w = fadd(fdiv(g, den), fmul(p.wd, x));
+  const float den = fadd(fsqrt0(divc(v, p.bc2, p.ibc2)), p.eps);
+  u = fadd(fdiv_pos(divc(m, p.bc1, p.ibc1), den), fmul(p.wd, x));
+  w = fadd(fdiv_pos(g, den), fmul(p.wd, x));
 }
 
 // FUSED: wait for the owners' p (fused NVLink exchange), then bulk-copy each
@@ -186,7 +178,9 @@ __global__ void __launch_bounds__(SNT, 1) update_stream(const __grid_constant__ 
   const int cmax = (1 << (p.bits - 1)) - 1;
   for (uint32_t i = 0; i < mine; i++) {
     const int s = i % UST;
-    mbar_wait(&sm.full[s], (i / UST) & 1);
+    // the tile's bytes: a short sleep between polls keeps the waiting warps off
+    // the issue slots of the ones computing (a tile streams in ~2 us)
+    mbar_wait_backoff(&sm.full[s], (i / UST) & 1, 64);
     const UDesc d = sm.desc[s];
     const uint32_t nvec = d.len >> 2;
     float* m = p.m + d.off;
@@ -235,10 +229,7 @@ __global__ void __launch_bounds__(SNT, 1) update_stream(const __grid_constant__ 
         x4 = load4_masked(x, j, d.L);
       }
       if (MODE == 0) {
-        adam1s(g4.x, m4.x, v4.x, x4.x, p);
-        adam1s(g4.y, m4.y, v4.y, x4.y, p);
-        adam1s(g4.z, m4.z, v4.z, x4.z, p);
-        adam1s(g4.w, m4.w, v4.w, x4.w, p);
+        adam4(g4, m4, v4, x4, p);
         if (f < nvec) {
           st4(m + j, m4);
           st4(v + j, v4);

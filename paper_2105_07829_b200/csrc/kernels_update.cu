@@ -8,21 +8,13 @@ namespace bpc {
 
 enum { U_NONE = 0, U_SIGN = 2, U_TOPK = 3, U_RANDK = 4, U_LDITHER = 5, U_NDITHER = 6 };
 
-__device__ __forceinline__ void adam1(float g, float& m, float& v, float& x, const UpdateParams& p) {
-  m = fadd(fmul(p.beta1, m), fmul(p.omb1, g));                 // line 12
-  v = fadd(fmul(p.beta2, v), fmul(p.omb2, fmul(g, g)));        // line 13
-  const float mh = fdiv(m, p.bc1);                             // line 14: m / (1 - beta1^t) (R16)
-  const float vh = fdiv(v, p.bc2);                             // line 15: v / (1 - beta2^t)
-  const float r = fdiv(mh, fadd(__fsqrt_rn(vh), p.eps));       // line 16
-  x = fsub(x, fmul(p.lr, fadd(r, fmul(p.wd, x))));             // x update (Adam core)
-}
 
 // LANS (R22): u = r + lambda x, w = c + lambda x from the updated m, v
 __device__ __forceinline__ void lans_uw1(float g, float m, float v, float x, const UpdateParams& p, float& u,
                                          float& w) {
-  const float den = fadd(__fsqrt_rn(fdiv(v, p.bc2)), p.eps);
-  u = fadd(fdiv(fdiv(m, p.bc1), den), fmul(p.wd, x));
-  w = fadd(fdiv(g, den), fmul(p.wd, x));
+  const float den = fadd(fsqrt0(divc(v, p.bc2, p.ibc2)), p.eps);
+  u = fadd(fdiv_pos(divc(m, p.bc1, p.ibc1), den), fmul(p.wd, x));
+  w = fadd(fdiv_pos(g, den), fmul(p.wd, x));
 }
 
 // MODE 0: Adam core; LANS (R22) MODE 1: m, v + the tile's pairwise sums of
@@ -115,10 +107,7 @@ __global__ void __launch_bounds__(UNT, 4) update_kernel(const __grid_constant__ 
       }
     }
     if (MODE == 0) {
-      adam1(g4.x, m4[it].x, v4[it].x, x4[it].x, p);
-      adam1(g4.y, m4[it].y, v4[it].y, x4[it].y, p);
-      adam1(g4.z, m4[it].z, v4[it].z, x4[it].z, p);
-      adam1(g4.w, m4[it].w, v4[it].w, x4[it].w, p);
+      adam4(g4, m4[it], v4[it], x4[it], p);
       if (full) {
         st4(m + j, m4[it]);
         st4(v + j, v4[it]);
