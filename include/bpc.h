@@ -27,11 +27,20 @@
  *    enqueued on them.  host_* are host pointers.  The context owns its
  *    worker error e, server error e~ (owned shard only), m, v, t and all
  *    payload buffers.
- *  - All device work is enqueued on cfg.cuda_stream (borrowed), in call order,
- *    and is CUDA-graph capturable when the world size is 1.
+ *  - All device work is enqueued on cfg.cuda_stream (borrowed), in call order.
+ *  - CUDA graphs: one step's calls (compress .. step, any world size, either
+ *    exchange) may be captured once on cfg.cuda_stream and replayed; each replay
+ *    is the next step.  The step counter t and the per-kernel-family launch and
+ *    exchange epochs live in device memory and advance inside the kernels (the
+ *    step's last update launch advances t), so no host value is baked into the
+ *    graph.  The bias corrections of step t come from a device table built at
+ *    bpc_init (R16).  bpc_sync, bpc_copy_state / load_state, get / set_step and
+ *    bpc_get_timing synchronise and must stay outside a capture; timing must be
+ *    off while capturing.
  *  - Call order per step: compress -> aggregate (or push, server, pull) -> step;
  *    out-of-order calls return BPC_ERR_BAD_STATE.  A context is not thread-safe.
- *  - Step counter t starts at 1 and advances in bpc_step.
+ *  - Step counter t starts at 1 and advances in bpc_step's last kernel
+ *    (SPEC.md:362, 411).
  *  - There is no CPU fallback: without a usable sm_100 device bpc_init fails
  *    with BPC_ERR_CUDA.
  */
@@ -241,6 +250,9 @@ bpc_status bpc_load_state(bpc_ctx* ctx, int32_t which, const void* host_src, uin
 /* Exchange transport in use (bpc_exchange_mode; BPC_EXCHANGE_NCCL also when
  * world_size == 1 or for an external exchange, where no transport runs). */
 bpc_status bpc_get_exchange(const bpc_ctx* ctx, int32_t* mode);
+/* The device step counter t: get waits for cfg.cuda_stream to drain and reads it;
+ * set (t >= 1, else BPC_ERR_INVALID_ARGUMENT) writes it in stream order and
+ * waits (resume after bpc_load_state of e, e~, m, v). */
 bpc_status bpc_get_step(const bpc_ctx* ctx, uint32_t* t);
 bpc_status bpc_set_step(bpc_ctx* ctx, uint32_t t);
 

@@ -97,8 +97,6 @@ bpc_status make_plan(const bpc_config* cfg, Plan* P, std::string* err) {
   if (cfg->optimizer == BPC_OPT_LANS && !(cfg->lans_alpha_l > 0.f && cfg->lans_alpha_l <= cfg->lans_alpha_u))
     return fail(BPC_ERR_INVALID_ARGUMENT, "LANS needs 0 < alpha_l <= alpha_u");
   if (cfg->unit_mode != 0 && cfg->unit_mode != 1) return fail(BPC_ERR_INVALID_ARGUMENT, "unit_mode is 0 or 1");
-  if (cfg->unit_mode == 1 && !stream_worker(C.kind))
-    return fail(BPC_ERR_UNSUPPORTED_KIND, "per-tensor units: scaled sign, dithering or NONE only");
   uint64_t ce = cfg->chunk_elems ? cfg->chunk_elems : (1ull << 18);
   if (ce < kSlice || ce > 16 * kSlice || (ce & (ce - 1)))
     return fail(BPC_ERR_INVALID_ARGUMENT, "chunk_elems must be a power of two in [2^14, 2^18]");
@@ -110,8 +108,8 @@ bpc_status make_plan(const bpc_config* cfg, Plan* P, std::string* err) {
     const uint64_t L = cfg->tensor_numel[t], o = cfg->tensor_offset[t];
     if (L == 0) return fail(BPC_ERR_EMPTY_BLOCK, "tensor with numel 0");
     if (L >= (1ull << 31)) return fail(BPC_ERR_INVALID_ARGUMENT, "tensor numel >= 2^31");
-    if (cfg->unit_mode == 1 && L > (uint64_t)kStreamSlice * UNIT_MAX_SLICES)
-      return fail(BPC_ERR_INVALID_ARGUMENT, "per-tensor unit larger than 2^27 elements");
+    if (cfg->unit_mode == 1 && stream_worker(C.kind) && L > (uint64_t)kStreamSlice * UNIT_MAX_SLICES)
+      return fail(BPC_ERR_INVALID_ARGUMENT, "per-tensor unit of a norm-based kind larger than 2^27 elements");
     if (cfg->optimizer == BPC_OPT_LANS && L > 4096ull * LANS_MAX_TILES)
       return fail(BPC_ERR_INVALID_ARGUMENT, "LANS block (tensor) larger than 2^25 elements");
     if (o % 4) return fail(BPC_ERR_INVALID_ARGUMENT, "tensor offsets must be multiples of 4 elements");
@@ -221,11 +219,23 @@ struct bpc_ctx {
   // candidate thresholds, counters, candidate lists
   uint32_t* d_chunk2u[2] = {nullptr, nullptr};
   uint32_t* d_guess[2] = {nullptr, nullptr};
-  uint32_t* d_cnt[2] = {nullptr, nullptr};
+  uint32_t* d_scnt[2] = {nullptr, nullptr};         // candidates per slice (streaming pass)
+  uint32_t* d_first_slice[2] = {nullptr, nullptr};  // per unit: its first slice
   uint32_t* d_cand[2] = {nullptr, nullptr};
   uint32_t* d_cand_off[2] = {nullptr, nullptr};
   uint32_t sel_cap[2] = {0, 0};                  // CTA select kernel: candidates in shared memory
   uint32_t* d_big[2] = {nullptr, nullptr};       // units handed from the warp to the CTA select
+  uint2* d_apply_blk = nullptr;                  // server: 256-entry blocks of the ranks' entries
+  uint32_t n_apply_blk = 0;
+  // per-tensor units longer than SEL_LMAX, per side: the large-unit select path
+  uint32_t* d_large_units[2] = {nullptr, nullptr};
+  uint2* d_lslices[2] = {nullptr, nullptr};
+  uint32_t* d_lslice_first[2] = {nullptr, nullptr};
+  uint32_t* d_lstate[2] = {nullptr, nullptr};
+  uint32_t* d_lhist[2] = {nullptr, nullptr};
+  uint2* d_lcnt[2] = {nullptr, nullptr};
+  uint2* d_loff[2] = {nullptr, nullptr};
+  uint32_t n_large[2] = {0, 0}, n_lslices[2] = {0, 0};
   float* d_sdelta = nullptr;   // server Delta of the owned units (sparse kinds without EF)
   unsigned int* d_flag = nullptr;
   // streaming worker (norm-based compressors): slices, partials, unit counters
@@ -233,22 +243,18 @@ struct bpc_ctx {
   uint32_t n_wslices = 0;
   double* d_wpartials = nullptr;
   unsigned long long* d_wcounters = nullptr;
-  uint32_t wepoch = 0;
   // streaming server (owned units)
   Slice* d_sslices = nullptr;
   uint32_t n_sslices = 0;
   double* d_spartials = nullptr;
   unsigned long long* d_scounters = nullptr;
-  uint32_t sepoch = 0;
   int num_sms = 148;
   ncclComm_t comm = nullptr;
   // peer-memory exchange (BPC_EXCHANGE_P2P): peers' IPC-mapped RECV / P / flags
   int32_t exchange = BPC_EXCHANGE_NCCL;
   unsigned long long* d_xflags = nullptr;   // [2n]: push slots [0, n), pull slots [n, 2n)
-  unsigned long long* d_xdone = nullptr;    // [2]: CTA counters of the push / pull copy kernels
   std::vector<uint8_t*> peer_recv, peer_p;
   std::vector<unsigned long long*> peer_flags;
-  uint32_t push_epoch = 0, pull_epoch = 0;
   bool local_group = false;   // bpc_connect_local: peers are contexts of this process (direct pointers)
   // LANS (BPC_OPT_LANS): per update tile partial sums, per block coefficients
   double* d_lans_part = nullptr;
@@ -259,7 +265,12 @@ struct bpc_ctx {
   float2* d_lans_coef = nullptr;
   uint32_t* d_blk_tile = nullptr;
   int push_grid = 1, pull_grid = 1;
-  uint32_t t = 1;
+  // device-side step state: the step counter t and the launch / exchange epochs
+  // live in HBM and advance inside the kernels, so a captured step replays
+  DevState* d_st = nullptr;
+  float4* d_bct = nullptr;   // bias corrections per step (R16), see BiasTab
+  uint32_t nbct = 0;
+  int32_t bconv = 0;
   int phase = 0;   // 0 compress, 1 push, 2 server, 3 pull, 4 step
   bool timing = false;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> events;
@@ -367,14 +378,21 @@ void free_ctx(bpc_ctx* ctx) {
                   (void*)ctx->d_wufirst, (void*)ctx->d_wuns, (void*)ctx->d_sufirst, (void*)ctx->d_suns,
                   (void*)ctx->d_wutotal, (void*)ctx->d_sutotal})
     if (q) cudaFree(q);
-  if (ctx->d_xdone) cudaFree(ctx->d_xdone);
+  for (void* q : {(void*)ctx->d_st, (void*)ctx->d_bct})
+    if (q) cudaFree(q);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   for (void* p : {(void*)ctx->e, (void*)ctx->etl, (void*)ctx->m, (void*)ctx->v, (void*)ctx->send,
                   (void*)ctx->pbuf, (void*)ctx->d_chunks, (void*)ctx->d_witems, (void*)ctx->d_sitems,
                   (void*)ctx->d_utiles, (void*)ctx->d_flag, (void*)ctx->d_sdelta,
                   (void*)ctx->d_chunk2u[0], (void*)ctx->d_chunk2u[1], (void*)ctx->d_guess[0], (void*)ctx->d_guess[1],
-                  (void*)ctx->d_cnt[0], (void*)ctx->d_cnt[1], (void*)ctx->d_cand[0], (void*)ctx->d_cand[1],
+                  (void*)ctx->d_scnt[0], (void*)ctx->d_scnt[1], (void*)ctx->d_first_slice[0],
+                  (void*)ctx->d_first_slice[1], (void*)ctx->d_cand[0], (void*)ctx->d_cand[1],
                   (void*)ctx->d_cand_off[0], (void*)ctx->d_cand_off[1], (void*)ctx->d_big[0], (void*)ctx->d_big[1],
+                  (void*)ctx->d_apply_blk, (void*)ctx->d_large_units[0], (void*)ctx->d_large_units[1],
+                  (void*)ctx->d_lslices[0], (void*)ctx->d_lslices[1], (void*)ctx->d_lslice_first[0],
+                  (void*)ctx->d_lslice_first[1], (void*)ctx->d_lstate[0], (void*)ctx->d_lstate[1],
+                  (void*)ctx->d_lhist[0], (void*)ctx->d_lhist[1], (void*)ctx->d_lcnt[0], (void*)ctx->d_lcnt[1],
+                  (void*)ctx->d_loff[0], (void*)ctx->d_loff[1],
                   (void*)ctx->d_wslices, (void*)ctx->d_wpartials, (void*)ctx->d_wcounters,
                   (void*)ctx->d_sslices, (void*)ctx->d_spartials, (void*)ctx->d_scounters})
     if (p) cudaFree(p);
@@ -413,8 +431,6 @@ bpc_status setup_p2p(bpc_ctx* ctx) {
   cudaError_t ce;
   CK(cudaMalloc((void**)&ctx->d_xflags, 16ull * n), "alloc exchange flags");
   CK(cudaMemset(ctx->d_xflags, 0, 16ull * n), "zero exchange flags");
-  CK(cudaMalloc((void**)&ctx->d_xdone, 16), "alloc exchange counters");
-  CK(cudaMemset(ctx->d_xdone, 0, 16), "zero exchange counters");
   struct Rec {
     cudaIpcMemHandle_t h[3];
     int32_t ok;
@@ -489,18 +505,31 @@ bpc_status setup_p2p(bpc_ctx* ctx) {
 bool fused_exchange(const bpc_ctx* ctx) {
   return ctx->exchange == BPC_EXCHANGE_P2P && stream_worker(ctx->cfg.comp.kind);
 }
-PeerSync peer_sync(const bpc_ctx* ctx) {
+// launch bookkeeping of one kernel of family `fam` (EP_*): epochs and the step
+// counter are read and advanced on the device (DevState)
+PeerSync peer_sync(const bpc_ctx* ctx, int fam) {
   PeerSync s = {};
+  s.st = ctx->d_st;
+  s.fam = fam;
+  s.wait_fam = -1;
+  s.sig_fam = -1;
   s.n = (uint32_t)ctx->cfg.world_size;
   s.self = (uint32_t)ctx->cfg.rank;
   return s;
 }
-void set_signal(bpc_ctx* ctx, PeerSync* s, int which, uint32_t epoch) {
+// wait for exchange family `fam` (EP_PUSH: slots [0, n); EP_PULL: [n, 2n)) in
+// this rank's flag array
+void set_wait(const bpc_ctx* ctx, PeerSync* s, int fam) {
+  s->wait_fam = fam;
+  s->wflags = ctx->d_xflags;
+  s->wslot0 = fam == EP_PUSH ? 0u : (uint32_t)ctx->cfg.world_size;
+}
+// release exchange family `fam` into this rank's slot of every peer's flag array
+void set_signal(const bpc_ctx* ctx, PeerSync* s, int fam) {
   const int n = ctx->cfg.world_size, rank = ctx->cfg.rank;
-  s->done = ctx->d_xdone + which;
+  s->sig_fam = fam;
   for (int r = 0; r < n; r++) s->sflag[r] = r == rank ? nullptr : ctx->peer_flags[r];
-  s->sslot = (uint32_t)(which * n + rank);
-  s->sepoch = epoch;
+  s->sslot = (uint32_t)((fam == EP_PUSH ? 0 : n) + rank);
 }
 
 // Streaming worker / server launch: one pass, or (per-tensor units) partials,
@@ -521,13 +550,56 @@ cudaError_t launch_stream_side(bpc_ctx* ctx, bool server, StreamParams& q) {
   ut.nunits = server ? ctx->n_sunits : ctx->n_wunits;
   ut.total = server ? ctx->d_sutotal : ctx->d_wutotal;
   q.pass = 1;
+  const int sig = q.sync.sig_fam;   // the exchange is released by pass 2 only
+  q.sync.sig_fam = -1;
   cudaError_t e = go();
   if (e == cudaSuccess) e = launch_unit_tree(ut, ctx->stream);
   q.pass = 2;
+  q.sync.sig_fam = sig;
   q.unit_total = ut.total;
   if (e == cudaSuccess) e = go();
   ctx->launches += 3;
   return e;
+}
+
+// sparse kinds, one side: prep (server entries, candidate threshold), the
+// streaming pass (cstream_kernel<C_TOPK / C_RANDK>: q / Delta, candidates, raw
+// units), then the exact selection and payload (kernels_sparse.cu)
+bpc_status launch_sparse_side(bpc_ctx* ctx, const SparseParams& p, const float* d_grad) {
+  const int kind = ctx->cfg.comp.kind;
+  CK(launch_sparse_prep(kind, p, ctx->stream), "sparse prep launch");
+  StreamParams q = {};
+  q.grad = d_grad;
+  q.err = p.vals;
+  q.out = p.out;
+  q.recv = p.recv;
+  q.slot_bytes = p.slot_bytes;
+  q.chunks = ctx->d_chunks;
+  q.slices = p.slices;
+  q.n_slices = p.n_slices;
+  q.partials = p.server ? ctx->d_spartials : ctx->d_wpartials;
+  q.counters = p.server ? ctx->d_scounters : ctx->d_wcounters;
+  q.n = p.n;
+  q.inv_n = p.inv_n;
+  q.rank = p.server ? 0u : (uint32_t)ctx->cfg.rank;
+  q.stage = p.stage;
+  q.seed = p.seed;
+  q.bits = 1;
+  q.use_ef = p.use_ef;
+  q.check_finite = p.server ? 0 : p.check_finite;
+  q.flag = ctx->d_flag;
+  q.sync = peer_sync(ctx, p.server ? EP_SERVER : EP_WORKER);
+  q.sp_chunk2u = p.chunk2u;
+  q.sp_guess = p.guess;
+  q.sp_scnt = p.scnt;
+  q.sp_cand = p.cand;
+  q.sp_cand_off = p.cand_off;
+  cudaError_t e = p.server ? launch_server_stream(kind, q, ctx->num_sms, ctx->stream)
+                           : launch_worker_stream(kind, q, ctx->num_sms, ctx->stream);
+  CK(e, "sparse streaming launch");
+  CK(launch_sparse_select(kind, p, ctx->stream), "sparse select launch");
+  ctx->launches += 4;
+  return BPC_OK;
 }
 
 SparseParams sparse_params(bpc_ctx* ctx, int side) {
@@ -539,12 +611,13 @@ SparseParams sparse_params(bpc_ctx* ctx, int side) {
   p.n_slices = side ? ctx->n_sslices : ctx->n_wslices;
   p.chunk2u = ctx->d_chunk2u[side];
   p.guess = ctx->d_guess[side];
-  p.cnt = ctx->d_cnt[side];
+  p.scnt = ctx->d_scnt[side];
+  p.first_slice = ctx->d_first_slice[side];
   p.cand = ctx->d_cand[side];
   p.cand_off = ctx->d_cand_off[side];
   p.n = (uint32_t)ctx->cfg.world_size;
   p.inv_n = 1.0 / (double)ctx->cfg.world_size;
-  p.t = ctx->t;
+  p.st = ctx->d_st;
   p.stage = side ? 1u : 0u;
   p.rrank = side ? 0u : (uint32_t)ctx->cfg.rank;
   p.seed = ctx->cfg.seed;
@@ -556,6 +629,18 @@ SparseParams sparse_params(bpc_ctx* ctx, int side) {
   p.flag = ctx->d_flag;
   p.sel_cap = ctx->sel_cap[side];
   p.big = ctx->d_big[side];
+  p.apply_blk = ctx->d_apply_blk;
+  p.n_apply_blk = side ? ctx->n_apply_blk : 0;
+  p.large_units = ctx->d_large_units[side];
+  p.n_large = ctx->n_large[side];
+  p.lslices = ctx->d_lslices[side];
+  p.n_lslices = ctx->n_lslices[side];
+  p.lslice_first = ctx->d_lslice_first[side];
+  p.lstate = ctx->d_lstate[side];
+  p.lhist = ctx->d_lhist[side];
+  p.lcnt = ctx->d_lcnt[side];
+  p.loff = ctx->d_loff[side];
+  p.large_grid = 2u * (uint32_t)ctx->num_sms;
   return p;
 }
 
@@ -658,6 +743,33 @@ bpc_status bpc_init(const bpc_config* cfg, bpc_ctx** out) {
     if ((ce = alloc((void**)&ctx->recv, ctx->recv_bytes)) != cudaSuccess) return bail(cuda_fail(ctx, ce, "alloc recv"));
   }
   if ((ce = alloc((void**)&ctx->d_flag, 4)) != cudaSuccess) return bail(cuda_fail(ctx, ce, "alloc flag"));
+  // step state (t = 1, epochs 0) and the bias-correction table (R16): rows for
+  // t = 1.. until both fl32(1 - beta^t) reach 1.0f, at most 2^20 rows
+  if ((ce = alloc((void**)&ctx->d_st, sizeof(DevState))) != cudaSuccess) return bail(cuda_fail(ctx, ce, "alloc step state"));
+  {
+    const uint32_t one = 1;
+    if ((ce = cudaMemcpy(&ctx->d_st->t, &one, 4, cudaMemcpyHostToDevice)) != cudaSuccess)
+      return bail(cuda_fail(ctx, ce, "init step state"));
+    std::vector<float4> bct;
+    const double b1 = (double)cfg->beta1, b2 = (double)cfg->beta2;
+    ctx->bconv = 0;
+    for (uint32_t t = 1; t <= (1u << 20); t++) {
+      float4 r;
+      r.x = (float)(1.0 - std::pow(b1, (double)t));
+      r.y = (float)(1.0 - std::pow(b2, (double)t));
+      r.z = 1.0f / r.x;   // RN(1 / bc): IEEE fp32 division on the host
+      r.w = 1.0f / r.y;
+      bct.push_back(r);
+      if (r.x == 1.0f && r.y == 1.0f) {
+        ctx->bconv = 1;
+        break;
+      }
+    }
+    ctx->nbct = (uint32_t)bct.size();
+    if ((ce = alloc((void**)&ctx->d_bct, 16ull * bct.size())) != cudaSuccess) return bail(cuda_fail(ctx, ce, "alloc bias table"));
+    if ((ce = cudaMemcpy(ctx->d_bct, bct.data(), 16ull * bct.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
+      return bail(cuda_fail(ctx, ce, "upload bias table"));
+  }
   // device tables
   std::vector<DevChunk> dch(P.chunks.size());
   std::vector<uint32_t> witems, sitems;
@@ -700,35 +812,49 @@ bpc_status bpc_init(const bpc_config* cfg, bpc_ctx** out) {
   ctx->n_witems = (uint32_t)witems.size();
   ctx->n_sitems = (uint32_t)sitems.size();
   if (sparse_kind) {
-    // per side: chunk -> unit, candidate capacity per unit (the
-    // guess keeps ~1.5-5 k candidates; the lists hold about twice that, the server
-    // also the n ranks' k entries), counters zeroed once (the select kernel resets)
+    // per side: chunk -> unit, and each unit's candidate list: one index-ordered
+    // sub-list per 2^13-element slice of cs entries, cs ~ 3x the expected
+    // candidates of a slice + 32 (the guess keeps ~1.5-5 k candidates per unit;
+    // the server also lists the n ranks' k entries); an overflowing slice sends
+    // its unit to the exact whole-unit path
     for (int side = 0; side < 2; side++) {
       const std::vector<uint32_t>& items = side ? sitems : witems;
-      std::vector<uint32_t> c2u(P.chunks.size(), 0xffffffffu), off(items.size() + 1, 0);
+      std::vector<uint32_t> c2u(P.chunks.size(), 0xffffffffu), off(items.size() + 1, 0), first(items.size(), 0);
       for (uint32_t u = 0; u < items.size(); u++) {
         const auto& ci = P.chunks[items[u]];
-        const uint64_t L = ci.len, k = ci.k;
-        uint64_t cap;
-        if (cfg->comp.kind == BPC_RANDOM_K) {
-          cap = k + (uint64_t)(16.0 * std::sqrt((double)k)) + 256;
-        } else {
-          cap = L <= 4096 ? L : (uint64_t)std::ceil(2.0 * sparse_sample_rank((uint32_t)k, (uint32_t)L) * (double)L / 4096.0) + 1024;
-          if (side) cap += (uint64_t)n * k;
-        }
+        const uint64_t L = ci.len, k = ci.k, ns = (L + kStreamSlice - 1) / kStreamSlice;
+        double expect;   // candidates of the unit
+        if (cfg->comp.kind == BPC_RANDOM_K) expect = (double)k + 8.0 * std::sqrt((double)k) + 64.0;
+        else if (side && !cfg->comp.use_ef) expect = (double)n * k;   // nonzero Delta only
+        else expect = (double)sparse_sample_rank((uint32_t)k, (uint32_t)L) * (double)L / 4096.0 + (side ? (double)n * k : 0.0);
+        const double per = std::min<double>((double)kStreamSlice, expect * (double)kStreamSlice / (double)L);
+        uint64_t cs = L <= 4096 ? L : (uint64_t)std::ceil(3.0 * per + 32.0);
+        cs = std::min<uint64_t>(cs, kStreamSlice);
         c2u[items[u]] = u;
-        off[u + 1] = off[u] + (uint32_t)std::min<uint64_t>(L, cap);
-        ctx->sel_cap[side] = std::max<uint32_t>(ctx->sel_cap[side], (uint32_t)std::min<uint64_t>(L, cap));
+        off[u + 1] = off[u] + (uint32_t)(ns * cs);
+        if (L <= SEL_LMAX) ctx->sel_cap[side] = std::max<uint32_t>(ctx->sel_cap[side], (uint32_t)std::min<uint64_t>(L, ns * cs));
       }
-      // a power of two: the bitonic sorts of the tie / selection lists (<= the
-      // candidate count) pad to the next power of two inside this region
+      // the units' first slices in this side's slice table (same construction as below)
+      {
+        uint32_t si = 0;
+        for (uint32_t c = 0; c < P.chunks.size(); c++) {
+          const auto& ci = P.chunks[c];
+          if (side == 1 && ci.owner != rank) continue;
+          if (c2u[c] != 0xffffffffu) first[c2u[c]] = si;
+          si += (uint32_t)((ci.len + kStreamSlice - 1) / kStreamSlice);
+        }
+        if ((ce = alloc((void**)&ctx->d_scnt[side], 4ull * std::max<uint32_t>(si, 1))) != cudaSuccess)
+          return bail(cuda_fail(ctx, ce, "alloc slice counts"));
+      }
+      // a power of two: the CTA select pads nothing, but the bound keeps its shared
+      // memory fixed
       uint32_t sc = 1;
       while (sc < ctx->sel_cap[side]) sc <<= 1;
       ctx->sel_cap[side] = std::min<uint32_t>(sc, SEL_CAP);
       if ((s = upload(ctx, &ctx->d_chunk2u[side], c2u)) != BPC_OK) return bail(s);
       if ((s = upload(ctx, &ctx->d_cand_off[side], off)) != BPC_OK) return bail(s);
+      if ((s = upload(ctx, &ctx->d_first_slice[side], first)) != BPC_OK) return bail(s);
       if ((ce = alloc((void**)&ctx->d_guess[side], 4ull * items.size())) != cudaSuccess) return bail(cuda_fail(ctx, ce, "alloc guesses"));
-      if ((ce = alloc((void**)&ctx->d_cnt[side], 4ull * items.size())) != cudaSuccess) return bail(cuda_fail(ctx, ce, "alloc counters"));
       if ((ce = alloc((void**)&ctx->d_cand[side], 4ull * off.back())) != cudaSuccess) return bail(cuda_fail(ctx, ce, "alloc candidates"));
       if ((ce = alloc((void**)&ctx->d_big[side], 4ull * items.size())) != cudaSuccess) return bail(cuda_fail(ctx, ce, "alloc select flags"));
     }
@@ -782,6 +908,53 @@ bpc_status bpc_init(const bpc_config* cfg, bpc_ctx** out) {
     }
   }
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cfg->device);
+  if (sparse_kind) {
+    // server: the ranks' entries in 256-entry blocks (sparse_apply)
+    std::vector<uint2> ab;
+    for (uint32_t u = 0; u < sitems.size(); u++) {
+      const uint64_t ne = (uint64_t)n * P.chunks[sitems[u]].k;
+      for (uint64_t f = 0; f < ne; f += 256) ab.push_back(make_uint2(u, (uint32_t)f));
+    }
+    if ((s = upload(ctx, &ctx->d_apply_blk, ab)) != BPC_OK) return bail(s);
+    ctx->n_apply_blk = (uint32_t)ab.size();
+    // per side: units longer than SEL_LMAX and their slices (same order as the slice tables)
+    for (int side = 0; side < 2; side++) {
+      const std::vector<uint32_t>& items = side ? sitems : witems;
+      std::vector<uint32_t> lunits, lfirst;
+      std::vector<uint2> lsl;
+      std::vector<int32_t> lu_of(P.chunks.size(), -1);
+      for (uint32_t u = 0; u < items.size(); u++)
+        if (P.chunks[items[u]].len > SEL_LMAX) {
+          lu_of[items[u]] = (int32_t)lunits.size();
+          lunits.push_back(u);
+        }
+      uint32_t si = 0;
+      int32_t cur = -1;
+      for (uint32_t c = 0; c < P.chunks.size(); c++) {
+        const auto& ci = P.chunks[c];
+        if (side == 1 && ci.owner != rank) continue;
+        for (uint64_t s0 = 0; s0 < ci.len; s0 += kStreamSlice, si++) {
+          if (lu_of[c] < 0) continue;
+          if (lu_of[c] != cur) {
+            cur = lu_of[c];
+            lfirst.push_back((uint32_t)lsl.size());
+          }
+          lsl.push_back(make_uint2(si, (uint32_t)lu_of[c]));
+        }
+      }
+      lfirst.push_back((uint32_t)lsl.size());
+      ctx->n_large[side] = (uint32_t)lunits.size();
+      ctx->n_lslices[side] = (uint32_t)lsl.size();
+      if (lunits.empty()) continue;
+      if ((s = upload(ctx, &ctx->d_large_units[side], lunits)) != BPC_OK) return bail(s);
+      if ((s = upload(ctx, &ctx->d_lslices[side], lsl)) != BPC_OK) return bail(s);
+      if ((s = upload(ctx, &ctx->d_lslice_first[side], lfirst)) != BPC_OK) return bail(s);
+      if ((ce = alloc((void**)&ctx->d_lstate[side], 32ull * lunits.size())) != cudaSuccess) return bail(cuda_fail(ctx, ce, "alloc large state"));
+      if ((ce = alloc((void**)&ctx->d_lhist[side], 1024ull * lunits.size())) != cudaSuccess) return bail(cuda_fail(ctx, ce, "alloc large hist"));
+      if ((ce = alloc((void**)&ctx->d_lcnt[side], 8ull * lsl.size())) != cudaSuccess) return bail(cuda_fail(ctx, ce, "alloc large counts"));
+      if ((ce = alloc((void**)&ctx->d_loff[side], 8ull * lsl.size())) != cudaSuccess) return bail(cuda_fail(ctx, ce, "alloc large offsets"));
+    }
+  }
   if ((ce = cudaDeviceSynchronize()) != cudaSuccess) return bail(cuda_fail(ctx, ce, "init sync"));
   // NCCL communicator (collective over all ranks)
   if (cfg->nccl_unique_id && n > 1) {
@@ -804,7 +977,7 @@ bpc_status bpc_connect_local(bpc_ctx* const* ctxs, int32_t n) {
     bpc_ctx* c = ctxs[r];
     if (!c) return BPC_ERR_INVALID_ARGUMENT;
     if (c->cfg.world_size != n || c->cfg.rank != r || c->comm || c->local_group || c->phase != 0 ||
-        c->t != 1) {
+        c->launches != 0) {
       c->err = "bpc_connect_local: needs fresh contexts of world_size n, rank r at index r, no NCCL id";
       return BPC_ERR_BAD_STATE;
     }
@@ -836,10 +1009,6 @@ bpc_status bpc_connect_local(bpc_ctx* const* ctxs, int32_t n) {
     if (!ctx->d_xflags) {
       CK(cudaMalloc((void**)&ctx->d_xflags, 16ull * n), "alloc exchange flags");
       CK(cudaMemset(ctx->d_xflags, 0, 16ull * n), "zero exchange flags");
-    }
-    if (!ctx->d_xdone) {
-      CK(cudaMalloc((void**)&ctx->d_xdone, 16), "alloc exchange counters");
-      CK(cudaMemset(ctx->d_xdone, 0, 16), "zero exchange counters");
     }
   }
   for (int r = 0; r < n; r++) {
@@ -880,10 +1049,8 @@ bpc_status bpc_compress(bpc_ctx* ctx, const float* d_grad) {
     q.n_slices = ctx->n_wslices;
     q.partials = ctx->d_wpartials;
     q.counters = ctx->d_wcounters;
-    q.epoch = ++ctx->wepoch;
     q.n = (uint32_t)ctx->cfg.world_size;
     q.inv_n = 1.0 / (double)ctx->cfg.world_size;
-    q.t = ctx->t;
     q.rank = (uint32_t)ctx->cfg.rank;
     q.stage = 0;
     q.seed = ctx->cfg.seed;
@@ -891,13 +1058,13 @@ bpc_status bpc_compress(bpc_ctx* ctx, const float* d_grad) {
     q.use_ef = ctx->cfg.comp.use_ef;
     q.check_finite = ctx->cfg.check_finite;
     q.flag = ctx->d_flag;
-    q.sync = peer_sync(ctx);
+    q.sync = peer_sync(ctx, EP_WORKER);
     if (fused_exchange(ctx)) {   // fused push: payloads go straight to the owners' RECV slots
       const Plan& P = ctx->plan;
       q.ndst = (uint32_t)ctx->cfg.world_size;
       for (int r = 0; r < ctx->cfg.world_size; r++)
         q.dst[r] = ctx->peer_recv[r] + (uint64_t)ctx->cfg.rank * P.seg_bytes[r];
-      set_signal(ctx, &q.sync, 0, ++ctx->push_epoch);
+      set_signal(ctx, &q.sync, EP_PUSH);
     }
     CK(launch_stream_side(ctx, false, q), "worker stream launch");
   } else {
@@ -905,8 +1072,7 @@ bpc_status bpc_compress(bpc_ctx* ctx, const float* d_grad) {
     p.grad = d_grad;
     p.vals = ctx->e;
     p.out = ctx->send;
-    CK(launch_sparse(ctx->cfg.comp.kind, p, 2 * ctx->num_sms, ctx->stream), "worker sparse launch");
-    ctx->launches += 3;
+    if (bpc_status st = launch_sparse_side(ctx, p, d_grad)) return st;
   }
   timer_end(ctx, BPC_TIMER_COMPRESS, b);
   ctx->phase = 1;
@@ -934,11 +1100,8 @@ bpc_status bpc_exchange_push(bpc_ctx* ctx) {
         q.dst[q.njobs] = ctx->peer_recv[r] + (uint64_t)rank * P.seg_bytes[r];
         q.len[q.njobs++] = P.seg_bytes[r];
       }
-      for (int r = 0; r < n; r++)
-        if (r != rank) q.peer_flag[q.npeers++] = ctx->peer_flags[r];
-      q.slot = rank;
-      q.epoch = ++ctx->push_epoch;
-      q.done = ctx->d_xdone;
+      q.sync = peer_sync(ctx, EP_PUSH);
+      set_signal(ctx, &q.sync, EP_PUSH);
       CK(launch_p2p_copy(q, ctx->push_grid, ctx->stream), "push copy launch");
       ctx->launches += 1;
     } else {
@@ -961,13 +1124,16 @@ bpc_status bpc_exchange_push(bpc_ctx* ctx) {
 }
 
 // sparse kinds over the P2P exchange: one warp waits for every peer's release of
-// flag slots [slot0, slot0 + n) at `epoch` before the consumer kernel reads
-static bpc_status launch_flag_wait(bpc_ctx* ctx, int slot0, uint32_t epoch, const char* what) {
+// exchange family `fam` (EP_PUSH / EP_PULL) at this rank's own epoch of it
+// (advanced by this rank's copy kernel) before the consumer kernel reads
+static bpc_status launch_flag_wait(bpc_ctx* ctx, int fam, const char* what) {
   P2PWait w = {};
+  const int slot0 = fam == EP_PUSH ? 0 : ctx->cfg.world_size;
   for (int r = 0; r < ctx->cfg.world_size; r++)
     if (r != ctx->cfg.rank) w.slots[w.nslots++] = slot0 + r;
   w.flags = ctx->d_xflags;
-  w.epoch = epoch;
+  w.st = ctx->d_st;
+  w.fam = fam;
   CK(launch_p2p_wait(w, ctx->stream), what);
   ctx->launches++;
   return BPC_OK;
@@ -995,10 +1161,8 @@ bpc_status bpc_server(bpc_ctx* ctx) {
     q.n_slices = ctx->n_sslices;
     q.partials = ctx->d_spartials;
     q.counters = ctx->d_scounters;
-    q.epoch = ++ctx->sepoch;
     q.n = (uint32_t)ctx->cfg.world_size;
     q.inv_n = 1.0 / (double)ctx->cfg.world_size;
-    q.t = ctx->t;
     q.rank = 0;
     q.stage = 1;
     q.seed = ctx->cfg.seed;
@@ -1010,34 +1174,29 @@ bpc_status bpc_server(bpc_ctx* ctx) {
     const uint32_t bb = ctx->cfg.comp.kind == BPC_SCALED_SIGN ? 1u : ctx->cfg.comp.bits;
     q.piece_stride = (uint32_t)round_up((uint64_t)kStreamSlice * bb / 8 + 32, 16);
     q.stage_payload = (uint64_t)q.piece_stride * q.n <= 49152 && ctx->cfg.world_size <= 32;
-    q.sync = peer_sync(ctx);
+    q.sync = peer_sync(ctx, EP_SERVER);
     if (fused_exchange(ctx)) {   // wait for every rank's push; p stays in the local P; signal
-      q.sync.wflags = ctx->d_xflags;
-      q.sync.wslot0 = 0;
-      q.sync.wepoch = ctx->push_epoch;
-      set_signal(ctx, &q.sync, 1, ++ctx->pull_epoch);
-      if (ctx->n_sslices == 0) {   // owns no chunk: nothing to read or send, only the signal
+      set_wait(ctx, &q.sync, EP_PUSH);
+      set_signal(ctx, &q.sync, EP_PULL);
+      if (ctx->n_sslices == 0) {   // owns no chunk: no server launch, only the signal
         P2PParams e = {};
-        for (int r = 0; r < ctx->cfg.world_size; r++)
-          if (r != ctx->cfg.rank) e.peer_flag[e.npeers++] = ctx->peer_flags[r];
-        e.slot = (int)q.sync.sslot;
-        e.epoch = q.sync.sepoch;
-        e.done = q.sync.done;
+        e.sync = peer_sync(ctx, EP_PULL);
+        set_signal(ctx, &e.sync, EP_PULL);
         CK(launch_p2p_copy(e, 1, ctx->stream), "pull signal launch");
+        ctx->launches++;
       }
     }
     CK(launch_stream_side(ctx, true, q), "server stream launch");
   } else {
     if (sparse_p2p(ctx)) {   // every rank's delta has landed in RECV
-      if (bpc_status st = launch_flag_wait(ctx, 0, ctx->push_epoch, "push wait launch")) return st;
+      if (bpc_status st = launch_flag_wait(ctx, EP_PUSH, "push wait launch")) return st;
     }
     SparseParams p = sparse_params(ctx, 1);
     p.recv = ctx->recv;
     p.slot_bytes = slot;
     p.vals = ctx->cfg.comp.use_ef ? ctx->etl : ctx->d_sdelta;
     p.out = ctx->pbuf;
-    CK(launch_sparse(ctx->cfg.comp.kind, p, 2 * ctx->num_sms, ctx->stream), "server sparse launch");
-    ctx->launches += 3;
+    if (bpc_status st = launch_sparse_side(ctx, p, nullptr)) return st;
   }
   timer_end(ctx, BPC_TIMER_SERVER, b);
   ctx->phase = 3;
@@ -1064,11 +1223,9 @@ bpc_status bpc_exchange_pull(bpc_ctx* ctx) {
           q.dst[q.njobs] = ctx->peer_p[r] + P.seg_off[rank];
           q.len[q.njobs++] = P.seg_bytes[rank];
         }
-        q.peer_flag[q.npeers++] = ctx->peer_flags[r];
       }
-      q.slot = n + rank;
-      q.epoch = ++ctx->pull_epoch;
-      q.done = ctx->d_xdone + 1;
+      q.sync = peer_sync(ctx, EP_PULL);
+      set_signal(ctx, &q.sync, EP_PULL);
       CK(launch_p2p_copy(q, ctx->pull_grid, ctx->stream), "pull copy launch");
       ctx->launches += 1;
     } else {
@@ -1113,28 +1270,27 @@ bpc_status bpc_step(bpc_ctx* ctx, float* d_params, float lr) {
   p.beta2 = c.beta2;
   p.omb1 = (float)(1.0 - (double)c.beta1);
   p.omb2 = (float)(1.0 - (double)c.beta2);
-  // bias corrections 1 - beta^t, fp64 then one rounding (R16); the kernels divide
-  p.bc1 = (float)(1.0 - std::pow((double)c.beta1, (double)ctx->t));
-  p.bc2 = (float)(1.0 - std::pow((double)c.beta2, (double)ctx->t));
-  p.ibc1 = 1.0f / p.bc1;   // RN(1 / bc): IEEE fp32 division on the host
-  p.ibc2 = 1.0f / p.bc2;
+  // bias corrections 1 - beta^t of the device's t, fp64 then one rounding (R16)
+  p.bias.bct = ctx->d_bct;
+  p.bias.nbct = ctx->nbct;
+  p.bias.conv = ctx->bconv;
+  p.bias.beta1 = (double)c.beta1;
+  p.bias.beta2 = (double)c.beta2;
   p.eps = c.eps;
   p.lr = lr;
   p.wd = c.weight_decay;
   p.bits = c.comp.bits;
   p.f16 = c.comp.f16_values;
   p.mu = c.momentum;
-  p.sync = peer_sync(ctx);
+  p.sync = peer_sync(ctx, EP_UPDATE);
   if (fused_exchange(ctx)) {   // wait for every owner's p, then read it from the owner's P
-    p.sync.wflags = ctx->d_xflags;
-    p.sync.wslot0 = (uint32_t)c.world_size;
-    p.sync.wepoch = ctx->pull_epoch;
+    set_wait(ctx, &p.sync, EP_PULL);
     for (int r = 0; r < c.world_size; r++) p.psrc[r] = ctx->peer_p[r];
   }
   cudaEvent_t b = nullptr;
   timer_begin(ctx, BPC_TIMER_UPDATE, &b);
   if (sparse_p2p(ctx)) {   // every owner's p has landed in P
-    if (bpc_status st = launch_flag_wait(ctx, c.world_size, ctx->pull_epoch, "pull wait launch")) return st;
+    if (bpc_status st = launch_flag_wait(ctx, EP_PULL, "pull wait launch")) return st;
   }
   const bool sparse = c.comp.kind == BPC_TOP_K || c.comp.kind == BPC_RANDOM_K;
   auto pass = [&](int mode) -> cudaError_t {
@@ -1156,14 +1312,15 @@ bpc_status bpc_step(bpc_ctx* ctx, float* d_params, float lr) {
     lc.alpha_l = c.lans_alpha_l;
     lc.alpha_u = c.lans_alpha_u;
     CK(launch_lans_coef(lc, ctx->stream), "LANS coefficient launch");
+    p.sync.inc_t = 1;   // the step's last launch advances t
     CK(pass(2), "LANS pass 2 launch");
     ctx->launches += 3;
   } else {
+    p.sync.inc_t = 1;
     CK(pass(c.optimizer == BPC_OPT_NAG ? 3 : 0), "update launch");
     ctx->launches++;
   }
   timer_end(ctx, BPC_TIMER_UPDATE, b);
-  ctx->t++;
   ctx->phase = 0;
   return BPC_OK;
 }
@@ -1268,6 +1425,16 @@ bpc_status bpc_load_state(bpc_ctx* ctx, int32_t which, const void* host_src, uin
   DeviceGuard dg(ctx->cfg.device);
   if (bytes != b) return BPC_ERR_SIZE_MISMATCH;
   CK(cudaStreamSynchronize(ctx->stream), "sync");
+  if (which == BPC_BUF_SERVER_ERR && !stream_worker(ctx->cfg.comp.kind) && b) {
+    // sparse kinds: the server reads Delta = fl32(0 + e~) as e~ itself, which holds
+    // for every e~ it writes (never -0); a loaded -0 is stored as the +0 it decodes to
+    std::vector<uint32_t> w(b / 4);
+    memcpy(w.data(), host_src, b);
+    for (auto& x : w)
+      if (x == 0x80000000u) x = 0;
+    CK(cudaMemcpy(p, w.data(), b, cudaMemcpyHostToDevice), "load state");
+    return BPC_OK;
+  }
   if (b) CK(cudaMemcpy(p, host_src, b, cudaMemcpyHostToDevice), "load state");
   return BPC_OK;
 }
@@ -1278,15 +1445,21 @@ bpc_status bpc_get_exchange(const bpc_ctx* ctx, int32_t* mode) {
   return BPC_OK;
 }
 
-bpc_status bpc_get_step(const bpc_ctx* ctx, uint32_t* t) {
-  if (!ctx || !t) return BPC_ERR_INVALID_ARGUMENT;
-  *t = ctx->t;
+// t lives on the device (DevState): read / written in the context's stream order
+bpc_status bpc_get_step(const bpc_ctx* cctx, uint32_t* t) {
+  if (!cctx || !t) return BPC_ERR_INVALID_ARGUMENT;
+  bpc_ctx* ctx = const_cast<bpc_ctx*>(cctx);   // error text only
+  DeviceGuard dg(ctx->cfg.device);
+  CK(cudaMemcpyAsync(t, &ctx->d_st->t, 4, cudaMemcpyDeviceToHost, ctx->stream), "step read");
+  CK(cudaStreamSynchronize(ctx->stream), "step read sync");
   return BPC_OK;
 }
 
 bpc_status bpc_set_step(bpc_ctx* ctx, uint32_t t) {
   if (!ctx || t < 1) return BPC_ERR_INVALID_ARGUMENT;
-  ctx->t = t;
+  DeviceGuard dg(ctx->cfg.device);
+  CK(cudaMemcpyAsync(&ctx->d_st->t, &t, 4, cudaMemcpyHostToDevice, ctx->stream), "step write");
+  CK(cudaStreamSynchronize(ctx->stream), "step write sync");
   return BPC_OK;
 }
 

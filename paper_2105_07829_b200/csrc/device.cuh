@@ -197,33 +197,58 @@ __device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long
   asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+// The step-varying values one launch uses, read from DevState when it starts
+// (after griddepcontrol.wait / stream order: the previous launches' last CTAs
+// have stored theirs)
+struct LaunchEp {
+  uint32_t E;      // this launch's epoch in its family
+  uint32_t Esig;   // the exchange epoch it releases (sig_fam)
+  uint32_t Ewait;  // the exchange epoch it waits for (wait_fam)
+  uint32_t t;      // the step counter
+};
+__device__ __forceinline__ LaunchEp launch_begin(const PeerSync& s) {
+  LaunchEp e;
+  e.t = s.st->t;
+  e.E = s.st->ep[s.fam] + 1;
+  e.Esig = s.sig_fam >= 0 ? s.st->ep[s.sig_fam] + 1 : 0u;
+  e.Ewait = s.wait_fam >= 0 ? s.st->ep[s.wait_fam] : 0u;
+  return e;
+}
 // One thread: wait until every other rank released this step's epoch, then
 // order the later bulk (async-proxy) reads of the exchanged bytes after it.
-__device__ __forceinline__ void peer_wait(const PeerSync& s) {
-  if (!s.wflags) return;
+__device__ __forceinline__ void peer_wait(const PeerSync& s, const LaunchEp& e) {
+  if (s.wait_fam < 0) return;
   for (uint32_t r = 0; r < s.n; r++) {
     if (r == s.self) continue;
     const unsigned long long* f = s.wflags + s.wslot0 + r;
     const long long t0 = clock64();
-    for (uint32_t it = 1; ld_relaxed_sys(f) < (unsigned long long)s.wepoch; it++) {
+    for (uint32_t it = 1; ld_relaxed_sys(f) < (unsigned long long)e.Ewait; it++) {
       __nanosleep(64);
       if ((it & 63) == 0 && clock64() - t0 > BPC_WATCHDOG_CYCLES)
-        watchdog_fire("peer flag", s.wslot0 + r, 0, ld_relaxed_sys(f), s.wepoch);
+        watchdog_fire("peer flag", s.wslot0 + r, 0, ld_relaxed_sys(f), e.Ewait);
     }
     (void)ld_acquire_sys(f);
   }
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
-// Every thread that stored exchanged bytes runs __threadfence_system(), then a
-// barrier over those threads, then this with `leader` = one of them: the last
-// CTA of the launch releases the epoch to every peer.
-__device__ __forceinline__ void peer_signal(const PeerSync& s, bool leader) {
-  if (!s.done || !leader) return;
-  const unsigned long long prev = atomicAdd(s.done, 1ull);
-  if (prev + 1 == (unsigned long long)s.sepoch * gridDim.x) {
+// One thread per CTA (`leader`), after the CTA's work -- for a signalling launch,
+// after every thread that stored exchanged bytes ran __threadfence_system() and
+// a barrier: the last CTA of the launch releases the exchange epoch to every
+// peer and stores the launch's epochs (and the next step counter) for the next
+// launches.
+__device__ __forceinline__ void launch_end(const PeerSync& s, const LaunchEp& e, bool leader) {
+  if (!leader) return;
+  const unsigned long long prev = atomicAdd(&s.st->done[s.fam], 1ull);
+  if (prev + 1 == (unsigned long long)gridDim.x) {   // the last CTA (the next launch of
+    s.st->done[s.fam] = 0ull;                        // the family runs after this grid)
     __threadfence_system();
-    for (uint32_t r = 0; r < s.n; r++)
-      if (s.sflag[r]) st_release_sys(s.sflag[r] + s.sslot, (unsigned long long)s.sepoch);
+    if (s.sig_fam >= 0) {
+      for (uint32_t r = 0; r < s.n; r++)
+        if (s.sflag[r]) st_release_sys(s.sflag[r] + s.sslot, (unsigned long long)e.Esig);
+      s.st->ep[s.sig_fam] = e.Esig;
+    }
+    s.st->ep[s.fam] = e.E;
+    if (s.inc_t) s.st->t = e.t + 1;
   }
 }
 
@@ -304,14 +329,15 @@ __device__ __forceinline__ float4 splat4(float a) { return make_float4(a, a, a, 
 __device__ __forceinline__ float4 fmul4s(float4 a, float4 b) {   // scalar products
   return make_float4(fmul(a.x, b.x), fmul(a.y, b.y), fmul(a.z, b.z), fmul(a.w, b.w));
 }
-__device__ __forceinline__ void adam4(float4 g, float4& m, float4& v, float4& x, const UpdateParams& p) {
+__device__ __forceinline__ void adam4(float4 g, float4& m, float4& v, float4& x, const UpdateParams& p,
+                                      const float4 bc) {   // bc = (bc1, bc2, 1/bc1, 1/bc2) of the step
   m = fadd4(fmul4s(splat4(p.beta1), m), fmul4s(splat4(p.omb1), g));                 // line 12
   v = fadd4(fmul4s(splat4(p.beta2), v), fmul4s(splat4(p.omb2), fmul4s(g, g)));      // line 13
   float4 r;
 #pragma unroll
   for (int u = 0; u < 4; u++) {
-    const float mh = divc(u == 0 ? m.x : u == 1 ? m.y : u == 2 ? m.z : m.w, p.bc1, p.ibc1);   // line 14
-    const float vh = divc(u == 0 ? v.x : u == 1 ? v.y : u == 2 ? v.z : v.w, p.bc2, p.ibc2);   // line 15
+    const float mh = divc(u == 0 ? m.x : u == 1 ? m.y : u == 2 ? m.z : m.w, bc.x, bc.z);   // line 14
+    const float vh = divc(u == 0 ? v.x : u == 1 ? v.y : u == 2 ? v.z : v.w, bc.y, bc.w);   // line 15
     const float ru = fdiv_pos(mh, fadd(fsqrt0(vh), p.eps));                                   // line 16
     if (u == 0) r.x = ru; else if (u == 1) r.y = ru; else if (u == 2) r.z = ru; else r.w = ru;
   }

@@ -9,18 +9,49 @@ namespace bpc {
 
 constexpr int P2P_MAXJ = 64;   // max world size of the peer-memory exchange
 
-// Fused NVLink exchange inside a streaming kernel (BPC_EXCHANGE_P2P):
-//  wait   - before its first load of exchanged bytes, the kernel waits until
-//           wflags[wslot0 + r] >= wepoch for every rank r != self (system-scope
-//           acquire of the producers' release);
-//  signal - after its last store, the last CTA releases sepoch into slot sslot
-//           of every peer's flag array (sflag[r], IPC-mapped; null for self).
+// Step-varying values of a context live in device memory: every kernel reads
+// the ones it needs when it starts, and the last CTA of a launch advances them.
+// No kernel parameter changes from step to step, so a CUDA graph of a step
+// replays correctly (any world size, fused exchange included).
+enum { EP_WORKER = 0, EP_SERVER = 1, EP_UPDATE = 2, EP_PUSH = 3, EP_PULL = 4 };
+struct DevState {
+  uint32_t t;                  // Alg. 5 step counter, >= 1
+  uint32_t ep[7];              // launch epochs per family (EP_*); push / pull = exchange epochs
+  unsigned long long done[8];  // per-family CTA arrivals of the running launch (the last CTA resets)
+};
+// Bias corrections of step t (R16): bct[t - 1] = (fl32(1 - b1^t), fl32(1 - b2^t),
+// RN(1 / bc1), RN(1 / bc2)) formed on the host in fp64; past nbct both are 1.0f
+// (conv = 1) or the table was capped (conv = 0: computed on the device)
+struct BiasTab {
+  const float4* bct;
+  uint32_t nbct;
+  int32_t conv;
+  double beta1, beta2;
+};
+__device__ __forceinline__ float4 bias_of(const BiasTab& b, uint32_t t) {
+  if (t <= b.nbct) return b.bct[t - 1];
+  if (b.conv) return make_float4(1.f, 1.f, 1.f, 1.f);
+  const float b1 = (float)(1.0 - pow(b.beta1, (double)t)), b2 = (float)(1.0 - pow(b.beta2, (double)t));
+  return make_float4(b1, b2, 1.f / b1, 1.f / b2);
+}
+
+// Launch bookkeeping and the fused NVLink exchange of one kernel launch:
+//  epoch  - E = st->ep[fam] + 1 for this launch; the last CTA (done counter
+//           reaching the grid size) stores it;
+//  wait   - wait_fam >= 0: before its first load of exchanged bytes the kernel
+//           waits until wflags[wslot0 + r] >= st->ep[wait_fam] for every rank
+//           r != self (system-scope acquire of the producers' release);
+//  signal - sig_fam >= 0: after its last store the last CTA releases
+//           st->ep[sig_fam] + 1 into slot sslot of every peer's flag array
+//           (sflag[r]; null for self) and stores it;
+//  inc_t  - the last CTA advances st->t (the step's final update launch).
 struct PeerSync {
-  const unsigned long long* wflags;   // null: no wait
-  uint32_t wslot0, wepoch;
-  unsigned long long* done;           // CTA counter (monotonic: sepoch * grid); null: no signal
+  DevState* st;
+  int32_t fam, wait_fam, sig_fam, inc_t;
+  const unsigned long long* wflags;
+  uint32_t wslot0;
   unsigned long long* sflag[P2P_MAXJ];
-  uint32_t sslot, sepoch;
+  uint32_t sslot;
   uint32_t n, self;
 };
 
@@ -54,8 +85,8 @@ struct UpdateParams {
   float* m;
   float* v;
   float* x;
-  float beta1, beta2, omb1, omb2, bc1, bc2, eps, lr, wd;   // bc = fl32(1 - beta^t), R16
-  float ibc1, ibc2;       // RN(1 / bc): the divisions by bc run as Markstein's correction (divc)
+  float beta1, beta2, omb1, omb2, eps, lr, wd;
+  BiasTab bias;           // bc = fl32(1 - beta^t) of the step (R16) and RN(1 / bc) (divc)
   uint32_t bits;
   int32_t mode;           // 0 Adam core; LANS (R22): 1 = pass 1 (m, v, block sums), 2 = pass 2 (x);
                           // 3 NAG (R24, velocity in m)
@@ -89,11 +120,11 @@ struct StreamParams {
   const Slice* slices;
   uint32_t n_slices;
   double* partials;       // per-slice tree partials of multi-slice units
-  unsigned long long* counters;   // per-unit published-slice counters (monotonic)
-  uint32_t epoch;         // launch number: a unit is complete at epoch * nslices
+  unsigned long long* counters;   // per-unit published-slice counters (monotonic: a unit is
+                                  // complete at E x nslices, E = this launch's epoch)
   uint32_t n;
   double inv_n;
-  uint32_t t, rank, stage;
+  uint32_t rank, stage;
   uint64_t seed;
   uint32_t bits;
   int32_t use_ef, check_finite;
@@ -115,9 +146,15 @@ struct StreamParams {
   uint8_t* dst[P2P_MAXJ];
   uint32_t ndst;
   PeerSync sync;
+  // sparse kinds (top-k, random-k): this side's candidate lists (kernels_sparse.cu)
+  const uint32_t* sp_chunk2u;
+  const uint32_t* sp_guess;
+  uint32_t* sp_scnt;          // candidates per slice (of this side's slice table)
+  uint32_t* sp_cand;          // unit u's list at sp_cand_off[u]: one sub-list of (cap / nslices) per slice
+  const uint32_t* sp_cand_off;
 };
 
-// sparse kinds (kernels_sparse.cu): guess -> stream -> select, per side
+// sparse kinds (kernels_sparse.cu): prep -> streaming pass (kernels_cstream.cu) -> select, per side
 struct SparseParams {
   const float* grad;        // worker: g (flat)
   float* vals;              // worker: e (flat; use_ef); server: e~ (use_ef) or the Delta scratch
@@ -132,25 +169,44 @@ struct SparseParams {
   uint32_t n_slices;
   const uint32_t* chunk2u;  // chunk -> unit index of this side
   uint32_t* guess;          // [n_units] candidate thresholds
-  uint32_t* cnt;            // [n_units] candidate counters (the select kernel resets them)
-  uint32_t* cand;           // candidate indices, unit u at [cand_off[u], cand_off[u + 1])
+  uint32_t* scnt;           // candidates per slice of this side's slice table (written by the streaming pass)
+  uint32_t* cand;           // candidate indices, unit u at [cand_off[u], cand_off[u + 1]): slice s of
+                            // the unit owns the index-ordered sub-list [s cs, s cs + min(scnt, cs)),
+                            // cs = (cand_off[u + 1] - cand_off[u]) / nslices
   const uint32_t* cand_off; // [n_units + 1]
+  const uint32_t* first_slice;  // [n_units] the unit's first slice in this side's slice table
   uint32_t n;
   double inv_n;
-  uint32_t t, stage, rrank;  // Philox counter words (R13): stage 0 push (rank), 1 pull (0)
+  const DevState* st;        // the step counter t (Philox counter word 2, R13)
+  uint32_t stage, rrank;     // Philox counter words (R13): stage 0 push (rank), 1 pull (0)
   uint64_t seed;
   int32_t server, randk_scaled, use_ef, f16, check_finite;
   unsigned int* flag;
   uint32_t sel_cap;         // CTA select kernel: candidates held in shared memory, a power of two <= SEL_CAP
   uint32_t* big;            // [n_units] units the warp select hands to the CTA select (it resets them)
+  const uint2* apply_blk;   // server: (unit, first entry) of each 256-entry block of the ranks' entries
+  uint32_t n_apply_blk;
+  // per-tensor units longer than SEL_LMAX (the large path)
+  const uint32_t* large_units;   // [n_large] unit indices
+  uint32_t n_large;
+  const uint2* lslices;          // (slice index, large unit) of every slice of the large units, by unit
+  uint32_t n_lslices;
+  const uint32_t* lslice_first;  // [n_large + 1]
+  uint32_t* lstate;              // [8 n_large] radix-select state
+  uint32_t* lhist;               // [256 n_large]
+  uint2* lcnt;                   // [n_lslices] (keys > T, keys == T)
+  uint2* loff;                   // [n_lslices] (first output position, T-ties before)
+  uint32_t large_grid;
 };
 constexpr uint32_t SEL_CAP = 16384;     // max candidates a select CTA holds in shared memory
+constexpr uint32_t SEL_LMAX = 1u << 18; // longer units (per-tensor) take the large-unit path
 // the sample rank of the top-k guess (host: capacity; device: the guess)
 __host__ __device__ inline uint32_t sparse_sample_rank(uint32_t k, uint32_t L) {
   const double mu = (double)k * 4096.0 / (double)L;
   return (uint32_t)ceil(mu + 3.0 * sqrt(mu) + 6.0);
 }
-cudaError_t launch_sparse(int kind, const SparseParams& p, int grid, cudaStream_t s);
+cudaError_t launch_sparse_prep(int kind, const SparseParams& p, cudaStream_t s);
+cudaError_t launch_sparse_select(int kind, const SparseParams& p, cudaStream_t s);
 size_t sparse_select_smem(uint32_t sel_cap);
 
 // peer-memory exchange (kernels_p2p.cu)
@@ -159,17 +215,14 @@ struct P2PParams {
   uint8_t* dst[P2P_MAXJ];           // local or a peer's IPC-mapped buffer
   uint64_t len[P2P_MAXJ];           // bytes, multiples of 16
   int njobs;
-  unsigned long long* peer_flag[P2P_MAXJ];   // peers' flag arrays (IPC-mapped)
-  int npeers;
-  int slot;                         // flag slot this launch releases on every peer
-  uint32_t epoch;
-  unsigned long long* done;         // local CTA counter (monotonic: epoch * grid)
+  PeerSync sync;                    // fam = sig_fam = EP_PUSH / EP_PULL: the copy's epoch, released to the peers
 };
 struct P2PWait {
   const unsigned long long* flags;  // this rank's flag array
   int slots[P2P_MAXJ];
   int nslots;
-  uint32_t epoch;
+  const DevState* st;               // wait until every slot >= st->ep[fam]
+  int fam;
 };
 
 // LANS block coefficients (R22): one CTA per block reduces its tiles' partial

@@ -49,7 +49,7 @@
 
 namespace bpc {
 
-enum { C_NONE = 0, C_SIGN = 2, C_LDITHER = 5, C_NDITHER = 6 };
+enum { C_NONE = 0, C_SIGN = 2, C_TOPK = 3, C_RANDK = 4, C_LDITHER = 5, C_NDITHER = 6 };
 
 constexpr int CCW = 16;                  // consumer warps
 constexpr int CCNT = 32 * CCW;           // consumer threads
@@ -80,6 +80,8 @@ struct CDesc {
   uint32_t pofs;       // server: byte offset of the slice's first field inside a staged piece
   uint32_t staged;     // server: payload pieces staged in smem
   uint32_t owner;      // server rank of the chunk (worker: fused push destination)
+  uint32_t gsl;        // the slice's index in this side's slice table
+  uint32_t sp_u, sp_g, sp_cs;   // sparse kinds: unit index, candidate threshold, sub-list capacity
 };
 
 struct __align__(128) CHead {
@@ -88,6 +90,7 @@ struct __align__(128) CHead {
   uint64_t pfin;            // fused exchange: the producer's last bulk store has completed
   CDesc desc[CMAXH];
   double red[2][CCW];       // the consumer warps' 512-element subtrees of a slice
+  uint32_t wcnt[2 * CCW];   // sparse kinds: candidates per consumer warp of the emitting slice (2 buffers)
   double part[CMAXH];
   double total[CMAXH];
 };
@@ -243,7 +246,12 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
   const uint32_t G = gridDim.x;
   const uint32_t mine = p.n_slices > blockIdx.x ? (p.n_slices - blockIdx.x + G - 1) / G : 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int b = KIND == C_SIGN ? 1 : (BITS ? BITS : (int)p.bits);   // bits per element in the payload stream
+  // SPARSE (top-k, random-k; kernels_sparse.cu brackets this launch): the
+  // streaming pass of a compressed unit computes q (worker) / reads Delta
+  // (server) and lists the candidates with key >= G_u; the exact selection and
+  // the payload follow in sparse_select
+  constexpr bool SPARSE = KIND == C_TOPK || KIND == C_RANDK;
+  const int b = (KIND == C_SIGN || SPARSE) ? 1 : (BITS ? BITS : (int)p.bits);   // bits per element in the payload stream
   if (threadIdx.x == 0) {
     for (uint32_t s = 0; s < NH; s++) {
       mbar_init(&hd.emptyH[s], CCW);
@@ -259,11 +267,12 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
   }
   __syncthreads();
   pdl_wait_and_release();
+  const LaunchEp ep = launch_begin(p.sync);   // this launch's epoch, the step counter t
 
   // ===================================================== producer
   if (warp == CPROD) {
     if (lane == 0) {
-      if (SERVER && FUSED) peer_wait(p.sync);   // fused exchange: every rank's delta has landed in RECV
+      if (SERVER && FUSED) peer_wait(p.sync, ep);   // fused exchange: every rank's delta has landed in RECV
       // write-back of emitted slice ie (its held stage): the error e / e~, or a raw
       // unit's payload (worker: g; server: the mean), 16-byte-aligned part
       auto flush = [&](uint32_t ie) {
@@ -277,7 +286,7 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
         if (o.nslices == 0) {
           uint8_t* pay = (!SERVER && FUSED) ? p.dst[o.owner] + o.recv : p.out + o.pay;
           dst = pay + 4ull * o.start;
-        } else if (p.use_ef) {
+        } else if (p.use_ef && !(SPARSE && SERVER)) {   // the sparse server only reads Delta
           dst = reinterpret_cast<uint8_t*>(p.err + (SERVER ? o.etl : o.off) + o.start);
         }
         if (dst) bulk_store(dst, H(hs), nvb);
@@ -314,12 +323,20 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
         d.pofs = 0;
         d.staged = 0;
         d.owner = c.owner;
+        d.gsl = blockIdx.x + i * G;
+        if (SPARSE && sl.nslices) {
+          d.sp_u = p.sp_chunk2u[sl.chunk];
+          d.sp_g = p.sp_guess[d.sp_u];
+          d.sp_cs = (p.sp_cand_off[d.sp_u + 1] - p.sp_cand_off[d.sp_u]) / sl.nslices;   // per-slice sub-list
+        }
         const uint32_t nvb = (sl.len & ~3u) * 4u;
         const bool comp = sl.nslices > 0;
         uint32_t tx = 0;
         uint64_t a0 = 0, a1 = 0;
         if (!SERVER) {
           tx = (p.use_ef && comp) ? 2 * nvb : nvb;
+        } else if (comp && SPARSE) {
+          tx = nvb;         // Delta (e~ + the applied entries, or the scratch) lands in the held stage
         } else if (comp) {
           const uint64_t s0 = 4 + (uint64_t)sl.start * b / 8;
           const uint64_t e0 = 4 + ((uint64_t)(sl.start + sl.len) * b + 7) / 8;
@@ -342,6 +359,8 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
           }
         } else if (!comp) {
           if (nvb) tma_load_1d(H(hs), p.recv + c.recv + 4ull * sl.start, nvb, &hd.fullI[t]);
+        } else if (SPARSE) {
+          if (nvb) tma_load_1d(H(hs), p.err + c.etl + sl.start, nvb, &hd.fullI[t]);
         } else {
           if (p.use_ef && nvb) tma_load_1d(H(hs), p.err + c.etl + sl.start, nvb, &hd.fullI[t]);
           for (uint32_t r = 0; r < p.n; r++)
@@ -367,6 +386,7 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
 
   // ===================================================== reducers
   if (warp >= CRED) {
+    if (SPARSE) return;   // no unit norm: the emit does not wait for a total
     for (uint32_t i = warp - CRED; i < mine; i += CRW) {
       const uint32_t hs = i % NH;
       // slice i produced.  Cannot alias: slice i + NH needs stage hs back, which
@@ -374,7 +394,7 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
       // the emit of slice i runs D slices later: a 1 us poll costs it nothing and
       // keeps the waiting warps off the issue slots the consumers need
       mbar_wait_backoff(&hd.pready[hs], (i / NH) & 1, 1000, 0x2000000u | i);
-      const uint32_t ns = hd.desc[hs].nslices;
+      const uint32_t ns = SPARSE ? 0u : hd.desc[hs].nslices;   // sparse kinds: no unit norm
       if (ns > 1 && p.pass == 1) {   // per-tensor units, pass 1: publish the partial only
         if (lane == 0) p.partials[hd.desc[hs].unit_first + hd.desc[hs].sidx] = hd.part[hs];
       } else if (ns > 1 && p.pass == 2) {   // pass 2: the unit's total from unit_tree_kernel
@@ -385,7 +405,7 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
           const CDesc& d = hd.desc[hs];
           p.partials[d.unit_first + d.sidx] = hd.part[hs];
           red_release_add(p.counters + d.unit, 1ull);
-          wait_counter(p.counters + d.unit, (unsigned long long)p.epoch * ns, 0x3000000u | i);
+          wait_counter(p.counters + d.unit, (unsigned long long)ep.E * ns, 0x3000000u | i);
         }
         __syncwarp();
         // unit total: pairwise tree over its slices, zero-padded to CUNITSL (R6)
@@ -482,6 +502,11 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
         } else {
           q = g4;
         }
+      } else if (SPARSE && comp && any) {
+        // Delta as sparse_apply left it (e~ + the ranks' entries; Delta = fl32(0 + e~)
+        // = e~ elsewhere: e~ never holds -0, bpc_load_state stores -0 as +0)
+        q = inv4 ? val[f] : load4_masked(p.err + d.etl, j, d.L);
+        wr = !inv4;
       } else if (any) {
         wr = true;
         if (!comp) {   // raw unit: mean of the ranks' fp32 values (rank 0's staged in val)
@@ -566,9 +591,9 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
         }
       }
       if (wr) val[f] = q;
-      lv[s] = comp ? (KIND == C_SIGN ? leaf4_abs(q) : leaf4_sq(q)) : 0.0;
+      lv[s] = (comp && !SPARSE) ? (KIND == C_SIGN ? leaf4_abs(q) : leaf4_sq(q)) : 0.0;
     }
-    if (comp) {
+    if (comp && !SPARSE) {
       // the lane's 16-element subtree: groups (0, 1) and (2, 3) pair up; in step
       // order that is (s0, s1), (s2, s3) for an even rotation and (s3, s0),
       // (s1, s2) for an odd one (IEEE + is commutative)
@@ -596,7 +621,65 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
       return;
     }
     float* errp = p.use_ef ? (SERVER ? p.err + d.etl : p.err + d.off) : nullptr;
-    if (KIND == C_SIGN) {
+    if (SPARSE) {
+      // the unit's candidates: key >= G_u (top-k |q| bits, R9; random-k the
+      // complemented Philox word, R10), in index order into this slice's own
+      // sub-list of the unit's list (lanes own contiguous elements: a scan of the
+      // lanes' counts in lane order is the index order) + the slice's count.
+      // q stays in the held stage: it is the worker's new e (bulk-stored)
+      const uint32_t u = d.sp_u, G = d.sp_g;
+      uint32_t mask = 0;   // bit 4 k + e: element 16 lq + 4 k + e of the slice
+#pragma unroll
+      for (int s = 0; s < 4; s++) {
+        const uint32_t k = (s + rot) & 3u;
+        const uint32_t f = lf + k;
+        const uint32_t j = d.start + 4 * f;
+        if (!(FULL || 4 * f < d.len)) continue;
+        const float4 q = val[f];
+        if (!SERVER && errp && !FULL && f >= (d.len >> 2)) store4_masked(errp, j, L, q);   // ragged: not bulk-stored
+        uint4 key;
+        if (KIND == C_TOPK) {
+          key = make_uint4(__float_as_uint(q.x) & 0x7fffffffu, __float_as_uint(q.y) & 0x7fffffffu,
+                           __float_as_uint(q.z) & 0x7fffffffu, __float_as_uint(q.w) & 0x7fffffffu);
+        } else {
+          const uint4 w = philox4x32_10_rk(make_uint4(j >> 2, d.id, ep.t, (stage_id << 31) | rng_rank), p.rk);
+          key = make_uint4(~w.x, ~w.y, ~w.z, ~w.w);
+        }
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          const uint32_t ke = e == 0 ? key.x : e == 1 ? key.y : e == 2 ? key.z : key.w;
+          if (ke >= G && (FULL || j + e < L)) mask |= 1u << (4 * k + e);
+        }
+      }
+      const uint32_t cnt = __popc(mask);
+      uint32_t incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      uint32_t* wc = hd.wcnt + CCW * (d.gsl & 1);   // double-buffered: one barrier per slice
+      if (lane == 31) wc[warp] = incl;
+      cons_sync();
+      uint32_t wi = lane < CCW ? wc[lane] : 0u;   // warps' counts: inclusive scan over 16 lanes
+#pragma unroll
+      for (int o = 1; o < CCW; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += y;
+      }
+      const uint32_t wbefore = warp ? __shfl_sync(0xffffffffu, wi, warp - 1) : 0u;
+      const uint32_t total = __shfl_sync(0xffffffffu, wi, CCW - 1);
+      uint32_t before = incl - cnt + wbefore;
+      // sub-list of slice sidx: cs entries at cand_off[u] + sidx cs
+      const uint32_t cs = d.sp_cs;
+      uint32_t* sub = p.sp_cand + p.sp_cand_off[u] + d.sidx * cs;
+      const uint32_t j0 = d.start + 16 * lq;
+      for (uint32_t m = mask; m; m &= m - 1) {
+        if (before < cs) sub[before] = j0 + (uint32_t)(__ffs(m) - 1);
+        before++;
+      }
+      if (threadIdx.x == 0) p.sp_scnt[d.gsl] = total;   // > cs: the list overflowed
+    } else if (KIND == C_SIGN) {
       const float sc = __double2float_rn(total / (double)L);
       const float nsc = -sc;
       uint32_t m16 = 0;
@@ -640,7 +723,7 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
         const uint32_t j = d.start + 4 * f;
         if (!(FULL || 4 * f < d.len)) continue;
         const float4 q = val[f];
-        const uint4 w4 = philox4x32_10_rk(make_uint4(j >> 2, d.id, p.t, (stage_id << 31) | rng_rank), p.rk);
+        const uint4 w4 = philox4x32_10_rk(make_uint4(j >> 2, d.id, ep.t, (stage_id << 31) | rng_rank), p.rk);
         uint32_t g = 0, codes[4];
 #pragma unroll
         for (int u = 0; u < 4; u++) {
@@ -686,20 +769,32 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
     }
   };
 
+  // ring positions as running counters (no division by the run-time NH per slice):
+  // produce slice i in held stage ph (phase bit phb), input stage pt (phase ptb);
+  // emit slice i - D in held stage eh (phase ehb)
+  uint32_t ph = 0, phb = 0, pt = 0, ptb = 0, eh = 0, ehb = 0;
   for (uint32_t i = 0; i < mine + D; i++) {
     // ---------------- produce slice i
     if (i < mine) {
-      const uint32_t hs = i % NH, t = i % CNI;
-      mbar_wait(&hd.fullI[t], (i / CNI) & 1, 0x4000000u | i);
+      const uint32_t hs = ph, t = pt;
+      mbar_wait(&hd.fullI[t], ptb, 0x4000000u | i);
       const CDesc d = hd.desc[hs];
       const bool comp = d.nslices > 0;
       if (d.len == CSL) produce(BoolC<true>{}, i, t, d, H(hs), comp);
       else produce(BoolC<false>{}, i, t, d, H(hs), comp);
       __syncwarp();
       if (lane == 0) mbar_arrive1(&hd.emptyI[t]);   // input stage consumed by this warp
-      cons_sync();                                    // all q written, red complete
-      if (warp == 0) {
-        if (comp) {   // the slice partial: pairwise tree over the 16 warp subtrees
+      if (++pt == (uint32_t)CNI) {
+        pt = 0;
+        ptb ^= 1;
+      }
+      if (++ph == NH) {
+        ph = 0;
+        phb ^= 1;
+      }
+      if (!SPARSE) cons_sync();                       // all q written, red complete
+      if (warp == 0 && !SPARSE) {
+        if (comp && !SPARSE) {   // the slice partial: pairwise tree over the 16 warp subtrees
           double r = lane < CCW ? hd.red[i & 1][lane] : 0.0;
 #pragma unroll
           for (int m = 1; m < CCW; m <<= 1) r = r + __shfl_xor_sync(0xffffffffu, r, m);
@@ -711,14 +806,14 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
     // ---------------- emit slice i - D
     if (i >= D) {
       const uint32_t ie = i - D;
-      const uint32_t hs = ie % NH;
+      const uint32_t hs = eh;
       const CDesc d = hd.desc[hs];
       // payload destination: worker -> the owner's RECV slot (fused push) or SEND;
       // server -> the local P
       uint8_t* const pay = (!SERVER && FUSED) ? p.dst[d.owner] + d.recv : p.out + d.pay;
       // every slice (raw included) waits for its reducer before the stage is
       // recycled: keeps each mbarrier at most one phase ahead of its waiters
-      mbar_wait(&hd.tready[hs], (ie / NH) & 1, 0x5000000u | ie);
+      if (!SPARSE) mbar_wait(&hd.tready[hs], ehb, 0x5000000u | ie);
       const double total = hd.total[hs];
       if (p.pass == 1) {
         // per-tensor units, pass 1: nothing to emit (pass 2 re-produces the slice)
@@ -730,15 +825,19 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
       fence_proxy_async();   // this thread's smem writes before the producer's bulk store
       __syncwarp();
       if (lane == 0) mbar_arrive1(&hd.emptyH[hs]);   // this warp is done with held stage hs
+      if (++eh == NH) {
+        eh = 0;
+        ehb ^= 1;
+      }
     }
   }
   if (bad) atomicOr(p.flag, 1u);
-  if (FUSED && p.pass != 1) {   // fused exchange: release this step's payload bytes to the peers
-    __threadfence_system();
-    cons_sync();
-    if (threadIdx.x == 0) mbar_wait(&hd.pfin, 0, 0x6000000u);   // the producer's raw stores landed
-    peer_signal(p.sync, threadIdx.x == 0);
-  }
+  // fused exchange: this step's payload bytes are released to the peers by the
+  // launch's last CTA; every launch stores its epoch there
+  if (FUSED && p.pass != 1) __threadfence_system();
+  cons_sync();
+  if (threadIdx.x == 0 && FUSED && p.pass != 1) mbar_wait(&hd.pfin, 0, 0x6000000u);   // the producer's raw stores landed
+  launch_end(p.sync, ep, threadIdx.x == 0);
 }
 
 // ring geometry for a launch: input-stage size and layout, number of held stages
@@ -788,7 +887,7 @@ static cudaError_t launch_cstream_t(int kind, StreamParams p, int grid, cudaStre
     cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, fn, p);
   };
-  const bool fused = p.ndst > 0 || p.sync.wflags != nullptr;
+  const bool fused = p.ndst > 0 || p.sync.wait_fam >= 0;
   auto dither = [&](auto kind_tag) -> cudaError_t {
     constexpr int K = decltype(kind_tag)::value;
     switch (p.bits) {
@@ -801,6 +900,8 @@ static cudaError_t launch_cstream_t(int kind, StreamParams p, int grid, cudaStre
   switch (kind) {
     case C_NONE: return fused ? go(cstream_kernel<C_NONE, SERVER, true, 0>) : go(cstream_kernel<C_NONE, SERVER, false, 0>);
     case C_SIGN: return fused ? go(cstream_kernel<C_SIGN, SERVER, true, 0>) : go(cstream_kernel<C_SIGN, SERVER, false, 0>);
+    case C_TOPK: return go(cstream_kernel<C_TOPK, SERVER, false, 0>);     // sparse: no fused exchange
+    case C_RANDK: return go(cstream_kernel<C_RANDK, SERVER, false, 0>);
     case C_LDITHER: return dither(std::integral_constant<int, C_LDITHER>{});
     case C_NDITHER: return dither(std::integral_constant<int, C_NDITHER>{});
   }

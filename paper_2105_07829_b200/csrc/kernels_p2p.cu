@@ -13,6 +13,7 @@ namespace bpc {
 // grid strides over all jobs' 16-byte words; afterwards the last CTA to finish
 // releases `epoch` into flag slot `slot` of every peer.
 __global__ void __launch_bounds__(512) p2p_copy_signal(const __grid_constant__ P2PParams p) {
+  const LaunchEp ep = launch_begin(p.sync);   // fam = sig_fam: the exchange epoch of this copy
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t g0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   for (int jb = 0; jb < p.njobs; jb++) {
@@ -30,28 +31,23 @@ __global__ void __launch_bounds__(512) p2p_copy_signal(const __grid_constant__ P
     }
     for (; w < nw; w += stride) d[w] = __ldg(s + w);
   }
-  // make this CTA's peer stores visible system-wide, then count CTAs
+  // make this CTA's peer stores visible system-wide; the last CTA releases the epoch
   __threadfence_system();
   __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned long long prev = atomicAdd(p.done, 1ull);
-    if (prev + 1 == (unsigned long long)p.epoch * gridDim.x) {   // last CTA of this launch
-      __threadfence_system();
-      for (int r = 0; r < p.npeers; r++) st_release_sys(p.peer_flag[r] + p.slot, (unsigned long long)p.epoch);
-    }
-  }
+  launch_end(p.sync, ep, threadIdx.x == 0);
 }
 
-// One warp waits until flags[i] >= epoch for every listed slot.
+// One warp waits until flags[i] >= the epoch of family `fam` for every listed slot.
 __global__ void p2p_wait(const __grid_constant__ P2PWait w) {
   const int lane = threadIdx.x;
+  const unsigned long long epoch = w.st->ep[w.fam];
   for (int i = lane; i < w.nslots; i += 32) {
     const unsigned long long* f = w.flags + w.slots[i];
     const long long t0 = clock64();
-    for (uint32_t it = 1; ld_relaxed_sys(f) < (unsigned long long)w.epoch; it++) {
+    for (uint32_t it = 1; ld_relaxed_sys(f) < epoch; it++) {
       __nanosleep(100);
       if ((it & 63) == 0 && clock64() - t0 > BPC_WATCHDOG_CYCLES)
-        watchdog_fire("p2p flag", (uint32_t)w.slots[i], 0, ld_relaxed_sys(f), (unsigned long long)w.epoch);
+        watchdog_fire("p2p flag", (uint32_t)w.slots[i], 0, ld_relaxed_sys(f), epoch);
     }
     (void)ld_acquire_sys(f);
   }

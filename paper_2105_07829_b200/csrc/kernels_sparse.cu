@@ -12,12 +12,12 @@
 //                  mu = k S / L; random-k: the uniform keys' quantile
 //                  1 - (k + 8 sqrt(k) + 64) / L).  G only decides which elements
 //                  are examined exactly; any G gives the same result.
-//   sparse_dense   persistent CTAs over 2^13-element slices, HBM streaming.
-//                  Worker: q = g + e (Alg. 4 l.5), e := q (use_ef),
-//                  raw units copied.  Server: reads Delta (e~ + the applied
-//                  entries; 4 B/element), raw units averaged.  Every element
-//                  with key >= G_u joins the unit's candidate list (gathered per
-//                  slice in shared memory, one global append per slice).
+//   streaming     cstream_kernel<C_TOPK / C_RANDK> (kernels_cstream.cu): the TMA
+//                  pipeline of the norm kinds.  Worker: q = g + e (Alg. 4 l.5,
+//                  PAPER.md:241), e := q (bulk store), raw units copied.  Server:
+//                  reads Delta (e~ + the applied entries; 4 B/element), raw units
+//                  averaged.  Every element with key >= G_u joins the unit's
+//                  candidate list (gathered per slice, one global append).
 //   sparse_select  if the unit has k <= c <= cap candidates, every element
 //                  outside them has key < G <= T (the k-th largest key), so the
 //                  exact selection (keys desc, index asc, R9/R10) is a radix
@@ -36,20 +36,19 @@ enum { SP_TOPK = 3, SP_RANDK = 4 };
 
 constexpr int SG_NT = 256;        // prep kernel threads
 constexpr int SG_S = 4096;        // sample size (16 runs of 256)
-constexpr int SS_NT = 512;        // dense kernel threads (16 elements per thread per slice)
-constexpr int SS_CAND = 1024;     // candidates a dense CTA gathers per slice before one global append
 constexpr int SE_NT = 512;        // CTA select kernel threads
 constexpr int SW_WARPS = 4;       // warp select: units (warps) per CTA
 constexpr uint32_t SW_CAP = 4096; // warp select: max candidates
 constexpr uint32_t SW_KMAX = 512; // warp select: max k
-constexpr int PREP_IDX = 4096;    // server prep: rank index entries staged in shared memory
+constexpr int SA_NT = 256;        // server apply: entries per block
 
 __device__ __forceinline__ uint32_t topk_key(float v) { return __float_as_uint(v) & 0x7fffffffu; }
 template <int KIND>
 __device__ __forceinline__ uint32_t sel_key(float v, uint32_t j, const SparseParams& p, uint32_t id) {
   if (KIND == SP_TOPK) return topk_key(v);
-  // random-k: the k smallest Philox words = the k largest complements (R10)
-  const uint4 w = rng4(p.seed, j >> 2, id, p.t, p.stage, p.rrank);
+  // random-k: the k smallest Philox words = the k largest complements (R10); t is
+  // the step counter in device memory (read-only in these kernels, L1-resident)
+  const uint4 w = rng4(p.seed, j >> 2, id, p.st->t, p.stage, p.rrank);
   const uint32_t u = j & 3u;
   return ~(u == 0 ? w.x : (u == 1 ? w.y : (u == 2 ? w.z : w.w)));
 }
@@ -106,27 +105,6 @@ __device__ __forceinline__ uint2 warp_find_bin256(const uint32_t* hist, uint32_t
   return make_uint2(__shfl_sync(0xffffffffu, bin, src), __shfl_sync(0xffffffffu, ab, src));
 }
 
-// ascending bitonic sort of a[0, n) in shared memory, n a power of two, by
-// `nt` threads (tid in [0, nt)); `sync` orders the stages
-template <class Sync>
-__device__ __forceinline__ void bitonic_sort(uint32_t* a, uint32_t n, uint32_t tid, uint32_t nt, Sync sync) {
-  for (uint32_t size = 2; size <= n; size <<= 1) {
-    for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-      for (uint32_t i = tid; i < n / 2; i += nt) {
-        const uint32_t lo = 2 * i - (i & (stride - 1));
-        const uint32_t hi = lo + stride;
-        const bool up = (lo & size) == 0;
-        const uint32_t x = a[lo], y = a[hi];
-        if ((x > y) == up) {
-          a[lo] = y;
-          a[hi] = x;
-        }
-      }
-      sync();
-    }
-  }
-}
-
 template <int NT>
 __device__ __forceinline__ uint32_t block_excl_scan_u32(uint32_t v, uint32_t* scan, uint32_t* total) {
   constexpr int NW = NT / 32;
@@ -176,61 +154,43 @@ __device__ __forceinline__ const uint8_t* rank_payload(const SparseParams& p, co
 }
 
 // ================================================================ prep
+// server: the ranks' entries, one thread per entry; block b covers entries
+// [first, first + 256) of unit apply_blk[b].x's n k entries (rank-major)
+template <int KIND>
+__global__ void __launch_bounds__(SA_NT) sparse_apply_kernel(const __grid_constant__ SparseParams p) {
+  const uint2 blk = p.apply_blk[blockIdx.x];
+  const uint32_t u = blk.x;
+  const DevChunk c = p.chunks[p.items[u]];
+  const uint32_t k = c.k, n = p.n;
+  float* V = const_cast<float*>(unit_values(p, c));
+  const uint32_t i = blk.y + threadIdx.x;
+  if (i >= n * k) return;
+  const uint32_t r = i / k, e = i - r * k;
+  auto idx_of = [&](uint32_t rr) { return reinterpret_cast<const uint32_t*>(rank_payload(p, c, rr) + 8); };
+  const uint32_t j = idx_of(r)[e];
+  // the first rank holding j sums every holder in rank order (R5)
+  uint32_t pos;
+  for (uint32_t r2 = 0; r2 < r; r2++)
+    if (holds(idx_of(r2), k, j, &pos)) return;
+  double acc = 0.0;
+  acc += (double)get_val(rank_payload(p, c, r) + 8 + 4ull * k, e, p.f16);
+  for (uint32_t r2 = r + 1; r2 < n; r2++)
+    if (holds(idx_of(r2), k, j, &pos)) acc += (double)get_val(rank_payload(p, c, r2) + 8 + 4ull * k, pos, p.f16);
+  V[j] = mean_plus(acc, p.inv_n, (double)V[j]);   // no EF: V is the zeroed scratch
+}
+
+// the candidate threshold of each unit
 template <int KIND>
 __global__ void __launch_bounds__(SG_NT) sparse_prep_kernel(const __grid_constant__ SparseParams p) {
-  __shared__ uint32_t sidx[PREP_IDX];   // server: the ranks' index lists, when they fit
   __shared__ uint32_t red[SG_NT / 32];
-  __shared__ uint32_t scnt;
   const uint32_t u = blockIdx.x;
   const DevChunk c = p.chunks[p.items[u]];
   const uint32_t L = c.len, k = c.k;
   float* V = const_cast<float*>(unit_values(p, c));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const bool topk_noef_server = KIND == SP_TOPK && p.server && !p.use_ef;
-  // ---- server: Delta_j at the ranks' entries (rank order, fp64, R5)
-  if (p.server) {
-    const uint32_t n = p.n;
-    const bool staged = (uint64_t)n * k <= (uint64_t)PREP_IDX;
-    if (staged) {
-      for (uint32_t i = threadIdx.x; i < n * k; i += SG_NT) {
-        const uint32_t r = i / k, e = i - r * k;
-        sidx[i] = reinterpret_cast<const uint32_t*>(rank_payload(p, c, r) + 8)[e];
-      }
-    }
-    if (threadIdx.x == 0) scnt = 0;
-    __syncthreads();
-    auto idx_of = [&](uint32_t r) -> const uint32_t* {
-      return staged ? sidx + r * k : reinterpret_cast<const uint32_t*>(rank_payload(p, c, r) + 8);
-    };
-    uint32_t* cand = p.cand + p.cand_off[u];
-    const uint32_t cap = p.cand_off[u + 1] - p.cand_off[u];
-    for (uint32_t i = threadIdx.x; i < n * k; i += SG_NT) {
-      const uint32_t r = i / k, e = i - r * k;
-      const uint32_t j = idx_of(r)[e];
-      // the first rank holding j sums every holder in rank order
-      bool first = true;
-      uint32_t pos;
-      for (uint32_t r2 = 0; r2 < r && first; r2++) first = !holds(idx_of(r2), k, j, &pos);
-      if (!first) continue;
-      double acc = 0.0;
-      acc += (double)get_val(rank_payload(p, c, r) + 8 + 4ull * k, e, p.f16);
-      for (uint32_t r2 = r + 1; r2 < n; r2++)
-        if (holds(idx_of(r2), k, j, &pos)) acc += (double)get_val(rank_payload(p, c, r2) + 8 + 4ull * k, pos, p.f16);
-      const float d = mean_plus(acc, p.inv_n, (double)V[j]);   // no EF: V is the zeroed scratch
-      V[j] = d;
-      if (topk_noef_server && d != 0.f) {   // no dense pass: the candidates are the nonzero Delta
-        const uint32_t s = atomicAdd(&scnt, 1u);
-        if (s < cap) cand[s] = j;
-      }
-    }
-    __syncthreads();
-    if (topk_noef_server) {
-      if (threadIdx.x == 0) {
-        p.cnt[u] = scnt;
-        p.guess[u] = 1u;
-      }
-      return;
-    }
+  if (KIND == SP_TOPK && p.server && !p.use_ef) {   // Delta is +0 outside the ranks' entries
+    if (threadIdx.x == 0) p.guess[u] = 1u;
+    return;
   }
   // ---- candidate threshold
   uint32_t G;
@@ -283,143 +243,13 @@ __global__ void __launch_bounds__(SG_NT) sparse_prep_kernel(const __grid_constan
   if (threadIdx.x == 0) p.guess[u] = G;
 }
 
-// ================================================================ dense
-template <int KIND, bool SERVER>
-__global__ void __launch_bounds__(SS_NT, 2) sparse_dense_kernel(const __grid_constant__ SparseParams p) {
-  __shared__ uint32_t scand[SS_CAND];   // the slice's candidates (unit indices)
-  __shared__ uint32_t scnt, sbase;
-  bool bad = false;
-  for (uint32_t si = blockIdx.x; si < p.n_slices; si += gridDim.x) {
-    const Slice sl = p.slices[si];
-    const DevChunk c = p.chunks[sl.chunk];
-    const uint32_t L = c.len, s0 = sl.start, len = sl.len;
-    if (sl.nslices == 0) {   // ---- raw unit: worker payload = g (no EF, R3); server: the ranks' mean
-      float* out = reinterpret_cast<float*>(p.out + c.pay);
-      for (uint32_t i = threadIdx.x; 4 * i < len; i += SS_NT) {
-        const uint32_t j = s0 + 4 * i;
-        float4 v;
-        if (!SERVER) {
-          v = load4_masked(p.grad + c.off, j, L);
-          if (p.check_finite) bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
-        } else {
-          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-          for (uint32_t r = 0; r < p.n; r++) {
-            const float4 d = load4_masked(reinterpret_cast<const float*>(p.recv + r * p.slot_bytes + c.recv), j, L);
-            a0 += (double)d.x; a1 += (double)d.y; a2 += (double)d.z; a3 += (double)d.w;
-          }
-          v = make_float4(mean_plus(a0, p.inv_n, 0.0), mean_plus(a1, p.inv_n, 0.0),
-                          mean_plus(a2, p.inv_n, 0.0), mean_plus(a3, p.inv_n, 0.0));
-        }
-        store4_masked(out, j, L, v);
-      }
-      continue;
-    }
-    if (SERVER && KIND == SP_TOPK && !p.use_ef) continue;   // candidates listed by the prep kernel
-    const uint32_t u = p.chunk2u[sl.chunk];
-    const uint32_t G = p.guess[u];
-    float* V = const_cast<float*>(unit_values(p, c));
-    float4 q[4];
-    if (!SERVER) {
-      float4 g4[4], e4[4];
-#pragma unroll
-      for (int it = 0; it < 4; it++) {   // all loads in flight first
-        const uint32_t j = s0 + 4 * (threadIdx.x + it * SS_NT);
-        const bool in = 4 * (threadIdx.x + it * SS_NT) < len;
-        g4[it] = e4[it] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (in) {
-          g4[it] = j + 4 <= L ? ldg4_stream(p.grad + c.off + j) : load4_masked(p.grad + c.off, j, L);
-          if (p.use_ef) e4[it] = j + 4 <= L ? ldg4_stream(p.vals + c.off + j) : load4_masked(p.vals + c.off, j, L);
-        }
-      }
-#pragma unroll
-      for (int it = 0; it < 4; it++) {
-        const uint32_t j = s0 + 4 * (threadIdx.x + it * SS_NT);
-        if (p.check_finite)
-          bad |= !(isfinite(g4[it].x) && isfinite(g4[it].y) && isfinite(g4[it].z) && isfinite(g4[it].w));
-        q[it] = p.use_ef ? make_float4(fadd(g4[it].x, e4[it].x), fadd(g4[it].y, e4[it].y), fadd(g4[it].z, e4[it].z),
-                                       fadd(g4[it].w, e4[it].w))
-                         : g4[it];
-        if (p.use_ef && 4 * (threadIdx.x + it * SS_NT) < len) {   // e := q (the selected get e = q - val later)
-          if (j + 4 <= L) st4(V + j, q[it]);
-          else store4_masked(V, j, L, q[it]);
-        }
-      }
-    } else if (KIND == SP_TOPK || p.use_ef) {
-      // Delta = e~ with the entries applied.  e~ is never -0 (every write is +0 +
-      // x, x - x, or a mean that starts at +0), except after bpc_load_state of a
-      // -0: Delta = fl32(0 + e~) is then +0, fixed here (read-only otherwise)
-#pragma unroll
-      for (int it = 0; it < 4; it++) {
-        const uint32_t f = threadIdx.x + it * SS_NT;
-        const uint32_t j = s0 + 4 * f;
-        q[it] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (4 * f < len) q[it] = j + 4 <= L ? ldg4_stream(V + j) : load4_masked(V, j, L);
-      }
-#pragma unroll
-      for (int it = 0; it < 4; it++) {
-        const uint32_t j = s0 + 4 * (threadIdx.x + it * SS_NT);
-#pragma unroll
-        for (int e = 0; e < 4; e++)
-          if (__float_as_uint(get(q[it], e)) == 0x80000000u && j + e < L) {
-            set(q[it], e, 0.f);
-            V[j + e] = 0.f;
-          }
-      }
-    } else {
-#pragma unroll
-      for (int it = 0; it < 4; it++) q[it] = make_float4(0.f, 0.f, 0.f, 0.f);   // random-k, no EF: keys only
-    }
-    // ---- candidates: key >= G, gathered per slice in shared memory, then one
-    // global append per slice (a unit's slices run on many CTAs at once)
-    if (threadIdx.x == 0) scnt = 0;
-    __syncthreads();
-#pragma unroll
-    for (int it = 0; it < 4; it++) {
-      const uint32_t f = threadIdx.x + it * SS_NT;
-      const uint32_t j = s0 + 4 * f;
-      uint32_t m = 0;
-      if (4 * f < len) {
-#pragma unroll
-        for (int e = 0; e < 4; e++)
-          if (j + e < L && sel_key<KIND>(get(q[it], e), j + e, p, c.id) >= G) m |= 1u << e;
-      }
-      if (__ballot_sync(0xffffffffu, m != 0u)) {
-#pragma unroll
-        for (int e = 0; e < 4; e++)
-          if ((m >> e) & 1u) {
-            const uint32_t pos = atomicAdd(&scnt, 1u);
-            if (pos < (uint32_t)SS_CAND) scand[pos] = j + e;
-          }
-      }
-    }
-    __syncthreads();
-    const uint32_t ns = scnt;
-    if (ns) {
-      const uint32_t cap = p.cand_off[u + 1] - p.cand_off[u];
-      if (threadIdx.x == 0)   // more than SS_CAND: the list is incomplete, push the count past cap
-        sbase = atomicAdd(p.cnt + u, ns > (uint32_t)SS_CAND ? ns + cap + 1 : ns);
-      __syncthreads();
-      uint32_t* cand = p.cand + p.cand_off[u];
-      for (uint32_t i = threadIdx.x; i < ns && i < (uint32_t)SS_CAND; i += SS_NT)
-        if (sbase + i < cap) cand[sbase + i] = scand[i];
-    }
-    __syncthreads();   // scnt / scand / sbase reused by the next slice
-  }
-  if (bad) atomicOr(p.flag, 1u);
-}
-
 // ================================================================ select
-__device__ __forceinline__ void emit_one(const SparseParams& p, float* V, uint8_t* pay, uint32_t k, uint32_t pos,
-                                         uint32_t j, bool scaled, float scale) {
-  const float q = V[j];
-  const float val = quant_val(scaled ? fmul(q, scale) : q, p.f16);   // R23
-  reinterpret_cast<uint32_t*>(pay + 8)[pos] = j;
-  put_val(pay + 8 + 4ull * k, pos, val, p.f16);
-  if (p.use_ef) V[j] = fsub(q, val);   // e = q - dec (operator fusion: O(k), PAPER.md:502)
-}
+// The unit's candidates are index-ordered per slice and the slices are in index
+// order, so the concatenated list is sorted by index: after the radix select of
+// T, one ordered pass (ties counted in index order) emits the payload -- no sort.
 
 // server without EF: the scratch goes back to all-zero (only the ranks' entries
-// were written by the prep kernel), by `nt` threads from `tid`
+// were written by sparse_apply), by `nt` threads from `tid`
 __device__ __forceinline__ void clear_scratch(const SparseParams& p, const DevChunk& c, float* V, uint32_t tid,
                                               uint32_t nt) {
   for (uint32_t i = tid; i < p.n * c.k; i += nt) {
@@ -428,11 +258,23 @@ __device__ __forceinline__ void clear_scratch(const SparseParams& p, const DevCh
   }
 }
 
-// ---- one warp per unit: the candidate path for c <= SW_CAP, k <= SW_KMAX
+// one payload entry (position pos) of the selected index j with its value q
+__device__ __forceinline__ void emit_entry(const SparseParams& p, float* V, uint8_t* pay, uint32_t k, uint32_t pos,
+                                           uint32_t j, float q, bool scaled, float scale) {
+  const float val = quant_val(scaled ? fmul(q, scale) : q, p.f16);   // R23
+  reinterpret_cast<uint32_t*>(pay + 8)[pos] = j;
+  put_val(pay + 8 + 4ull * k, pos, val, p.f16);
+  if (p.use_ef) V[j] = fsub(q, val);   // e = q - dec (operator fusion: O(k), PAPER.md:502)
+}
+
+// the unit's candidate count (sum over its slices, each at most cs) and whether
+// a slice overflowed its sub-list
+__device__ __forceinline__ uint32_t unit_ns(const DevChunk& c) { return (c.len + 8191u) / 8192u; }
+
+// ---- one warp per unit: c <= SW_CAP candidates, k <= SW_KMAX
 struct WarpSel {
-  uint32_t idx[SW_CAP];   // candidate indices; bit 31 = selected, bit 30 = T-tie
-  uint32_t key[SW_CAP];   // keys, then the T-tie / selection lists
-  uint32_t hist[256];
+  uint32_t idx[SW_CAP];   // candidate indices, ascending
+  uint32_t key[SW_CAP];   // keys, then the selected indices
 };
 
 template <int KIND>
@@ -444,94 +286,114 @@ __global__ void __launch_bounds__(32 * SW_WARPS) sparse_select_warp_kernel(const
   WarpSel& s = reinterpret_cast<WarpSel*>(swraw)[w];
   const DevChunk c = p.chunks[p.items[u]];
   const uint32_t L = c.len, k = c.k;
-  const uint32_t cap = p.cand_off[u + 1] - p.cand_off[u];
-  const uint32_t cnt = p.cnt[u];
-  if (!(cnt >= k && cnt <= cap && cnt <= SW_CAP && k <= SW_KMAX)) {
+  if (L > SEL_LMAX) return;   // per-tensor unit: the large-unit path (sparse_large_*)
+  const uint32_t ns = unit_ns(c), cs = (p.cand_off[u + 1] - p.cand_off[u]) / ns;
+  // lane l: slice l's count (a chunk unit has <= 32 slices)
+  const uint32_t sc = (uint32_t)lane < ns ? p.scnt[p.first_slice[u] + lane] : 0u;
+  const bool ovf = __any_sync(0xffffffffu, sc > cs);
+  uint32_t incl = sc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= (uint32_t)o) incl += y;
+  }
+  const uint32_t cnt = __shfl_sync(0xffffffffu, incl, 31);
+  if (ovf || cnt < k || cnt > SW_CAP || k > SW_KMAX) {
     if (lane == 0) p.big[u] = 1;   // the CTA select kernel takes this unit
     return;
   }
   float* V = const_cast<float*>(unit_values(p, c));
   uint8_t* pay = p.out + c.pay;
   const uint32_t* cand = p.cand + p.cand_off[u];
-  for (uint32_t i = lane; i < cnt; i += 32) {
-    const uint32_t j = cand[i];
-    s.idx[i] = j;
-    s.key[i] = sel_key<KIND>(KIND == SP_TOPK ? V[j] : 0.f, j, p, c.id);
-  }
-  __syncwarp();
-  // k-th largest key: 4 x 8-bit radix select
-  uint32_t prefix = 0, pmask = 0, kk = k, above = 0;
-  for (int pass = 0; pass < 4; pass++) {
-    const int sh = 24 - 8 * pass;
+  // the sub-lists, concatenated in slice order (= index order): 8 slices at a time,
+  // two entries per lane and slice, 16 loads in flight (cs <= 2^13, but the
+  // counts are ~3x below cs: the lanes loop while a slice has more)
+  for (uint32_t s0 = 0; s0 < ns; s0 += 8) {
+    uint32_t v[16];
 #pragma unroll
-    for (int i = 0; i < 8; i++) s.hist[lane + 32 * i] = 0;
-    __syncwarp();
-    for (uint32_t i = lane; i < cnt; i += 32) {
-      const uint32_t key = s.key[i];
-      hist_add(s.hist, (key >> sh) & 255u, (key & pmask) == prefix);
+    for (int q = 0; q < 8; q++) {
+      const uint32_t sl = s0 + q;
+      const uint32_t n_sl = __shfl_sync(0xffffffffu, sc, sl & 31);
+      v[2 * q] = (sl < ns && lane < n_sl) ? cand[sl * cs + lane] : 0u;
+      v[2 * q + 1] = (sl < ns && lane + 32 < n_sl) ? cand[sl * cs + lane + 32] : 0u;
     }
-    __syncwarp();
-    const uint2 fb = warp_find_bin256(s.hist, kk);
-    __syncwarp();
-    prefix |= fb.x << sh;
-    pmask |= 0xffu << sh;
-    kk -= fb.y;
-    above += fb.y;
-  }
-  const uint32_t T = prefix, need = k - above;   // T-ties to take, lowest indices first
-  uint32_t neq = 0;
-  for (uint32_t i = lane; i < cnt; i += 32) {
-    const uint32_t key = s.key[i];
-    if (key > T) s.idx[i] |= 0x80000000u;
-    else if (key == T) {
-      s.idx[i] |= 0x40000000u;
-      neq++;
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      const uint32_t sl = s0 + q;
+      const uint32_t n_sl = __shfl_sync(0xffffffffu, sc, sl & 31), b_sl = __shfl_sync(0xffffffffu, incl - sc, sl & 31);
+      if (sl >= ns) continue;
+      if (lane < n_sl) s.idx[b_sl + lane] = v[2 * q];
+      if (lane + 32 < n_sl) s.idx[b_sl + lane + 32] = v[2 * q + 1];
+      for (uint32_t i = lane + 64; i < n_sl; i += 32) s.idx[b_sl + i] = cand[sl * cs + i];
     }
   }
-  neq = __reduce_add_sync(0xffffffffu, neq);
   __syncwarp();
-  uint32_t cut = 0xffffffffu;
-  if (need < neq) {   // the need-th smallest index among the T-ties (sorted in key[])
-    uint32_t base = 0;
-    for (uint32_t i0 = 0; i0 < cnt; i0 += 32) {
-      const uint32_t i = i0 + lane;
-      const bool t = i < cnt && (s.idx[i] & 0x40000000u);
-      const uint32_t b = __ballot_sync(0xffffffffu, t);
-      if (t) s.key[base + __popc(b & ((1u << lane) - 1))] = s.idx[i] & 0x3fffffffu;
-      base += __popc(b);
+  // keys, value reads batched 8 deep
+  for (uint32_t i0 = 0; i0 < cnt; i0 += 256) {
+    float vv[8];
+#pragma unroll
+    for (int r = 0; r < 8; r++) {
+      const uint32_t i = i0 + 32 * r + lane;
+      vv[r] = (KIND == SP_TOPK && i < cnt) ? V[s.idx[i]] : 0.f;
     }
-    uint32_t P = 1;
-    while (P < neq) P <<= 1;
-    for (uint32_t i = neq + lane; i < P; i += 32) s.key[i] = 0xffffffffu;
-    __syncwarp();
-    bitonic_sort(s.key, P, lane, 32, [] { __syncwarp(); });
-    cut = s.key[need - 1];
-    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < 8; r++) {
+      const uint32_t i = i0 + 32 * r + lane;
+      if (i < cnt) s.key[i] = sel_key<KIND>(vv[r], s.idx[i], p, c.id);
+    }
   }
-  // the k selected indices into key[], then sorted ascending
-  uint32_t base = 0;
+  __syncwarp();
+  // T = the k-th largest key: the largest t with #{key >= t} >= k, bit by bit
+  // from the top (no atomics, no barriers: one warp, keys in shared memory)
+  uint32_t T = 0;
+  for (int bit = 31; bit >= 0; bit--) {
+    const uint32_t t = T | (1u << bit);
+    uint32_t n_ge = 0;
+    for (uint32_t i = lane; i < cnt; i += 32) n_ge += s.key[i] >= t;
+    if (__reduce_add_sync(0xffffffffu, n_ge) >= k) T = t;
+  }
+  uint32_t n_gt = 0;
+  for (uint32_t i = lane; i < cnt; i += 32) n_gt += s.key[i] > T;
+  const uint32_t need = k - __reduce_add_sync(0xffffffffu, n_gt);   // T-ties to take, lowest indices first
+  // ordered pass over the index-sorted candidates: the selected indices, in
+  // order, compacted to the front of key[] (position <= read position)
+  uint32_t eq_run = 0, out_run = 0;
   for (uint32_t i0 = 0; i0 < cnt; i0 += 32) {
     const uint32_t i = i0 + lane;
-    const uint32_t x = i < cnt ? s.idx[i] : 0u;
-    const bool sel = i < cnt && ((x & 0x80000000u) || ((x & 0x40000000u) && (x & 0x3fffffffu) <= cut));
-    const uint32_t b = __ballot_sync(0xffffffffu, sel);
-    if (sel) s.key[base + __popc(b & ((1u << lane) - 1))] = x & 0x3fffffffu;
-    base += __popc(b);
+    const uint32_t key = i < cnt ? s.key[i] : 0u;
+    const bool eq = i < cnt && key == T;
+    const uint32_t be = __ballot_sync(0xffffffffu, eq);
+    const uint32_t er = eq_run + __popc(be & ((1u << lane) - 1));
+    const bool sel = i < cnt && (key > T || (eq && er < need));
+    const uint32_t bs = __ballot_sync(0xffffffffu, sel);
+    __syncwarp();
+    if (sel) s.key[out_run + __popc(bs & ((1u << lane) - 1))] = s.idx[i];
+    __syncwarp();
+    eq_run += __popc(be);
+    out_run += __popc(bs);
   }
-  uint32_t P = 1;
-  while (P < k) P <<= 1;
-  for (uint32_t i = k + lane; i < P; i += 32) s.key[i] = 0xffffffffu;
   __syncwarp();
-  bitonic_sort(s.key, P, lane, 32, [] { __syncwarp(); });
+  // emit, value reads batched 8 deep
   const bool scaled = KIND == SP_RANDK && p.randk_scaled;
   const float scale = (float)((double)L / (double)k);
-  for (uint32_t i = lane; i < k; i += 32) emit_one(p, V, pay, k, i, s.key[i], scaled, scale);
+  for (uint32_t i0 = 0; i0 < k; i0 += 256) {
+    float qv[8];
+    uint32_t jj[8];
+#pragma unroll
+    for (int r = 0; r < 8; r++) {
+      const uint32_t i = i0 + 32 * r + lane;
+      jj[r] = i < k ? s.key[i] : 0u;
+      qv[r] = i < k ? V[jj[r]] : 0.f;
+    }
+#pragma unroll
+    for (int r = 0; r < 8; r++) {
+      const uint32_t i = i0 + 32 * r + lane;
+      if (i < k) emit_entry(p, V, pay, k, i, jj[r], qv[r], scaled, scale);
+    }
+  }
   __syncwarp();
   if (p.server && !p.use_ef) clear_scratch(p, c, V, lane, 32);
-  if (lane == 0) {
-    *reinterpret_cast<uint64_t*>(pay) = (uint64_t)k;
-    p.cnt[u] = 0;   // the next step's dense pass appends from 0
-  }
+  if (lane == 0) *reinterpret_cast<uint64_t*>(pay) = (uint64_t)k;
 }
 
 // ---- one CTA per unit: larger candidate lists, or the exact whole-unit path
@@ -539,19 +401,8 @@ struct SelSmem {
   uint32_t hist[256];
   uint32_t info[4];
   uint32_t scan[SE_NT / 32 + 1];
+  uint32_t sbase[33];   // the sub-lists' offsets in the concatenated list
 };
-
-__device__ __forceinline__ uint32_t block_compact(const uint32_t* a, uint32_t n, uint32_t mask, uint32_t* out,
-                                                  uint32_t* counter) {
-  if (threadIdx.x == 0) *counter = 0;
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < n; i += SE_NT)
-    if (a[i] & mask) out[atomicAdd(counter, 1u)] = a[i] & 0x3fffffffu;
-  __syncthreads();
-  const uint32_t m = *counter;
-  __syncthreads();
-  return m;
-}
 
 // the rank-th largest (1-based) key over `n` keys given by key_of(i), 4 x 8-bit
 // digits; returns the key, *above = keys strictly larger
@@ -585,9 +436,51 @@ __device__ uint32_t block_kth_largest(KeyOf key_of, uint32_t n, uint32_t rank, S
   return prefix;
 }
 
+// ordered emission over `n` index-ascending items (4 consecutive per thread per
+// round): item i is selected if key > T, or key == T among the first `need`
+// T-ties in index order
+template <class ItemOf>
+__device__ void block_ordered_emit(ItemOf item_of, uint32_t n, uint32_t T, uint32_t need, SelSmem& sm,
+                                   const SparseParams& p, float* V, uint8_t* pay, uint32_t k, bool scaled,
+                                   float scale) {
+  uint32_t eq_run = 0, out_run = 0;
+  for (uint32_t base = 0; base < n; base += 4 * SE_NT) {
+    const uint32_t i0 = base + 4 * threadIdx.x;
+    uint32_t jj[4], gtm = 0, eqm = 0;
+    float qv[4];
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+      jj[e] = 0;
+      qv[e] = 0.f;
+      if (i0 + e < n) {
+        uint32_t key;
+        item_of(i0 + e, &jj[e], &key, &qv[e]);
+        gtm |= (uint32_t)(key > T) << e;
+        eqm |= (uint32_t)(key == T) << e;
+      }
+    }
+    uint32_t teq;
+    const uint32_t er = block_excl_scan_u32<SE_NT>(__popc(eqm), sm.scan, &teq);
+    uint32_t selm = gtm, rr = eq_run + er;
+#pragma unroll
+    for (int e = 0; e < 4; e++)
+      if ((eqm >> e) & 1u) {
+        if (rr < need) selm |= 1u << e;
+        rr++;
+      }
+    uint32_t tsel;
+    uint32_t pos = out_run + block_excl_scan_u32<SE_NT>(__popc(selm), sm.scan, &tsel);
+#pragma unroll
+    for (int e = 0; e < 4; e++)
+      if ((selm >> e) & 1u) emit_entry(p, V, pay, k, pos++, jj[e], qv[e], scaled, scale);
+    eq_run += teq;
+    out_run += tsel;
+  }
+}
+
 template <int KIND>
 __global__ void __launch_bounds__(SE_NT) sparse_select_kernel(const __grid_constant__ SparseParams p) {
-  // dynamic: [sel_cap] candidate indices | [sel_cap] keys / lists
+  // dynamic: [sel_cap] candidate indices | [sel_cap] keys
   extern __shared__ __align__(16) uint32_t sx[];
   __shared__ SelSmem sm;
   const uint32_t u = blockIdx.x;
@@ -598,133 +491,326 @@ __global__ void __launch_bounds__(SE_NT) sparse_select_kernel(const __grid_const
   uint8_t* pay = p.out + c.pay;
   const bool scaled = KIND == SP_RANDK && p.randk_scaled;
   const float scale = (float)((double)L / (double)k);
-  const uint32_t cap = p.cand_off[u + 1] - p.cand_off[u];
-  const uint32_t cnt = p.cnt[u];
+  const uint32_t ns = unit_ns(c), cs = (p.cand_off[u + 1] - p.cand_off[u]) / ns;
   const uint32_t* cand = p.cand + p.cand_off[u];
+  if (threadIdx.x < 32) {   // the sub-lists' offsets (ns <= 32)
+    const uint32_t lane = threadIdx.x;
+    const uint32_t sc = lane < ns ? p.scnt[p.first_slice[u] + lane] : 0u;
+    const bool ovf = __any_sync(0xffffffffu, sc > cs);
+    uint32_t incl = sc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= (uint32_t)o) incl += y;
+    }
+    sm.sbase[lane] = incl - sc;
+    if (lane == 31) sm.sbase[32] = ovf ? 0xffffffffu : incl;
+  }
+  __syncthreads();
+  const uint32_t cnt = sm.sbase[32];
   const uint32_t SC = p.sel_cap;
-  if (cnt >= k && cnt <= cap && cnt <= SC) {
+  uint32_t above, T;
+  if (cnt != 0xffffffffu && cnt >= k && cnt <= SC) {
     // ---- exact selection among the candidates (every other key < G <= T)
-    uint32_t* ci = sx;        // indices; bit 31 = selected, bit 30 = T-tie
-    uint32_t* ck = sx + SC;   // keys, then the T-tie / selection lists
+    uint32_t* ci = sx;
+    uint32_t* ck = sx + SC;
+    for (uint32_t sl = 0; sl < ns; sl++) {
+      const uint32_t b0 = sm.sbase[sl], n_sl = (sl + 1 < ns ? sm.sbase[sl + 1] : cnt) - b0;
+      for (uint32_t i = threadIdx.x; i < n_sl; i += SE_NT) ci[b0 + i] = cand[sl * cs + i];
+    }
+    __syncthreads();
     for (uint32_t i = threadIdx.x; i < cnt; i += SE_NT) {
-      const uint32_t j = cand[i];
-      ci[i] = j;
+      const uint32_t j = ci[i];
       ck[i] = sel_key<KIND>(KIND == SP_TOPK ? V[j] : 0.f, j, p, c.id);
     }
     __syncthreads();
-    uint32_t above;
-    const uint32_t T = block_kth_largest([&](uint32_t i) { return ck[i]; }, cnt, k, sm, &above);
-    const uint32_t need = k - above;
-    for (uint32_t i = threadIdx.x; i < cnt; i += SE_NT) {
-      const uint32_t key = ck[i];
-      if (key > T) ci[i] |= 0x80000000u;
-      else if (key == T) ci[i] |= 0x40000000u;
-    }
-    __syncthreads();
-    const uint32_t neq = block_compact(ci, cnt, 0x40000000u, ck, &sm.info[2]);
-    uint32_t cut = 0xffffffffu;
-    if (need < neq) {
-      uint32_t P = 1;
-      while (P < neq) P <<= 1;
-      for (uint32_t i = neq + threadIdx.x; i < P; i += SE_NT) ck[i] = 0xffffffffu;
-      __syncthreads();
-      bitonic_sort(ck, P, threadIdx.x, SE_NT, [] { __syncthreads(); });
-      cut = ck[need - 1];
-    }
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < cnt; i += SE_NT) {
-      const uint32_t x = ci[i];
-      if ((x & 0x40000000u) && (x & 0x3fffffffu) <= cut) ci[i] = x | 0x80000000u;
-    }
-    __syncthreads();
-    const uint32_t ns = block_compact(ci, cnt, 0x80000000u, ck, &sm.info[2]);   // == k
-    uint32_t P = 1;
-    while (P < ns) P <<= 1;
-    for (uint32_t i = ns + threadIdx.x; i < P; i += SE_NT) ck[i] = 0xffffffffu;
-    __syncthreads();
-    bitonic_sort(ck, P, threadIdx.x, SE_NT, [] { __syncthreads(); });
-    for (uint32_t i = threadIdx.x; i < k; i += SE_NT) emit_one(p, V, pay, k, i, ck[i], scaled, scale);
+    T = block_kth_largest([&](uint32_t i) { return ck[i]; }, cnt, k, sm, &above);
+    block_ordered_emit(
+        [&](uint32_t i, uint32_t* j, uint32_t* key, float* q) {
+          *j = ci[i];
+          *key = ck[i];
+          *q = V[*j];
+        },
+        cnt, T, k - above, sm, p, V, pay, k, scaled, scale);
   } else {
-    // ---- exact over the whole unit: radix select of T over all L keys, then an
-    // ordered compaction (index ascending) with the tie cut
-    uint32_t above;
-    const uint32_t T = block_kth_largest(
+    // ---- exact over the whole unit
+    T = block_kth_largest(
         [&](uint32_t j) { return sel_key<KIND>(KIND == SP_TOPK ? V[j] : 0.f, j, p, c.id); }, L, k, sm, &above);
-    const uint32_t need = k - above;   // take the `need` lowest-index T-ties
-    uint32_t eq_run = 0, out_run = 0;
-    for (uint32_t base = 0; base < L; base += 4 * SE_NT) {   // 4 consecutive elements per thread
-      const uint32_t j0 = base + 4 * threadIdx.x;
-      uint32_t gtm = 0, eqm = 0;
-#pragma unroll
-      for (int e = 0; e < 4; e++) {
-        if (j0 + e < L) {
-          const uint32_t key = sel_key<KIND>(KIND == SP_TOPK ? V[j0 + e] : 0.f, j0 + e, p, c.id);
-          gtm |= (uint32_t)(key > T) << e;
-          eqm |= (uint32_t)(key == T) << e;
-        }
-      }
-      uint32_t teq;
-      const uint32_t er = block_excl_scan_u32<SE_NT>(__popc(eqm), sm.scan, &teq);
-      uint32_t selm = gtm, rr = eq_run + er;
-#pragma unroll
-      for (int e = 0; e < 4; e++)
-        if ((eqm >> e) & 1u) {
-          if (rr < need) selm |= 1u << e;
-          rr++;
-        }
-      uint32_t tsel;
-      uint32_t pos = out_run + block_excl_scan_u32<SE_NT>(__popc(selm), sm.scan, &tsel);
-#pragma unroll
-      for (int e = 0; e < 4; e++)
-        if ((selm >> e) & 1u) emit_one(p, V, pay, k, pos++, j0 + e, scaled, scale);
-      eq_run += teq;
-      out_run += tsel;
-    }
+    block_ordered_emit(
+        [&](uint32_t i, uint32_t* j, uint32_t* key, float* q) {
+          *j = i;
+          *q = V[i];
+          *key = sel_key<KIND>(*q, i, p, c.id);
+        },
+        L, T, k - above, sm, p, V, pay, k, scaled, scale);
   }
   __syncthreads();
   if (p.server && !p.use_ef) clear_scratch(p, c, V, threadIdx.x, SE_NT);
   if (threadIdx.x == 0) {
     *reinterpret_cast<uint64_t*>(pay) = (uint64_t)k;
-    p.cnt[u] = 0;   // the next step's dense pass appends from 0
     p.big[u] = 0;
   }
+}
+
+// ================================================================ large units
+// Per-tensor units (NEXT #4) can hold 10^8 elements with k ~ 10^5:
+// T is found by a multi-CTA radix select over the unit's candidates (or over the
+// whole unit when they do not suffice), then the selection is emitted in index
+// order by a count / scan / compaction over the unit's 2^13-element slices.
+// lstate[8 u + .]: 0 prefix, 1 pmask, 2 kk, 3 above, 4 work mode (1 = candidates)
+
+template <int KIND>
+__device__ __forceinline__ uint32_t large_key(const SparseParams& p, const DevChunk& c, const float* V, uint32_t j) {
+  return sel_key<KIND>(KIND == SP_TOPK ? V[j] : 0.f, j, p, c.id);
+}
+
+// per large unit: the candidates suffice (no sub-list overflow, >= k of them)?
+__global__ void sparse_large_init(const __grid_constant__ SparseParams p) {
+  __shared__ uint32_t tot, ovf;
+  const uint32_t lu = blockIdx.x, u = p.large_units[lu];
+  const DevChunk c = p.chunks[p.items[u]];
+  const uint32_t ns = unit_ns(c), cs = (p.cand_off[u + 1] - p.cand_off[u]) / ns;
+  if (threadIdx.x == 0) tot = ovf = 0;
+  __syncthreads();
+  uint32_t t = 0, o = 0;
+  for (uint32_t s = threadIdx.x; s < ns; s += blockDim.x) {
+    const uint32_t sc = p.scnt[p.first_slice[u] + s];
+    t += sc;
+    o |= sc > cs;
+  }
+  atomicAdd(&tot, t);
+  if (o) atomicOr(&ovf, 1u);
+  __syncthreads();
+  if (threadIdx.x == 0) p.lstate[8 * lu + 4] = (!ovf && tot >= c.k) ? 1u : 0u;
+}
+
+// radix-select histogram pass over the large units' candidates (mode 1: the
+// sub-lists, slice by slice) or whole units (mode 0)
+template <int KIND>
+__global__ void __launch_bounds__(256) sparse_large_hist(const __grid_constant__ SparseParams p, int pass) {
+  __shared__ uint32_t h[256];
+  const int sh = 24 - 8 * pass;
+  for (uint32_t lu = 0; lu < p.n_large; lu++) {
+    const uint32_t u = p.large_units[lu];
+    const DevChunk c = p.chunks[p.items[u]];
+    const float* V = unit_values(p, c);
+    const bool cand = p.lstate[8 * lu + 4] != 0;
+    const uint32_t prefix = pass ? p.lstate[8 * lu + 0] : 0u, pmask = pass ? p.lstate[8 * lu + 1] : 0u;
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    if (cand) {
+      const uint32_t ns = unit_ns(c), cs = (p.cand_off[u + 1] - p.cand_off[u]) / ns;
+      for (uint32_t sl = blockIdx.x; sl < ns; sl += gridDim.x) {
+        const uint32_t n_sl = p.scnt[p.first_slice[u] + sl];
+        for (uint32_t i = threadIdx.x; i < n_sl; i += 256) {
+          const uint32_t j = p.cand[p.cand_off[u] + sl * cs + i];
+          const uint32_t key = large_key<KIND>(p, c, V, j);
+          hist_add(h, (key >> sh) & 255u, (key & pmask) == prefix);
+        }
+      }
+    } else {
+      for (uint32_t j = blockIdx.x * 256 + threadIdx.x; j < c.len; j += gridDim.x * 256) {
+        const uint32_t key = large_key<KIND>(p, c, V, j);
+        hist_add(h, (key >> sh) & 255u, (key & pmask) == prefix);
+      }
+    }
+    __syncthreads();
+    if (h[threadIdx.x]) atomicAdd(p.lhist + 256 * lu + threadIdx.x, h[threadIdx.x]);
+    __syncthreads();
+  }
+}
+
+// one warp per large unit: the bin holding the kk-th largest key; clears the histogram
+__global__ void sparse_large_find(const __grid_constant__ SparseParams p, int pass) {
+  const uint32_t lu = blockIdx.x;
+  const int sh = 24 - 8 * pass;
+  uint32_t* st = p.lstate + 8 * lu;
+  const uint32_t u = p.large_units[lu];
+  const uint32_t kk = pass ? st[2] : p.chunks[p.items[u]].k;
+  const uint2 fb = warp_find_bin256(p.lhist + 256 * lu, kk);
+  __syncwarp();
+  for (uint32_t b = threadIdx.x; b < 256; b += 32) p.lhist[256 * lu + b] = 0;
+  if (threadIdx.x == 0) {
+    st[0] = (pass ? st[0] : 0u) | (fb.x << sh);
+    st[1] = (pass ? st[1] : 0u) | (0xffu << sh);
+    st[2] = kk - fb.y;
+    st[3] = (pass ? st[3] : 0u) + fb.y;
+  }
+}
+
+// per slice of a large unit: keys above T and equal to T
+template <int KIND>
+__global__ void __launch_bounds__(SE_NT) sparse_large_count(const __grid_constant__ SparseParams p) {
+  __shared__ uint32_t red[2][SE_NT / 32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (uint32_t ls = blockIdx.x; ls < p.n_lslices; ls += gridDim.x) {
+    const uint2 us = p.lslices[ls];   // (slice index, large unit)
+    const Slice sl = p.slices[us.x];
+    const DevChunk c = p.chunks[sl.chunk];
+    const float* V = unit_values(p, c);
+    const uint32_t T = p.lstate[8 * us.y + 0];
+    uint32_t gt = 0, eq = 0;
+    for (uint32_t o = threadIdx.x; o < sl.len; o += SE_NT) {
+      const uint32_t key = large_key<KIND>(p, c, V, sl.start + o);
+      gt += key > T;
+      eq += key == T;
+    }
+    gt = __reduce_add_sync(0xffffffffu, gt);
+    eq = __reduce_add_sync(0xffffffffu, eq);
+    if (lane == 0) {
+      red[0][warp] = gt;
+      red[1][warp] = eq;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t a = 0, b = 0;
+      for (int w = 0; w < SE_NT / 32; w++) {
+        a += red[0][w];
+        b += red[1][w];
+      }
+      p.lcnt[ls] = make_uint2(a, b);
+    }
+    __syncthreads();
+  }
+}
+
+// one CTA per large unit: each slice's first output position and the T-ties
+// before it (ties go to the lowest indices: the first `need` in index order)
+__global__ void __launch_bounds__(SE_NT) sparse_large_scan(const __grid_constant__ SparseParams p) {
+  __shared__ uint32_t scan[SE_NT / 32 + 1];
+  const uint32_t lu = blockIdx.x;
+  const uint32_t u = p.large_units[lu];
+  const DevChunk c = p.chunks[p.items[u]];
+  const uint32_t need = c.k - p.lstate[8 * lu + 3];
+  uint32_t out_run = 0, eq_run = 0;
+  const uint32_t s0 = p.lslice_first[lu], s1 = p.lslice_first[lu + 1];
+  for (uint32_t b0 = s0; b0 < s1; b0 += SE_NT) {
+    const uint32_t ls = b0 + threadIdx.x;
+    const uint2 ce = ls < s1 ? p.lcnt[ls] : make_uint2(0, 0);
+    uint32_t teq;
+    const uint32_t eb = eq_run + block_excl_scan_u32<SE_NT>(ce.y, scan, &teq);
+    const uint32_t take = eb >= need ? 0u : min(ce.y, need - eb);
+    uint32_t tsel;
+    const uint32_t ob = out_run + block_excl_scan_u32<SE_NT>(ce.x + take, scan, &tsel);
+    if (ls < s1) p.loff[ls] = make_uint2(ob, eb);
+    out_run += tsel;
+    eq_run += teq;
+  }
+  if (threadIdx.x == 0) *reinterpret_cast<uint64_t*>(p.out + c.pay) = (uint64_t)c.k;
+}
+
+// per slice of a large unit: the selected elements in index order -> payload,
+// EF fix-ups; 16 consecutive elements per thread
+template <int KIND>
+__global__ void __launch_bounds__(SE_NT) sparse_large_emit(const __grid_constant__ SparseParams p) {
+  __shared__ uint32_t scan[SE_NT / 32 + 1];
+  const bool scaled = KIND == SP_RANDK && p.randk_scaled;
+  for (uint32_t ls = blockIdx.x; ls < p.n_lslices; ls += gridDim.x) {
+    const uint2 us = p.lslices[ls];
+    const Slice sl = p.slices[us.x];
+    const DevChunk c = p.chunks[sl.chunk];
+    float* V = const_cast<float*>(unit_values(p, c));
+    const uint32_t T = p.lstate[8 * us.y + 0];
+    const uint32_t need = c.k - p.lstate[8 * us.y + 3];
+    const uint2 off = p.loff[ls];   // (first output position, T-ties before this slice)
+    const float scale = (float)((double)c.len / (double)c.k);
+    uint8_t* pay = p.out + c.pay;
+    const uint32_t j0 = sl.start + 16 * threadIdx.x;
+    uint32_t gtm = 0, eqm = 0;
+#pragma unroll
+    for (int e = 0; e < 16; e++) {
+      if (16 * threadIdx.x + e < sl.len) {
+        const uint32_t key = large_key<KIND>(p, c, V, j0 + e);
+        gtm |= (uint32_t)(key > T) << e;
+        eqm |= (uint32_t)(key == T) << e;
+      }
+    }
+    uint32_t teq;
+    uint32_t rr = off.y + block_excl_scan_u32<SE_NT>(__popc(eqm), scan, &teq);
+    uint32_t selm = gtm;
+#pragma unroll
+    for (int e = 0; e < 16; e++)
+      if ((eqm >> e) & 1u) {
+        if (rr < need) selm |= 1u << e;
+        rr++;
+      }
+    uint32_t tsel;
+    uint32_t pos = off.x + block_excl_scan_u32<SE_NT>(__popc(selm), scan, &tsel);
+    for (uint32_t m = selm; m; m &= m - 1) {
+      const uint32_t j = j0 + (uint32_t)(__ffs(m) - 1);
+      const float q = V[j];
+      const float val = quant_val(scaled ? fmul(q, scale) : q, p.f16);   // R23
+      reinterpret_cast<uint32_t*>(pay + 8)[pos] = j;
+      put_val(pay + 8 + 4ull * c.k, pos, val, p.f16);
+      if (p.use_ef) V[j] = fsub(q, val);
+      pos++;
+    }
+    __syncthreads();
+  }
+}
+
+// after the emit: the no-EF server's scratch cleared
+__global__ void sparse_large_done(const __grid_constant__ SparseParams p) {
+  const uint32_t lu = blockIdx.x;
+  const uint32_t u = p.large_units[lu];
+  const DevChunk c = p.chunks[p.items[u]];
+  if (p.server && !p.use_ef) clear_scratch(p, c, const_cast<float*>(unit_values(p, c)), threadIdx.x, blockDim.x);
 }
 
 // ================================================================ launchers
 size_t sparse_select_smem(uint32_t sel_cap) { return 2ull * sel_cap * sizeof(uint32_t); }
 
 template <int KIND>
-static cudaError_t launch_sparse_t(const SparseParams& p, int grid, cudaStream_t s) {
-  cudaError_t e;
-  if (p.n_units) {
-    sparse_prep_kernel<KIND><<<p.n_units, SG_NT, 0, s>>>(p);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  }
-  if (p.n_slices) {
-    const unsigned g = (unsigned)std::min<uint32_t>((uint32_t)grid, p.n_slices);
-    if (p.server) sparse_dense_kernel<KIND, true><<<g, SS_NT, 0, s>>>(p);
-    else sparse_dense_kernel<KIND, false><<<g, SS_NT, 0, s>>>(p);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  }
-  if (p.n_units) {
-    const size_t ws = sizeof(WarpSel) * SW_WARPS;
-    e = cudaFuncSetAttribute(sparse_select_warp_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ws);
+static cudaError_t launch_prep_t(const SparseParams& p, cudaStream_t s) {
+  if (!p.n_units) return cudaSuccess;
+  if (p.server && p.n_apply_blk) {
+    sparse_apply_kernel<KIND><<<p.n_apply_blk, SA_NT, 0, s>>>(p);
+    cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    sparse_select_warp_kernel<KIND><<<(p.n_units + SW_WARPS - 1) / SW_WARPS, 32 * SW_WARPS, ws, s>>>(p);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    const size_t smem = sparse_select_smem(p.sel_cap);
-    e = cudaFuncSetAttribute(sparse_select_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    sparse_select_kernel<KIND><<<p.n_units, SE_NT, smem, s>>>(p);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
-  return cudaSuccess;
+  sparse_prep_kernel<KIND><<<p.n_units, SG_NT, 0, s>>>(p);
+  return cudaGetLastError();
 }
 
-cudaError_t launch_sparse(int kind, const SparseParams& p, int grid, cudaStream_t s) {
+template <int KIND>
+static cudaError_t launch_select_t(const SparseParams& p, cudaStream_t s) {
+  if (!p.n_units) return cudaSuccess;
+  const size_t ws = sizeof(WarpSel) * SW_WARPS;
+  cudaError_t e = cudaFuncSetAttribute(sparse_select_warp_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ws);
+  if (e != cudaSuccess) return e;
+  sparse_select_warp_kernel<KIND><<<(p.n_units + SW_WARPS - 1) / SW_WARPS, 32 * SW_WARPS, ws, s>>>(p);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  const size_t smem = sparse_select_smem(p.sel_cap);
+  e = cudaFuncSetAttribute(sparse_select_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  sparse_select_kernel<KIND><<<p.n_units, SE_NT, smem, s>>>(p);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (p.n_large) {   // per-tensor units
+    sparse_large_init<<<p.n_large, 256, 0, s>>>(p);
+    for (int pass = 0; pass < 4; pass++) {
+      sparse_large_hist<KIND><<<p.large_grid, 256, 0, s>>>(p, pass);
+      sparse_large_find<<<p.n_large, 32, 0, s>>>(p, pass);
+    }
+    sparse_large_count<KIND><<<p.large_grid, SE_NT, 0, s>>>(p);
+    sparse_large_scan<<<p.n_large, SE_NT, 0, s>>>(p);
+    sparse_large_emit<KIND><<<p.large_grid, SE_NT, 0, s>>>(p);
+    sparse_large_done<<<p.n_large, 256, 0, s>>>(p);
+    e = cudaGetLastError();
+  }
+  return e;
+}
+
+cudaError_t launch_sparse_prep(int kind, const SparseParams& p, cudaStream_t s) {
   switch (kind) {
-    case SP_TOPK: return launch_sparse_t<SP_TOPK>(p, grid, s);
-    case SP_RANDK: return launch_sparse_t<SP_RANDK>(p, grid, s);
+    case SP_TOPK: return launch_prep_t<SP_TOPK>(p, s);
+    case SP_RANDK: return launch_prep_t<SP_RANDK>(p, s);
+  }
+  return cudaErrorInvalidValue;
+}
+cudaError_t launch_sparse_select(int kind, const SparseParams& p, cudaStream_t s) {
+  switch (kind) {
+    case SP_TOPK: return launch_select_t<SP_TOPK>(p, s);
+    case SP_RANDK: return launch_select_t<SP_RANDK>(p, s);
   }
   return cudaErrorInvalidValue;
 }

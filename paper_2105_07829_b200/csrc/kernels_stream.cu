@@ -40,7 +40,10 @@ __device__ __forceinline__ void consumers_sync() {   // named barrier over the c
 
 // ============================================================== update_stream
 constexpr int UST = 3;                      // stages
-constexpr int UK = UTILE / 4 / CNT;         // float4 per consumer thread per tile = 2
+// Work items: 4096-element update tiles (LANS: its block sums are per 4096-tile,
+// R22), or their 2048-element halves (Adam, NAG): a 2048 item needs half the
+// shared memory, so two CTAs share an SM -- 32 consumer warps hide the latency
+// of the exact division / root sequences (8 per 4 elements) that 16 could not
 
 struct UDesc {
   uint64_t off;    // flat element offset of the chunk
@@ -54,25 +57,26 @@ struct UDesc {
   float ca, cb;    // LANS pass 2: the tile's block coefficients (R22)
 };
 
+template <int T>
 struct __align__(128) USmem {
-  float4 m[UST][UTILE / 4];
-  float4 v[UST][UTILE / 4];
-  float4 x[UST][UTILE / 4];
-  float4 pay[UST][UTILE / 4];     // payload piece: raw fp32 tile, or sign / code bits
+  float4 m[UST][T / 4];
+  float4 v[UST][T / 4];
+  float4 x[UST][T / 4];
+  float4 pay[UST][T / 4];         // payload piece: raw fp32 tile, or sign / code bits
   float4 head[UST];               // the payload's first 16 bytes: scale (sign) / norm (dither)
   UDesc desc[UST];
   uint64_t full[UST], empty[UST];
   uint64_t sums[UST];             // LANS pass 1: the consumers' warp subtrees of stage s are in red[s]
-  double red[UST][3][UTILE / 16];  // LANS pass 1: 16-element subtrees of x^2, u^2, w^2
+  double red[UST][3][T / 16];     // LANS pass 1: 16-element subtrees of x^2, u^2, w^2
 };
 
 
 // LANS (R22): u = r + lambda x, w = c + lambda x with r = m~/(sqrt(v~)+eps),
 // c = g~/(sqrt(v~)+eps), from the already-updated m, v (the oracle's order)
-__device__ __forceinline__ void lans_uw(float g, float m, float v, float x, const UpdateParams& p, float& u,
-                                        float& w) {
-  const float den = fadd(fsqrt0(divc(v, p.bc2, p.ibc2)), p.eps);
-  u = fadd(fdiv_pos(divc(m, p.bc1, p.ibc1), den), fmul(p.wd, x));
+__device__ __forceinline__ void lans_uw(float g, float m, float v, float x, const UpdateParams& p, const float4 bc,
+                                        float& u, float& w) {
+  const float den = fadd(fsqrt0(divc(v, bc.y, bc.w)), p.eps);
+  u = fadd(fdiv_pos(divc(m, bc.x, bc.z), den), fmul(p.wd, x));
   w = fadd(fdiv_pos(g, den), fmul(p.wd, x));
 }
 
@@ -85,12 +89,16 @@ __device__ __forceinline__ void lans_uw(float g, float m, float v, float x, cons
 //         tile's block coefficients (p.lans_coef, from lans_coef_kernel).
 // MODE 3: NAG (R24): g = g~ + lambda x, m = mu m + g (m holds the velocity),
 //         x -= lr (g + mu m); v is neither read nor written (16 B/element).
-template <int KIND, bool FUSED, int MODE>
-__global__ void __launch_bounds__(SNT, 1) update_stream(const __grid_constant__ UpdateParams p) {
+template <int KIND, bool FUSED, int MODE, int T>
+__global__ void __launch_bounds__(SNT, T == UTILE ? 1 : 2) update_stream(const __grid_constant__ UpdateParams p) {
+  static_assert(T == UTILE || (T == UTILE / 2 && MODE != 1 && MODE != 2), "LANS works on whole tiles");
+  constexpr int UK = T / 4 / CNT;   // float4 per consumer thread per item
+  constexpr uint32_t SPLIT = UTILE / T;
   extern __shared__ __align__(128) unsigned char sraw[];
-  USmem& sm = *reinterpret_cast<USmem*>(sraw);
+  USmem<T>& sm = *reinterpret_cast<USmem<T>*>(sraw);
   const uint32_t G = gridDim.x;
-  const uint32_t mine = p.n_tiles > blockIdx.x ? (p.n_tiles - blockIdx.x + G - 1) / G : 0;
+  const uint32_t n_items = p.n_tiles * SPLIT;
+  const uint32_t mine = n_items > blockIdx.x ? (n_items - blockIdx.x + G - 1) / G : 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = KIND == S_SIGN ? 1 : (int)p.bits;
   if (threadIdx.x == 0) {
@@ -103,13 +111,21 @@ __global__ void __launch_bounds__(SNT, 1) update_stream(const __grid_constant__ 
   }
   __syncthreads();
   pdl_wait_and_release();
+  const LaunchEp ep = launch_begin(p.sync);
+  const float4 bc = bias_of(p.bias, ep.t);   // the step's bias corrections (R16)
   if (warp == CW) {   // ---------------- producer
     if (lane == 0) {
-      if (FUSED) peer_wait(p.sync);   // fused exchange: every owner's p has landed in P
+      if (FUSED) peer_wait(p.sync, ep);   // fused exchange: every owner's p has landed in P
       for (uint32_t i = 0; i < mine; i++) {
         const int s = i % UST;
         if (i >= (uint32_t)UST) mbar_wait(&sm.empty[s], ((i / UST) - 1) & 1);
-        const Tile tl = p.tiles[blockIdx.x + i * G];
+        const uint32_t item = blockIdx.x + i * G;
+        Tile tl = p.tiles[item / SPLIT];
+        if (SPLIT > 1) {   // half h of the tile (the second half of a short tile may be empty)
+          const uint32_t h = item % SPLIT, s0 = h * T;
+          tl.len = tl.len > s0 ? min(tl.len - s0, (uint32_t)T) : 0u;
+          tl.start += s0;
+        }
         const DevChunk c = p.chunks[tl.chunk];
         const uint8_t* pay = (FUSED ? p.psrc[c.owner] : p.pbuf) + c.pay;
         const uint32_t nvb = (tl.len & ~3u) * 4u;
@@ -120,7 +136,7 @@ __global__ void __launch_bounds__(SNT, 1) update_stream(const __grid_constant__ 
         d.len = tl.len;
         d.L = c.len;
         d.raw = c.raw;
-        d.tile = blockIdx.x + i * G;
+        d.tile = item;
         if (MODE == 2) {
           const float2 cf = p.lans_coef[tl.pad];   // Tile.pad = block (tensor) index
           d.ca = cf.x;
@@ -128,7 +144,11 @@ __global__ void __launch_bounds__(SNT, 1) update_stream(const __grid_constant__ 
         }
         const uint8_t* psrc;
         uint32_t pbytes, hbytes = 0;
-        if (c.raw || KIND == S_NONE) {
+        if (tl.len == 0) {   // empty half: nothing to load, the phase completes at once
+          psrc = pay;
+          pbytes = 0;
+          d.pofs = 0;
+        } else if (c.raw || KIND == S_NONE) {
           psrc = pay + 4ull * tl.start;
           pbytes = nvb;
           d.pofs = 0;
@@ -229,7 +249,7 @@ __global__ void __launch_bounds__(SNT, 1) update_stream(const __grid_constant__ 
         x4 = load4_masked(x, j, d.L);
       }
       if (MODE == 0) {
-        adam4(g4, m4, v4, x4, p);
+        adam4(g4, m4, v4, x4, p, bc);
         if (f < nvec) {
           st4(m + j, m4);
           st4(v + j, v4);
@@ -250,7 +270,7 @@ __global__ void __launch_bounds__(SNT, 1) update_stream(const __grid_constant__ 
           set(m4, e, mm);
           set(v4, e, vv);
           float uu, ww;
-          lans_uw(g, mm, vv, get(x4, e), p, uu, ww);
+          lans_uw(g, mm, vv, get(x4, e), p, bc, uu, ww);
           const bool valid = in && j + e < d.L;   // padding contributes +0 to the block sums
           set(u4, e, valid ? uu : 0.f);
           set(w4, e, valid ? ww : 0.f);
@@ -300,7 +320,7 @@ __global__ void __launch_bounds__(SNT, 1) update_stream(const __grid_constant__ 
 #pragma unroll
         for (int e = 0; e < 4; e++) {
           float uu, ww;
-          lans_uw(get(g4, e), get(m4, e), get(v4, e), get(x4, e), p, uu, ww);
+          lans_uw(get(g4, e), get(m4, e), get(v4, e), get(x4, e), p, bc, uu, ww);
           const float dd = fadd(fmul(d.ca, uu), fmul(d.cb, ww));   // line 17
           set(x4, e, fsub(get(x4, e), fmul(p.lr, dd)));           // line 18
         }
@@ -314,19 +334,21 @@ __global__ void __launch_bounds__(SNT, 1) update_stream(const __grid_constant__ 
       mbar_arrive(&sm.empty[s]);                  // this warp is done with stage s
     }
   }
+  consumers_sync();   // every consumer's stores issued: the launch may count this CTA done
+  launch_end(p.sync, ep, threadIdx.x == 0);
 }
 
-size_t update_stream_smem() { return sizeof(USmem); }
+size_t update_stream_smem() { return sizeof(USmem<UTILE>); }
 
 cudaError_t launch_update_stream(int kind, const UpdateParams& p, int grid, cudaStream_t st) {
   if (p.n_tiles == 0) return cudaSuccess;
-  auto go = [&](auto fn) -> cudaError_t {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(USmem));
+  auto go = [&](auto fn, size_t smem, uint32_t per_sm, uint32_t split) -> cudaError_t {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)std::min<uint32_t>((uint32_t)grid, p.n_tiles));
+    cfg.gridDim = dim3((unsigned)std::min<uint32_t>((uint32_t)grid * per_sm, p.n_tiles * split));
     cfg.blockDim = dim3(SNT);
-    cfg.dynamicSmemBytes = sizeof(USmem);
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute a[1];
     a[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // prologue overlaps the predecessor
@@ -335,18 +357,20 @@ cudaError_t launch_update_stream(int kind, const UpdateParams& p, int grid, cuda
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, fn, p);
   };
-  const bool f = p.sync.wflags != nullptr;
+  const bool f = p.sync.wait_fam >= 0;
   auto pick = [&](auto kind_tag) -> cudaError_t {
     constexpr int K = decltype(kind_tag)::value;
+    constexpr int H = UTILE / 2;
+    const size_t sh = sizeof(USmem<H>), sf = sizeof(USmem<UTILE>);
     switch (p.mode * 2 + (f ? 1 : 0)) {
-      case 0: return go(update_stream<K, false, 0>);
-      case 1: return go(update_stream<K, true, 0>);
-      case 2: return go(update_stream<K, false, 1>);
-      case 3: return go(update_stream<K, true, 1>);
-      case 4: return go(update_stream<K, false, 2>);
-      case 5: return go(update_stream<K, true, 2>);
-      case 6: return go(update_stream<K, false, 3>);
-      case 7: return go(update_stream<K, true, 3>);
+      case 0: return go(update_stream<K, false, 0, H>, sh, 2, 2);
+      case 1: return go(update_stream<K, true, 0, H>, sh, 2, 2);
+      case 2: return go(update_stream<K, false, 1, UTILE>, sf, 1, 1);
+      case 3: return go(update_stream<K, true, 1, UTILE>, sf, 1, 1);
+      case 4: return go(update_stream<K, false, 2, UTILE>, sf, 1, 1);
+      case 5: return go(update_stream<K, true, 2, UTILE>, sf, 1, 1);
+      case 6: return go(update_stream<K, false, 3, H>, sh, 2, 2);
+      case 7: return go(update_stream<K, true, 3, H>, sh, 2, 2);
     }
     return cudaErrorInvalidValue;
   };

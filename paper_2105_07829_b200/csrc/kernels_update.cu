@@ -10,10 +10,10 @@ enum { U_NONE = 0, U_SIGN = 2, U_TOPK = 3, U_RANDK = 4, U_LDITHER = 5, U_NDITHER
 
 
 // LANS (R22): u = r + lambda x, w = c + lambda x from the updated m, v
-__device__ __forceinline__ void lans_uw1(float g, float m, float v, float x, const UpdateParams& p, float& u,
-                                         float& w) {
-  const float den = fadd(fsqrt0(divc(v, p.bc2, p.ibc2)), p.eps);
-  u = fadd(fdiv_pos(divc(m, p.bc1, p.ibc1), den), fmul(p.wd, x));
+__device__ __forceinline__ void lans_uw1(float g, float m, float v, float x, const UpdateParams& p,
+                                         const float4 bc, float& u, float& w) {
+  const float den = fadd(fsqrt0(divc(v, bc.y, bc.w)), p.eps);
+  u = fadd(fdiv_pos(divc(m, bc.x, bc.z), den), fmul(p.wd, x));
   w = fadd(fdiv_pos(g, den), fmul(p.wd, x));
 }
 
@@ -24,6 +24,8 @@ __global__ void __launch_bounds__(UNT, 4) update_kernel(const __grid_constant__ 
   constexpr bool SPARSE = KIND == U_TOPK || KIND == U_RANDK;
   __shared__ float gts[SPARSE ? UTILE : 1];
   __shared__ double red[MODE == 1 ? 3 : 1][32];
+  const LaunchEp ep = launch_begin(p.sync);
+  const float4 bc = bias_of(p.bias, ep.t);   // the step's bias corrections (R16)
   const Tile tl = p.tiles[blockIdx.x];
   const DevChunk c = p.chunks[tl.chunk];
   const uint8_t* pay = p.pbuf + c.pay;
@@ -107,7 +109,7 @@ __global__ void __launch_bounds__(UNT, 4) update_kernel(const __grid_constant__ 
       }
     }
     if (MODE == 0) {
-      adam4(g4, m4[it], v4[it], x4[it], p);
+      adam4(g4, m4[it], v4[it], x4[it], p, bc);
       if (full) {
         st4(m + j, m4[it]);
         st4(v + j, v4[it]);
@@ -128,7 +130,7 @@ __global__ void __launch_bounds__(UNT, 4) update_kernel(const __grid_constant__ 
         set(m4[it], e, mm);
         set(v4[it], e, vv);
         float uu, ww;
-        lans_uw1(g, mm, vv, get(xv, e), p, uu, ww);
+        lans_uw1(g, mm, vv, get(xv, e), p, bc, uu, ww);
         const bool valid = in && j + e < L;   // padding contributes +0 to the block sums
         set(u4, e, valid ? uu : 0.f);
         set(w4, e, valid ? ww : 0.f);
@@ -172,7 +174,7 @@ __global__ void __launch_bounds__(UNT, 4) update_kernel(const __grid_constant__ 
 #pragma unroll
       for (int e = 0; e < 4; e++) {
         float uu, ww;
-        lans_uw1(get(g4, e), get(m4[it], e), get(v4[it], e), get(x4[it], e), p, uu, ww);
+        lans_uw1(get(g4, e), get(m4[it], e), get(v4[it], e), get(x4[it], e), p, bc, uu, ww);
         const float dd = fadd(fmul(cf.x, uu), fmul(cf.y, ww));   // line 17
         set(x4[it], e, fsub(get(x4[it], e), fmul(p.lr, dd)));    // line 18
       }
@@ -190,6 +192,8 @@ __global__ void __launch_bounds__(UNT, 4) update_kernel(const __grid_constant__ 
       }
     }
   }
+  __syncthreads();   // the CTA's stores issued: count it done
+  launch_end(p.sync, ep, threadIdx.x == 0);
 }
 
 // LANS block coefficients (R22): CTA b sums its tiles' partials in pairwise
