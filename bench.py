@@ -53,11 +53,14 @@ def parse():
                     help="bpc_step update: Adam core (A9), the LANS / CLAN block-normalised update (NEXT #1) "
                          "or NAG (the CNN runs' optimizer, R24)")
     ap.add_argument("--units", choices=["chunk", "tensor"], default="chunk",
-                    help="compression unit: 2^18-element chunks (R1) or whole tensors (PAPER.md:505, "
-                         "two-pass kernels; norm-based compressors only)")
+                    help="compression unit: 2^18-element chunks (R1) or whole tensors (PAPER.md:505; norm "
+                         "kinds: two-pass kernels, sparse kinds: the large-unit select path)")
     ap.add_argument("--threshold-bytes", type=int, default=None,
                     help="size threshold (PAPER.md:504-505): tensors below it stay raw; default: the config's 1 MiB "
                          "(tools/threshold_search.py sweeps it)")
+    ap.add_argument("--launch", choices=["graph", "eager"], default="graph",
+                    help="timed steps: replay of a CUDA graph of one whole step (default; t and the "
+                         "exchange epochs advance on the device) or eager calls")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
@@ -127,6 +130,7 @@ def kernel_bytes(chunks, comp, n, rank, lans=False, nag=False, per_tensor=False)
     written) + the payload read twice; per-tensor units read the worker's
     g, e (server: e~ and the payloads) once more in their first pass."""
     ef = comp.use_ef
+    sparse = comp.kind in (3, 4)
     w = s = u = 0
     for c in chunks:
         L, pb = c.len, c.payload_bytes
@@ -135,6 +139,15 @@ def kernel_bytes(chunks, comp, n, rank, lans=False, nag=False, per_tensor=False)
             if c.owner == rank:
                 s += 4 * n * L + 4 * L
             u += (36 * L + 8 * L) if lans else (16 * L + 4 * L) if nag else (24 * L + 4 * L)
+        elif sparse:
+            # worker: g, e read, e written; server: Delta read (e~ is written only at
+            # the k selected and the ranks' entries); units > 2^18 (per-tensor) read
+            # q / Delta twice more (slice counts, ordered emission)
+            big = 8 * L if L > (1 << 18) else 0
+            w += (12 if ef else 4) * L + pb + big
+            if c.owner == rank:
+                s += n * pb + 4 * L + pb + big
+            u += (36 * L + 2 * pb) if lans else (16 * L + pb) if nag else (24 * L + pb)
         else:
             w += (12 if ef else 4) * L + pb + ((8 if ef else 4) * L if per_tensor else 0)
             if c.owner == rank:
@@ -302,7 +315,8 @@ def run_ours(args):
         obj = [bpc.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nid = obj[0]
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.Stream(dev)   # a capturable stream (not the legacy default stream)
+    torch.cuda.set_stream(stream)
     ctx = bpc.context_for(w, rank=rank, world_size=world, device=local, stream=stream.cuda_stream, nccl_id=nid,
                           exchange=args.exchange)
     chunks = ctx.chunks()
@@ -329,18 +343,37 @@ def run_ours(args):
 
     for i in range(args.warmup):
         step(i)
-    launches0 = ctx.launch_count()
     barrier()
+    run = step
+    if args.launch == "graph":
+        # one CUDA graph per gradient buffer, each one whole step (compress, push,
+        # server, pull, update); every replay is the next step (device-side t / epochs)
+        graphs, per_graph = [], []
+        for b in (0, 1):
+            g = torch.cuda.CUDAGraph()
+            l0 = ctx.launch_count()
+            with torch.cuda.graph(g, stream=stream):
+                step(b)
+            per_graph.append(ctx.launch_count() - l0)
+            graphs.append(g)
+        barrier()
+        for i in range(2):   # first replays (graph upload) stay out of the timed region
+            graphs[i].replay()
+        barrier()
+        run = lambda i: graphs[i % 2].replay()
+    launches0 = ctx.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     wt0 = time.time()
     e0.record(stream)
     for i in range(args.steps):
-        step(i)
+        run(i)
     e1.record(stream)
     barrier()
     wt1 = time.time()
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     launches = ctx.launch_count() - launches0
+    if args.launch == "graph":
+        launches = sum(per_graph[i % 2] for i in range(args.steps))
     clk = clocks.stop(wt0, wt1)
     ctx.sync()
 
@@ -457,7 +490,7 @@ def run_ours(args):
                        "l2": "inputs larger than L2 (g, e, m, v, x = %.0f MB per rank)" % (20 * D / 1e6),
                        "parallelism": f"dp{world} (sharded server: all-to-all + all-gather)",
                        "exchange": ctx.exchange if world > 1 else None,
-                       "optimizer": args.optimizer, "units": args.units,
+                       "optimizer": args.optimizer, "units": args.units, "launch": args.launch,
                        "threshold_bytes": w.threshold_bytes},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
@@ -482,8 +515,24 @@ def run_ours(args):
             per_dir = sum(b for r, b in enumerate(seg) if r != rank)
             line["nvlink"] = {"bytes_per_step_per_direction": per_dir,
                               "avg_GBps_per_direction": round(per_dir / (ms * 1e-3) / 1e9, 3),
-                              "peak_GBps_per_direction": 900.0}
+                              "peak_GBps_per_direction": 900.0,
+                              "source": "payload bytes of the other owners' segments (plan), not a counter; "
+                                        "ncu NVLink counters: profiles/r2/nvlink_*"}
+            # bus bandwidth per nccl-tests: the bytes a rank receives, P (n - 1) / n, over
+            # the exchange's own time; only where the exchange is its own launch (NCCL,
+            # or the sparse kinds' copy kernels) - the fused exchange has no such time
+            bus = {}
+            for k in ("push", "pull"):
+                if per[k][1]:
+                    bus[k + "_ms"] = round(per[k][0], 5)
+                    bus[k + "_busbw_GBps"] = round(per_dir / (per[k][0] * 1e-3) / 1e9, 2)
+            if bus:
+                line["bus"] = bus
         print(json.dumps(line), flush=True)
+    # the graphs hold the captured launches (NCCL kernels included): release them
+    # before the context's communicator and buffers go
+    run = graphs = None
+    torch.cuda.synchronize()
     ctx.finalize()
     if world > 1:
         dist.destroy_process_group()

@@ -1,6 +1,8 @@
 """Real multi-GPU parity: one process per GPU (torchrun), libbpc's exchange
 (bpc_aggregate; argv[2] = "p2p" NVLink peer stores or "nccl"), every rank
-checked against the CPU oracle on the same seeded inputs.  Launched by
+checked against the CPU oracle on the same seeded inputs.  argv[3] = "graph":
+steps 5-8 replay a CUDA graph of one whole step captured after step 4 (the
+step counter and exchange epochs advance on the device).  Launched by
 tests/test_gpu_multi.py; prints "RANK <r> <case> OK" per rank and case."""
 import os
 import sys
@@ -43,6 +45,9 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     names = sys.argv[1].split(",") if len(sys.argv) > 1 and sys.argv[1] else list(CASES)
     exchange = sys.argv[2] if len(sys.argv) > 2 else "p2p"
+    use_graph = len(sys.argv) > 3 and sys.argv[3] == "graph"
+    stream = torch.cuda.Stream(dev)   # capturable: the contexts borrow it
+    torch.cuda.set_stream(stream)
     for name in names:
         w = Config("mg", "custom", CASES[name], numels=SHAPES, n=world,
                    optimizer="lans" if name.startswith("lans") else "nag" if name.startswith("nag") else "adam",
@@ -62,13 +67,25 @@ def main():
         # host sync (ranks drift apart: the exchange's cross-step ordering), then
         # step 8 is checked
         dgrads = {step: torch.tensor(gen_grad(w, rank, step), device=dev) for step in range(4, 9)}
+        gstat = torch.zeros(D, dtype=torch.float32, device=dev)
+        graph = None
         torch.cuda.synchronize()
         for step in range(1, 9):
             gs = [gen_grad(w, i, step) for i in range(world)]
             delta, p, _ = oracle.round_(ocfg, ost, np.stack(gs), w.lr)
-            ctx.compress(dgrads[step] if step in dgrads else torch.tensor(gs[rank], device=dev))
-            ctx.aggregate()
-            ctx.step(x, w.lr)
+            if graph is not None:
+                gstat.copy_(dgrads[step])
+                graph.replay()
+            else:
+                ctx.compress(dgrads[step] if step in dgrads else torch.tensor(gs[rank], device=dev))
+                ctx.aggregate()
+                ctx.step(x, w.lr)
+            if use_graph and step == 4:
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph, stream=stream):
+                    ctx.compress(gstat)
+                    ctx.aggregate()
+                    ctx.step(x, w.lr)
             if step not in (1, 2, 3, 8):
                 continue
             ctx.sync()
@@ -107,6 +124,10 @@ def main():
                 a, bref = xs[off:off + L], ost.x[off:off + L]
                 rel = np.max(np.abs(a.astype(np.float64) - bref) / np.maximum(np.abs(bref), 1e-30))
                 assert rel <= 1e-6, f"{name} rank {rank}: x rel diff {rel}"
+        if use_graph:
+            assert ctx.t == 9, f"rank {rank}: t = {ctx.t} after 8 steps"
+        ctx.sync()
+        graph = None
         ctx.finalize()
         dist.barrier()
         print(f"RANK {rank} {name} OK", flush=True)

@@ -17,9 +17,10 @@ def _ngpus():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
+@pytest.mark.parametrize("launch", ["eager", "graph"])
 @pytest.mark.parametrize("exchange", ["p2p", "nccl"])
 @pytest.mark.parametrize("n", [2, 4, 8])
-def test_multi_parity(n, exchange):
+def test_multi_parity(n, exchange, launch):
     if _ngpus() < n:
         pytest.skip(f"needs {n} GPUs")
     import socket
@@ -29,7 +30,7 @@ def test_multi_parity(n, exchange):
     s.close()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(port),
-           os.path.join(ROOT, "tests", "multigpu_parity.py"), "", exchange]
+           os.path.join(ROOT, "tests", "multigpu_parity.py"), "", exchange, launch]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
