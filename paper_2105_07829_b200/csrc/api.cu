@@ -214,6 +214,7 @@ struct bpc_ctx {
   DevChunk* d_chunks = nullptr;
   uint32_t *d_witems = nullptr, *d_sitems = nullptr;
   Tile* d_utiles = nullptr;
+  uint2* d_ent = nullptr;     // sparse kinds: payload entries per 2048-element half tile
   uint32_t n_witems = 0, n_sitems = 0, n_utiles = 0;
   // sparse kinds (kernels_sparse.cu), per side (0 worker, 1 server): chunk -> unit,
   // candidate thresholds, counters, candidate lists
@@ -221,7 +222,7 @@ struct bpc_ctx {
   uint32_t* d_guess[2] = {nullptr, nullptr};
   uint32_t* d_scnt[2] = {nullptr, nullptr};         // candidates per slice (streaming pass)
   uint32_t* d_first_slice[2] = {nullptr, nullptr};  // per unit: its first slice
-  uint32_t* d_cand[2] = {nullptr, nullptr};
+  uint2* d_cand[2] = {nullptr, nullptr};
   uint32_t* d_cand_off[2] = {nullptr, nullptr};
   uint32_t sel_cap[2] = {0, 0};                  // CTA select kernel: candidates in shared memory
   uint32_t* d_big[2] = {nullptr, nullptr};       // units handed from the warp to the CTA select
@@ -383,7 +384,7 @@ void free_ctx(bpc_ctx* ctx) {
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   for (void* p : {(void*)ctx->e, (void*)ctx->etl, (void*)ctx->m, (void*)ctx->v, (void*)ctx->send,
                   (void*)ctx->pbuf, (void*)ctx->d_chunks, (void*)ctx->d_witems, (void*)ctx->d_sitems,
-                  (void*)ctx->d_utiles, (void*)ctx->d_flag, (void*)ctx->d_sdelta,
+                  (void*)ctx->d_utiles, (void*)ctx->d_ent, (void*)ctx->d_flag, (void*)ctx->d_sdelta,
                   (void*)ctx->d_chunk2u[0], (void*)ctx->d_chunk2u[1], (void*)ctx->d_guess[0], (void*)ctx->d_guess[1],
                   (void*)ctx->d_scnt[0], (void*)ctx->d_scnt[1], (void*)ctx->d_first_slice[0],
                   (void*)ctx->d_first_slice[1], (void*)ctx->d_cand[0], (void*)ctx->d_cand[1],
@@ -809,6 +810,8 @@ bpc_status bpc_init(const bpc_config* cfg, bpc_ctx** out) {
   if ((s = upload(ctx, &ctx->d_witems, witems)) != BPC_OK) return bail(s);
   if ((s = upload(ctx, &ctx->d_sitems, sitems)) != BPC_OK) return bail(s);
   if ((s = upload(ctx, &ctx->d_utiles, utiles)) != BPC_OK) return bail(s);
+  if (sparse_kind && (ce = alloc((void**)&ctx->d_ent, 16ull * utiles.size())) != cudaSuccess)
+    return bail(cuda_fail(ctx, ce, "alloc entry ranges"));
   ctx->n_witems = (uint32_t)witems.size();
   ctx->n_sitems = (uint32_t)sitems.size();
   if (sparse_kind) {
@@ -855,7 +858,7 @@ bpc_status bpc_init(const bpc_config* cfg, bpc_ctx** out) {
       if ((s = upload(ctx, &ctx->d_cand_off[side], off)) != BPC_OK) return bail(s);
       if ((s = upload(ctx, &ctx->d_first_slice[side], first)) != BPC_OK) return bail(s);
       if ((ce = alloc((void**)&ctx->d_guess[side], 4ull * items.size())) != cudaSuccess) return bail(cuda_fail(ctx, ce, "alloc guesses"));
-      if ((ce = alloc((void**)&ctx->d_cand[side], 4ull * off.back())) != cudaSuccess) return bail(cuda_fail(ctx, ce, "alloc candidates"));
+      if ((ce = alloc((void**)&ctx->d_cand[side], 8ull * off.back())) != cudaSuccess) return bail(cuda_fail(ctx, ce, "alloc candidates"));
       if ((ce = alloc((void**)&ctx->d_big[side], 4ull * items.size())) != cudaSuccess) return bail(cuda_fail(ctx, ce, "alloc select flags"));
     }
     if ((ce = alloc((void**)&ctx->d_sdelta, 4ull * sd_elems)) != cudaSuccess) return bail(cuda_fail(ctx, ce, "alloc Delta scratch"));
@@ -1293,10 +1296,14 @@ bpc_status bpc_step(bpc_ctx* ctx, float* d_params, float lr) {
     if (bpc_status st = launch_flag_wait(ctx, EP_PULL, "pull wait launch")) return st;
   }
   const bool sparse = c.comp.kind == BPC_TOP_K || c.comp.kind == BPC_RANDOM_K;
+  if (sparse) {   // each half tile's payload entries, for the update's scatter
+    p.ent = ctx->d_ent;
+    CK(launch_sparse_ranges(p, ctx->d_ent, ctx->stream), "entry ranges launch");
+    ctx->launches++;
+  }
   auto pass = [&](int mode) -> cudaError_t {
     p.mode = mode;
-    return sparse ? launch_update(c.comp.kind, p, ctx->stream)   // sparse decode: per-tile scatter
-                  : launch_update_stream(c.comp.kind, p, ctx->num_sms, ctx->stream);
+    return launch_update_stream(c.comp.kind, p, ctx->num_sms, ctx->stream);
   };
   if (c.optimizer == BPC_OPT_LANS) {
     // LANS (R22): m, v + per-tile block sums; per-block coefficients; x

@@ -94,6 +94,8 @@ struct UpdateParams {
   float mu;               // NAG momentum (mode 3, R24)
   double* lans_part;      // LANS pass 1: per update tile the pairwise sums of x^2, u^2, w^2
   const float2* lans_coef;  // LANS pass 2: per block (a, b) coefficients
+  const uint2* ent;       // sparse kinds: per 2048-element half tile (first payload entry, entries)
+                          // (sparse_ranges_kernel)
   PeerSync sync;          // fused exchange: wait for the owners' p (pull) ...
   const uint8_t* psrc[P2P_MAXJ];   // ... and read chunk payloads from psrc[owner] (P of each rank)
 };
@@ -150,7 +152,8 @@ struct StreamParams {
   const uint32_t* sp_chunk2u;
   const uint32_t* sp_guess;
   uint32_t* sp_scnt;          // candidates per slice (of this side's slice table)
-  uint32_t* sp_cand;          // unit u's list at sp_cand_off[u]: one sub-list of (cap / nslices) per slice
+  uint2* sp_cand;             // unit u's list at sp_cand_off[u]: one sub-list of (cap / nslices) per slice,
+                              // entries (index, select key)
   const uint32_t* sp_cand_off;
 };
 
@@ -170,7 +173,7 @@ struct SparseParams {
   const uint32_t* chunk2u;  // chunk -> unit index of this side
   uint32_t* guess;          // [n_units] candidate thresholds
   uint32_t* scnt;           // candidates per slice of this side's slice table (written by the streaming pass)
-  uint32_t* cand;           // candidate indices, unit u at [cand_off[u], cand_off[u + 1]): slice s of
+  uint2* cand;              // candidates (index, select key), unit u at [cand_off[u], cand_off[u + 1]): slice s of
                             // the unit owns the index-ordered sub-list [s cs, s cs + min(scnt, cs)),
                             // cs = (cand_off[u + 1] - cand_off[u]) / nslices
   const uint32_t* cand_off; // [n_units + 1]
@@ -257,6 +260,8 @@ cudaError_t launch_server_stream(int kind, const StreamParams& p, int grid, cuda
 cudaError_t launch_update_stream(int kind, const UpdateParams& p, int grid, cudaStream_t s);
 size_t cstream_smem();
 size_t update_stream_smem();
-cudaError_t launch_update(int kind, const UpdateParams& p, cudaStream_t s);
+// sparse kinds: p.ent of every half tile (binary searches of the tile bounds in
+// the chunk's ascending payload indices), before update_stream
+cudaError_t launch_sparse_ranges(const UpdateParams& p, uint2* ent, cudaStream_t s);
 
 }  // namespace bpc

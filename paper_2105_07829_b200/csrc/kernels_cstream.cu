@@ -672,10 +672,22 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
       uint32_t before = incl - cnt + wbefore;
       // sub-list of slice sidx: cs entries at cand_off[u] + sidx cs
       const uint32_t cs = d.sp_cs;
-      uint32_t* sub = p.sp_cand + p.sp_cand_off[u] + d.sidx * cs;
+      uint2* sub = p.sp_cand + p.sp_cand_off[u] + d.sidx * cs;
       const uint32_t j0 = d.start + 16 * lq;
+      const float* vq = reinterpret_cast<const float*>(val + lf);   // the lane's 16 values, element order
       for (uint32_t m = mask; m; m &= m - 1) {
-        if (before < cs) sub[before] = j0 + (uint32_t)(__ffs(m) - 1);
+        // each entry carries its key, so the select never gathers the unit's values
+        // (candidates are rare: the key is re-formed here, a Philox call for random-k)
+        const uint32_t bpos = (uint32_t)(__ffs(m) - 1), j = j0 + bpos;
+        uint32_t key;
+        if (KIND == C_TOPK) {
+          key = __float_as_uint(vq[bpos]) & 0x7fffffffu;
+        } else {
+          const uint4 w = philox4x32_10_rk(make_uint4(j >> 2, d.id, ep.t, (stage_id << 31) | rng_rank), p.rk);
+          const uint32_t e = j & 3u;
+          key = ~(e == 0 ? w.x : (e == 1 ? w.y : (e == 2 ? w.z : w.w)));
+        }
+        if (before < cs) sub[before] = make_uint2(j, key);
         before++;
       }
       if (threadIdx.x == 0) p.sp_scnt[d.gsl] = total;   // > cs: the list overflowed

@@ -16,8 +16,10 @@
 //                  pipeline of the norm kinds.  Worker: q = g + e (Alg. 4 l.5,
 //                  PAPER.md:241), e := q (bulk store), raw units copied.  Server:
 //                  reads Delta (e~ + the applied entries; 4 B/element), raw units
-//                  averaged.  Every element with key >= G_u joins the unit's
-//                  candidate list (gathered per slice, one global append).
+//                  averaged.  Every element with key >= G_u joins its slice's
+//                  index-ordered sub-list of the unit's candidates as (index,
+//                  key), so the select reads the lists contiguously and gathers
+//                  values only for the k selected elements.
 //   sparse_select  if the unit has k <= c <= cap candidates, every element
 //                  outside them has key < G <= T (the k-th largest key), so the
 //                  exact selection (keys desc, index asc, R9/R10) is a radix
@@ -304,42 +306,37 @@ __global__ void __launch_bounds__(32 * SW_WARPS) sparse_select_warp_kernel(const
   }
   float* V = const_cast<float*>(unit_values(p, c));
   uint8_t* pay = p.out + c.pay;
-  const uint32_t* cand = p.cand + p.cand_off[u];
-  // the sub-lists, concatenated in slice order (= index order): 8 slices at a time,
-  // two entries per lane and slice, 16 loads in flight (cs <= 2^13, but the
-  // counts are ~3x below cs: the lanes loop while a slice has more)
+  const uint2* cand = p.cand + p.cand_off[u];
+  // the sub-lists (index, key), concatenated in slice order (= index order): 8
+  // slices at a time, two entries per lane and slice, 16 loads in flight (cs <=
+  // 2^13, but the counts are ~3x below cs: the lanes loop while a slice has more)
   for (uint32_t s0 = 0; s0 < ns; s0 += 8) {
-    uint32_t v[16];
+    uint2 v[16];
 #pragma unroll
     for (int q = 0; q < 8; q++) {
       const uint32_t sl = s0 + q;
       const uint32_t n_sl = __shfl_sync(0xffffffffu, sc, sl & 31);
-      v[2 * q] = (sl < ns && lane < n_sl) ? cand[sl * cs + lane] : 0u;
-      v[2 * q + 1] = (sl < ns && lane + 32 < n_sl) ? cand[sl * cs + lane + 32] : 0u;
+      v[2 * q] = (sl < ns && lane < n_sl) ? cand[sl * cs + lane] : make_uint2(0u, 0u);
+      v[2 * q + 1] = (sl < ns && lane + 32 < n_sl) ? cand[sl * cs + lane + 32] : make_uint2(0u, 0u);
     }
 #pragma unroll
     for (int q = 0; q < 8; q++) {
       const uint32_t sl = s0 + q;
       const uint32_t n_sl = __shfl_sync(0xffffffffu, sc, sl & 31), b_sl = __shfl_sync(0xffffffffu, incl - sc, sl & 31);
       if (sl >= ns) continue;
-      if (lane < n_sl) s.idx[b_sl + lane] = v[2 * q];
-      if (lane + 32 < n_sl) s.idx[b_sl + lane + 32] = v[2 * q + 1];
-      for (uint32_t i = lane + 64; i < n_sl; i += 32) s.idx[b_sl + i] = cand[sl * cs + i];
-    }
-  }
-  __syncwarp();
-  // keys, value reads batched 8 deep
-  for (uint32_t i0 = 0; i0 < cnt; i0 += 256) {
-    float vv[8];
-#pragma unroll
-    for (int r = 0; r < 8; r++) {
-      const uint32_t i = i0 + 32 * r + lane;
-      vv[r] = (KIND == SP_TOPK && i < cnt) ? V[s.idx[i]] : 0.f;
-    }
-#pragma unroll
-    for (int r = 0; r < 8; r++) {
-      const uint32_t i = i0 + 32 * r + lane;
-      if (i < cnt) s.key[i] = sel_key<KIND>(vv[r], s.idx[i], p, c.id);
+      if (lane < n_sl) {
+        s.idx[b_sl + lane] = v[2 * q].x;
+        s.key[b_sl + lane] = v[2 * q].y;
+      }
+      if (lane + 32 < n_sl) {
+        s.idx[b_sl + lane + 32] = v[2 * q + 1].x;
+        s.key[b_sl + lane + 32] = v[2 * q + 1].y;
+      }
+      for (uint32_t i = lane + 64; i < n_sl; i += 32) {
+        const uint2 e = cand[sl * cs + i];
+        s.idx[b_sl + i] = e.x;
+        s.key[b_sl + i] = e.y;
+      }
     }
   }
   __syncwarp();
@@ -492,7 +489,7 @@ __global__ void __launch_bounds__(SE_NT) sparse_select_kernel(const __grid_const
   const bool scaled = KIND == SP_RANDK && p.randk_scaled;
   const float scale = (float)((double)L / (double)k);
   const uint32_t ns = unit_ns(c), cs = (p.cand_off[u + 1] - p.cand_off[u]) / ns;
-  const uint32_t* cand = p.cand + p.cand_off[u];
+  const uint2* cand = p.cand + p.cand_off[u];
   if (threadIdx.x < 32) {   // the sub-lists' offsets (ns <= 32)
     const uint32_t lane = threadIdx.x;
     const uint32_t sc = lane < ns ? p.scnt[p.first_slice[u] + lane] : 0u;
@@ -516,12 +513,11 @@ __global__ void __launch_bounds__(SE_NT) sparse_select_kernel(const __grid_const
     uint32_t* ck = sx + SC;
     for (uint32_t sl = 0; sl < ns; sl++) {
       const uint32_t b0 = sm.sbase[sl], n_sl = (sl + 1 < ns ? sm.sbase[sl + 1] : cnt) - b0;
-      for (uint32_t i = threadIdx.x; i < n_sl; i += SE_NT) ci[b0 + i] = cand[sl * cs + i];
-    }
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < cnt; i += SE_NT) {
-      const uint32_t j = ci[i];
-      ck[i] = sel_key<KIND>(KIND == SP_TOPK ? V[j] : 0.f, j, p, c.id);
+      for (uint32_t i = threadIdx.x; i < n_sl; i += SE_NT) {
+        const uint2 e = cand[sl * cs + i];
+        ci[b0 + i] = e.x;
+        ck[b0 + i] = e.y;
+      }
     }
     __syncthreads();
     T = block_kth_largest([&](uint32_t i) { return ck[i]; }, cnt, k, sm, &above);
@@ -603,8 +599,7 @@ __global__ void __launch_bounds__(256) sparse_large_hist(const __grid_constant__
       for (uint32_t sl = blockIdx.x; sl < ns; sl += gridDim.x) {
         const uint32_t n_sl = p.scnt[p.first_slice[u] + sl];
         for (uint32_t i = threadIdx.x; i < n_sl; i += 256) {
-          const uint32_t j = p.cand[p.cand_off[u] + sl * cs + i];
-          const uint32_t key = large_key<KIND>(p, c, V, j);
+          const uint32_t key = p.cand[p.cand_off[u] + sl * cs + i].y;
           hist_add(h, (key >> sh) & 255u, (key & pmask) == prefix);
         }
       }

@@ -47,6 +47,8 @@ constexpr int UST = 3;                      // stages
 
 struct UDesc {
   uint64_t off;    // flat element offset of the chunk
+  uint32_t e0, ne; // sparse kinds: the item's payload entries [e0, e0 + ne)
+  uint32_t k;      // sparse kinds: the chunk's k
   const uint8_t* pay;   // the chunk's payload (local P, or the owner's P over NVLink)
   uint32_t start;  // tile start (chunk-relative)
   uint32_t len;
@@ -100,7 +102,8 @@ __global__ void __launch_bounds__(SNT, T == UTILE ? 1 : 2) update_stream(const _
   const uint32_t n_items = p.n_tiles * SPLIT;
   const uint32_t mine = n_items > blockIdx.x ? (n_items - blockIdx.x + G - 1) / G : 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int b = KIND == S_SIGN ? 1 : (int)p.bits;
+  constexpr bool SPARSE = KIND == S_TOPK || KIND == S_RANDK;
+  const int b = (KIND == S_SIGN || SPARSE) ? 1 : (int)p.bits;
   if (threadIdx.x == 0) {
     for (int s = 0; s < UST; s++) {
       mbar_init(&sm.full[s], 1);
@@ -137,6 +140,12 @@ __global__ void __launch_bounds__(SNT, T == UTILE ? 1 : 2) update_stream(const _
         d.L = c.len;
         d.raw = c.raw;
         d.tile = item;
+        if (SPARSE) {   // the item's entries (T = UTILE: both halves of the tile)
+          const uint2 e = p.ent[SPLIT > 1 ? item : 2 * item];
+          d.e0 = e.x;
+          d.ne = SPLIT > 1 ? e.y : e.y + p.ent[2 * item + 1].y;
+          d.k = c.k;
+        }
         if (MODE == 2) {
           const float2 cf = p.lans_coef[tl.pad];   // Tile.pad = block (tensor) index
           d.ca = cf.x;
@@ -151,6 +160,10 @@ __global__ void __launch_bounds__(SNT, T == UTILE ? 1 : 2) update_stream(const _
         } else if (c.raw || KIND == S_NONE) {
           psrc = pay + 4ull * tl.start;
           pbytes = nvb;
+          d.pofs = 0;
+        } else if (SPARSE) {   // the consumers scatter the item's entries (L2-resident P)
+          psrc = pay;
+          pbytes = 0;
           d.pofs = 0;
         } else {
           const uint64_t s0 = 4 + (uint64_t)tl.start * b / 8;                  // first field byte
@@ -209,6 +222,21 @@ __global__ void __launch_bounds__(SNT, T == UTILE ? 1 : 2) update_stream(const _
     const uint32_t* words = reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(sm.pay[s]) + d.pofs);
     const float hdr = *reinterpret_cast<const float*>(&sm.head[s]);
     const float unit = fdiv(hdr, sl);
+    float* gts = reinterpret_cast<float*>(sm.pay[s]);   // sparse: the item's decoded g~ (T floats)
+    if (SPARSE && !d.raw && d.len) {
+      // zero the item, scatter its entries (indices ascending, inside [start, start + len)),
+      // then every thread reads its own float4s
+#pragma unroll
+      for (int k = 0; k < UK; k++) sm.pay[s][threadIdx.x + k * CNT] = make_float4(0.f, 0.f, 0.f, 0.f);
+      consumers_sync();
+      const uint32_t* idx = reinterpret_cast<const uint32_t*>(d.pay + 8);
+      const uint8_t* val = d.pay + 8 + 4ull * d.k;   // fp32, or binary16 values (R23)
+      for (uint32_t e = threadIdx.x; e < d.ne; e += CNT) {
+        const uint32_t q = d.e0 + e;
+        gts[idx[q] - d.start] = get_val(val, q, p.f16);
+      }
+      consumers_sync();
+    }
 #pragma unroll
     for (int k = 0; k < UK; k++) {
       const uint32_t f = threadIdx.x + k * CNT;   // float4 index inside the tile
@@ -223,6 +251,8 @@ __global__ void __launch_bounds__(SNT, T == UTILE ? 1 : 2) update_stream(const _
         const float h = hdr;
         const uint32_t nib = (words[f >> 3] >> ((f & 7) * 4)) & 15u;
         g4 = make_float4(nib & 1u ? h : -h, nib & 2u ? h : -h, nib & 4u ? h : -h, nib & 8u ? h : -h);
+      } else if (SPARSE) {
+        g4 = sm.pay[s][f];
       } else {
         const uint32_t field = load_field(words, (uint64_t)b * 4 * f, 4 * b);
 #pragma unroll
@@ -328,6 +358,9 @@ __global__ void __launch_bounds__(SNT, T == UTILE ? 1 : 2) update_stream(const _
         else store4_masked(x, j, d.L, x4);
       }
     }
+    if (SPARSE) {   // generic-proxy writes of pay[s] before the next bulk copy into it
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
     __syncwarp();
     if (lane == 0) {
       if (MODE == 1) mbar_arrive(&sm.sums[s]);    // red[s] written (release)
@@ -379,8 +412,49 @@ cudaError_t launch_update_stream(int kind, const UpdateParams& p, int grid, cuda
     case S_SIGN: return pick(std::integral_constant<int, S_SIGN>{});
     case S_LDITHER: return pick(std::integral_constant<int, S_LDITHER>{});
     case S_NDITHER: return pick(std::integral_constant<int, S_NDITHER>{});
+    case S_TOPK: return pick(std::integral_constant<int, S_TOPK>{});
+    case S_RANDK: return pick(std::integral_constant<int, S_RANDK>{});
   }
   return cudaErrorInvalidValue;
+}
+
+// one thread per 2048-element half tile: its entries in the chunk's ascending
+// payload indices, [lower_bound(start), lower_bound(start + len))
+__global__ void sparse_ranges_kernel(const __grid_constant__ UpdateParams p, uint2* ent) {
+  const uint32_t item = blockIdx.x * blockDim.x + threadIdx.x;
+  if (item >= 2 * p.n_tiles) return;
+  Tile tl = p.tiles[item >> 1];
+  const uint32_t s0 = (item & 1) * (UTILE / 2);
+  tl.len = tl.len > s0 ? min(tl.len - s0, (uint32_t)(UTILE / 2)) : 0u;
+  tl.start += s0;
+  const DevChunk c = p.chunks[tl.chunk];
+  if (c.raw || tl.len == 0) {
+    ent[item] = make_uint2(0u, 0u);
+    return;
+  }
+  const uint32_t* idx = reinterpret_cast<const uint32_t*>(p.pbuf + c.pay + 8);
+  auto lb = [&](uint32_t key) {
+    uint32_t lo = 0, n = c.k;
+    while (n > 0) {
+      const uint32_t h = n >> 1;
+      if (__ldg(idx + lo + h) < key) {
+        lo += h + 1;
+        n -= h + 1;
+      } else {
+        n = h;
+      }
+    }
+    return lo;
+  };
+  const uint32_t a = lb(tl.start), e = lb(tl.start + tl.len);
+  ent[item] = make_uint2(a, e - a);
+}
+
+cudaError_t launch_sparse_ranges(const UpdateParams& p, uint2* ent, cudaStream_t s) {
+  const uint32_t n = 2 * p.n_tiles;
+  if (!n) return cudaSuccess;
+  sparse_ranges_kernel<<<(n + 255) / 256, 256, 0, s>>>(p, ent);
+  return cudaGetLastError();
 }
 
 

@@ -14,5 +14,13 @@ done
 for spec in $3; do
   IFS=: read cfg kre skip cnt <<< "$spec"
   CMD="python bench.py --config $cfg --steps 3 --warmup 3 --no-e2e --no-cpu"
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:$kre -s $skip -c $cnt -o gpurun_out/iter_${cfg}_${kre} $CMD > gpurun_out/iter_ncu_${cfg}.log 2>&1; echo ncu$cfg=$?
+  R=gpurun_out/iter_${cfg}_${kre}
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:$kre -s $skip -c $cnt -o $R $CMD > gpurun_out/iter_ncu_${cfg}.log 2>&1; echo ncu$cfg=$?
+  # keep the exports (small); the report itself only if KEEP_REP is set
+  ncu -i $R.ncu-rep --page raw --csv > ${R}_raw.csv 2>/dev/null
+  ncu -i $R.ncu-rep --page details --csv > ${R}_details.csv 2>/dev/null
+  ncu -i $R.ncu-rep --page source --csv --print-source sass > ${R}_sass.csv 2>/dev/null
+  gzip -f ${R}_sass.csv
+  [ -z "$KEEP_REP" ] && rm -f $R.ncu-rep
 done
+du -sh gpurun_out
