@@ -92,7 +92,8 @@ struct __align__(128) CHead {
   double red[2][CCW];       // the consumer warps' 512-element subtrees of a slice
   uint32_t wcnt[2 * CCW];   // sparse kinds: candidates per consumer warp of the emitting slice (2 buffers)
   double part[CMAXH];
-  double total[CMAXH];
+  float4 dv[CMAXH];         // the slice's unit scalars from its total (reducer): sign (s);
+                            // dithering (N, RN(s_l / N) or 0, RN(N / s_l))
 };
 
 __device__ __forceinline__ void mbar_arrive1(uint64_t* bar) {
@@ -227,8 +228,12 @@ __device__ __forceinline__ float dither_mag(uint32_t code, float hdr, float unit
 // BITS: dithering bits as a compile-time constant (the paper's 3 / 5 / 7-bit runs,
 // every shift of the code packing is then an immediate), or 0 =
 // p.bits at run time
-template <int KIND, bool SERVER, bool FUSED, int BITS>
+// X: 0 plain, 1 FUSED (n > 1, BPC_EXCHANGE_P2P), 2 the server at n = 1 (N1: one
+// rank's payload, Delta = dec + e~ in fp32; the general n-rank code is not built)
+template <int KIND, bool SERVER, int X, int BITS>
 __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant__ StreamParams p) {
+  constexpr bool FUSED = X == 1;
+  constexpr bool N1 = SERVER && X == 2;
   extern __shared__ __align__(128) unsigned char sraw[];
   CHead& hd = *reinterpret_cast<CHead*>(sraw);
   const uint32_t NH = p.nstages;          // held stages
@@ -387,6 +392,20 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
   // ===================================================== reducers
   if (warp >= CRED) {
     if (SPARSE) return;   // no unit norm: the emit does not wait for a total
+    // the emit's scalars from the unit total, once per slice (not per lane):
+    // scaled sign s = fl32(||q||_1 / L); dithering N = fl32(sqrt(||q||^2))
+    // (R12), s_l / N and N / s_l with IEEE divisions
+    const float rslv = (float)((1u << ((BITS ? BITS : (int)p.bits) - 1)) - 1u);
+    auto publish = [&](uint32_t hs, double total) {
+      float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (KIND == C_SIGN) {
+        r.x = __double2float_rn(total / (double)hd.desc[hs].L);
+      } else if (KIND == C_LDITHER || KIND == C_NDITHER) {
+        const float N = __double2float_rn(sqrt(total));
+        r = make_float4(N, N != 0.f ? fdiv(rslv, N) : 0.f, fdiv(N, rslv), 0.f);
+      }
+      hd.dv[hs] = r;
+    };
     for (uint32_t i = warp - CRED; i < mine; i += CRW) {
       const uint32_t hs = i % NH;
       // slice i produced.  Cannot alias: slice i + NH needs stage hs back, which
@@ -398,7 +417,7 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
       if (ns > 1 && p.pass == 1) {   // per-tensor units, pass 1: publish the partial only
         if (lane == 0) p.partials[hd.desc[hs].unit_first + hd.desc[hs].sidx] = hd.part[hs];
       } else if (ns > 1 && p.pass == 2) {   // pass 2: the unit's total from unit_tree_kernel
-        if (lane == 0) hd.total[hs] = __ldcg(p.unit_total + hd.desc[hs].unit);
+        if (lane == 0) publish(hs, __ldcg(p.unit_total + hd.desc[hs].unit));
       } else if (ns > 1) {
         if (lane == 0) {
           // publish this slice's partial, then wait for the unit's other slices
@@ -418,9 +437,9 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
           v = (uint32_t)lane < ns ? __ldcg(P + lane) : 0.0;
         }
         v = warp_tree(v);
-        if (lane == 0) hd.total[hs] = v;
+        if (lane == 0) publish(hs, v);
       } else if (ns == 1 && lane == 0) {
-        hd.total[hs] = hd.part[hs];
+        publish(hs, hd.part[hs]);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive1(&hd.tready[hs]);
@@ -466,7 +485,7 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
     // server, n = 1: rank 0's field of the lane (sign: one half-word), read once
     U128 fld{0, 0};
     float h0 = 0.f;
-    if (SERVER && comp && p.n == 1 && lane_any) {
+    if (N1 && comp && lane_any) {
       h0 = *reinterpret_cast<const float*>(IH(t));
       const uint32_t* words = d.staged ? reinterpret_cast<const uint32_t*>(I(t) + d.pofs)
                                        : reinterpret_cast<const uint32_t*>(p.recv + d.recv + 4 +
@@ -511,7 +530,7 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
         wr = true;
         if (!comp) {   // raw unit: mean of the ranks' fp32 values (rank 0's staged in val)
           double acc[4] = {0.0, 0.0, 0.0, 0.0};
-          for (uint32_t r = 0; r < p.n; r++) {
+          for (uint32_t r = 0; r < (N1 ? 1u : p.n); r++) {
             const float4 x4 = (r == 0 && inv4)
                                   ? val[f]
                                   : load4_masked(reinterpret_cast<const float*>(p.recv + r * p.slot_bytes + d.recv), j, d.L);
@@ -524,7 +543,7 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
           if (FULL || j + 1 < d.L) q.y = mean_plus(acc[1], p.inv_n, 0.0);
           if (FULL || j + 2 < d.L) q.z = mean_plus(acc[2], p.inv_n, 0.0);
           if (FULL || j + 3 < d.L) q.w = mean_plus(acc[3], p.inv_n, 0.0);
-        } else if (p.n == 1) {
+        } else if (N1) {
           // n = 1: Delta = fl32(fl64(dec * 1.0) + fl64(e~)) equals the fp32 sum
           // fl32(dec + e~): the fp64 sum of two fp32 values is exact unless their
           // exponents differ by more than 29, and then both roundings return the
@@ -606,7 +625,7 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
 
   // ---------------- emit: payload (sign bits / codes) + error of a slice (into the
   // held stage; the producer bulk-stores it), raw units: ragged tail only
-  auto emit = [&](auto full_tag, const CDesc& d, float4* val, uint8_t* pay, double total) {
+  auto emit = [&](auto full_tag, const CDesc& d, float4* val, uint8_t* pay, const float4 dv) {
     constexpr bool FULL = decltype(full_tag)::value;
     const uint32_t L = d.L;
     const uint32_t nvec = d.len >> 2;
@@ -692,7 +711,7 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
       }
       if (threadIdx.x == 0) p.sp_scnt[d.gsl] = total;   // > cs: the list overflowed
     } else if (KIND == C_SIGN) {
-      const float sc = __double2float_rn(total / (double)L);
+      const float sc = dv.x;
       const float nsc = -sc;
       uint32_t m16 = 0;
 #pragma unroll
@@ -724,9 +743,7 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
         reinterpret_cast<uint32_t*>(pay + 4)[wi] = m16 | (other << 16);
       if (d.sidx == 0 && threadIdx.x == 0) *reinterpret_cast<float*>(pay) = sc;
     } else if (KIND == C_LDITHER || KIND == C_NDITHER) {
-      const float N = __double2float_rn(sqrt(total));
-      const float inv = N != 0.f ? fdiv(slv, N) : 0.f;
-      const float unit = fdiv(N, slv);
+      const float N = dv.x, inv = dv.y, unit = dv.z;
       U128 fld{0, 0};   // the lane's 16 codes in element order
 #pragma unroll
       for (int s = 0; s < 4; s++) {
@@ -826,13 +843,13 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
       // every slice (raw included) waits for its reducer before the stage is
       // recycled: keeps each mbarrier at most one phase ahead of its waiters
       if (!SPARSE) mbar_wait(&hd.tready[hs], ehb, 0x5000000u | ie);
-      const double total = hd.total[hs];
+      const float4 dv = hd.dv[hs];
       if (p.pass == 1) {
         // per-tensor units, pass 1: nothing to emit (pass 2 re-produces the slice)
       } else if (d.len == CSL) {
-        emit(BoolC<true>{}, d, H(hs), pay, total);
+        emit(BoolC<true>{}, d, H(hs), pay, dv);
       } else {
-        emit(BoolC<false>{}, d, H(hs), pay, total);
+        emit(BoolC<false>{}, d, H(hs), pay, dv);
       }
       fence_proxy_async();   // this thread's smem writes before the producer's bulk store
       __syncwarp();
@@ -900,20 +917,28 @@ static cudaError_t launch_cstream_t(int kind, StreamParams p, int grid, cudaStre
     return cudaLaunchKernelEx(&cfg, fn, p);
   };
   const bool fused = p.ndst > 0 || p.sync.wait_fam >= 0;
+  const int x = fused ? 1 : (SERVER && p.n == 1 ? 2 : 0);
+  auto pick = [&](auto k_tag, auto b_tag) -> cudaError_t {
+    constexpr int K = decltype(k_tag)::value, B = decltype(b_tag)::value;
+    if (x == 1) return go(cstream_kernel<K, SERVER, 1, B>);
+    if (SERVER && x == 2) return go(cstream_kernel<K, SERVER, SERVER ? 2 : 0, B>);
+    return go(cstream_kernel<K, SERVER, 0, B>);
+  };
   auto dither = [&](auto kind_tag) -> cudaError_t {
-    constexpr int K = decltype(kind_tag)::value;
     switch (p.bits) {
-      case 3: return fused ? go(cstream_kernel<K, SERVER, true, 3>) : go(cstream_kernel<K, SERVER, false, 3>);
-      case 5: return fused ? go(cstream_kernel<K, SERVER, true, 5>) : go(cstream_kernel<K, SERVER, false, 5>);
-      case 7: return fused ? go(cstream_kernel<K, SERVER, true, 7>) : go(cstream_kernel<K, SERVER, false, 7>);
+      case 3: return pick(kind_tag, std::integral_constant<int, 3>{});
+      case 5: return pick(kind_tag, std::integral_constant<int, 5>{});
+      case 7: return pick(kind_tag, std::integral_constant<int, 7>{});
     }
-    return fused ? go(cstream_kernel<K, SERVER, true, 0>) : go(cstream_kernel<K, SERVER, false, 0>);
+    return pick(kind_tag, std::integral_constant<int, 0>{});
   };
   switch (kind) {
-    case C_NONE: return fused ? go(cstream_kernel<C_NONE, SERVER, true, 0>) : go(cstream_kernel<C_NONE, SERVER, false, 0>);
-    case C_SIGN: return fused ? go(cstream_kernel<C_SIGN, SERVER, true, 0>) : go(cstream_kernel<C_SIGN, SERVER, false, 0>);
-    case C_TOPK: return go(cstream_kernel<C_TOPK, SERVER, false, 0>);     // sparse: no fused exchange
-    case C_RANDK: return go(cstream_kernel<C_RANDK, SERVER, false, 0>);
+    case C_NONE: return pick(std::integral_constant<int, C_NONE>{}, std::integral_constant<int, 0>{});
+    case C_SIGN: return pick(std::integral_constant<int, C_SIGN>{}, std::integral_constant<int, 0>{});
+    case C_TOPK:   // sparse: no fused exchange
+      return x == 2 ? go(cstream_kernel<C_TOPK, SERVER, SERVER ? 2 : 0, 0>) : go(cstream_kernel<C_TOPK, SERVER, 0, 0>);
+    case C_RANDK:
+      return x == 2 ? go(cstream_kernel<C_RANDK, SERVER, SERVER ? 2 : 0, 0>) : go(cstream_kernel<C_RANDK, SERVER, 0, 0>);
     case C_LDITHER: return dither(std::integral_constant<int, C_LDITHER>{});
     case C_NDITHER: return dither(std::integral_constant<int, C_NDITHER>{});
   }
