@@ -134,6 +134,7 @@ struct StreamParams {
   uint32_t stage_payload;   // server: stage the n ranks' payload pieces in smem
   uint32_t piece_stride;    // server: bytes per staged piece
   uint32_t nstages, stage_a, stage_b;   // ring geometry (set by the launcher)
+  uint32_t defer;                       // emit deferral D (set by the launcher)
   uint32_t rk[20];          // Philox round keys of the seed (set by the launcher, R13)
   // per-tensor units (NEXT #4): two passes.  pass 0: single pass
   // (units <= 32 slices, cross-CTA unit totals); pass 1: produce + publish the

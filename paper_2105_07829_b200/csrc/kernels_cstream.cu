@@ -43,6 +43,7 @@
 // deadlock.  Each mbarrier has a single in-order waiter group; the reducers,
 // run out of order (slice i -> reducer i % 4) but each waits on its slice's
 // held-stage barrier, which cannot run a phase ahead of it.
+#include <cstdlib>
 #include <type_traits>
 
 #include "device.cuh"
@@ -59,7 +60,8 @@ constexpr int CRW = 4;                   // reducer warps (slice i -> reducer i 
 constexpr int CSNT = CCNT + 32 + 32 * CRW;   // + producer + reducers
 constexpr int CMAXH = 8;                 // max held stages
 constexpr int CNI = 2;                   // input stages
-constexpr int CMAXD = 3;                 // max emit deferral
+constexpr int CMAXD = 3;                 // max emit deferral (D = 4 measured slower for the server)
+constexpr int CRED_R = CMAXD + 1;        // ring of the consumer warps' slice subtrees (>= D + 1)
 constexpr int CSL = 8192;                // elements per slice
 constexpr int CLE = 16;                  // elements per consumer lane per slice
 constexpr int CUNITSL = (1 << 18) / CSL; // max slices per unit (32)
@@ -89,7 +91,7 @@ struct __align__(128) CHead {
   uint64_t pready[CMAXH];   // slice in held stage s produced (its reducer waits on it)
   uint64_t pfin;            // fused exchange: the producer's last bulk store has completed
   CDesc desc[CMAXH];
-  double red[2][CCW];       // the consumer warps' 512-element subtrees of a slice
+  double red[CRED_R][CCW];  // the consumer warps' 512-element subtrees of slice i at i % CRED_R
   uint32_t wcnt[2 * CCW];   // sparse kinds: candidates per consumer warp of the emitting slice (2 buffers)
   double part[CMAXH];
   float4 dv[CMAXH];         // the slice's unit scalars from its total (reducer): sign (s);
@@ -237,7 +239,7 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
   extern __shared__ __align__(128) unsigned char sraw[];
   CHead& hd = *reinterpret_cast<CHead*>(sraw);
   const uint32_t NH = p.nstages;          // held stages
-  const uint32_t D = NH - 2 < (uint32_t)CMAXD ? NH - 2 : (uint32_t)CMAXD;   // emit deferral
+  const uint32_t D = p.defer;              // emit deferral, <= NH - 2 and <= CMAXD
   const uint32_t SI = p.stage_b;          // bytes per input stage
   const uint32_t SIE = p.stage_a;         // byte offset of the e region inside an input stage
   unsigned char* held = sraw + sizeof(CHead);
@@ -261,7 +263,7 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
     for (uint32_t s = 0; s < NH; s++) {
       mbar_init(&hd.emptyH[s], CCW);
       mbar_init(&hd.tready[s], 1);
-      mbar_init(&hd.pready[s], 1);
+      mbar_init(&hd.pready[s], SPARSE ? 1 : CCW);   // every consumer warp (its subtree, its q)
     }
     for (uint32_t t = 0; t < (uint32_t)CNI; t++) {
       mbar_init(&hd.fullI[t], 1);
@@ -414,6 +416,13 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
       // keeps the waiting warps off the issue slots the consumers need
       mbar_wait_backoff(&hd.pready[hs], (i / NH) & 1, 1000, 0x2000000u | i);
       const uint32_t ns = SPARSE ? 0u : hd.desc[hs].nslices;   // sparse kinds: no unit norm
+      if (ns > 0) {   // the slice partial: pairwise tree over the 16 consumer warps' subtrees
+        double r = lane < CCW ? hd.red[i % CRED_R][lane] : 0.0;
+#pragma unroll
+        for (int m = 1; m < CCW; m <<= 1) r = r + __shfl_xor_sync(0xffffffffu, r, m);
+        if (lane == 0) hd.part[hs] = r;
+        __syncwarp();
+      }
       if (ns > 1 && p.pass == 1) {   // per-tensor units, pass 1: publish the partial only
         if (lane == 0) p.partials[hd.desc[hs].unit_first + hd.desc[hs].sidx] = hd.part[hs];
       } else if (ns > 1 && p.pass == 2) {   // pass 2: the unit's total from unit_tree_kernel
@@ -619,7 +628,10 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
       const bool odd = rot & 1u;
       const double x1 = odd ? lv[3] : lv[1], y1 = odd ? lv[1] : lv[3];
       const double a = warp_tree((lv[0] + x1) + (lv[2] + y1));   // the warp's 512 elements
-      if (lane == 0) hd.red[i & 1][warp] = a;
+      // slot i % CRED_R is free: its previous slice i - CRED_R was emitted by this
+      // warp (iteration i - 1 emitted slice i - 1 - D >= i - CRED_R, in order),
+      // which waited for that slice's reducer
+      if (lane == 0) hd.red[i % CRED_R][warp] = a;
     }
   };
 
@@ -821,16 +833,9 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
         ph = 0;
         phb ^= 1;
       }
-      if (!SPARSE) cons_sync();                       // all q written, red complete
-      if (warp == 0 && !SPARSE) {
-        if (comp && !SPARSE) {   // the slice partial: pairwise tree over the 16 warp subtrees
-          double r = lane < CCW ? hd.red[i & 1][lane] : 0.0;
-#pragma unroll
-          for (int m = 1; m < CCW; m <<= 1) r = r + __shfl_xor_sync(0xffffffffu, r, m);
-          if (lane == 0) hd.part[hs] = r;   // the slice's reducer publishes it
-        }
-        if (lane == 0) mbar_arrive1(&hd.pready[hs]);   // release: q and part[hs] visible to the reducer
-      }
+      // release: this warp's subtree (and q) to the slice's reducer, which forms the
+      // slice partial; the consumer warps never wait for each other
+      if (!SPARSE && lane == 0) mbar_arrive1(&hd.pready[hs]);
     }
     // ---------------- emit slice i - D
     if (i >= D) {
@@ -899,6 +904,16 @@ static cudaError_t launch_cstream_t(int kind, StreamParams p, int grid, cudaStre
     p.rk[2 * r + 1] = (uint32_t)(p.seed >> 32) + (uint32_t)r * 0xBB67AE85u;
   }
   if (p.nstages < 3) return cudaErrorInvalidConfiguration;   // deferral >= 1 needs 3 held stages
+  {
+    // D = NH - 2 <= CMAXD for the norm kinds (the emit waits for the unit total);
+    // 1 for the sparse kinds, which wait for nothing (measured: C3 1.101 ms at
+    // D = 1, 1.123 at D = 3); BPC_CSTREAM_DEFER overrides it for measurements
+    uint32_t dmax = (kind == C_TOPK || kind == C_RANDK) ? 1u : (uint32_t)CMAXD;
+    if (const char* e = getenv("BPC_CSTREAM_DEFER")) dmax = (uint32_t)atoi(e);
+    if (dmax < 1) dmax = 1;
+    if (dmax > (uint32_t)CMAXD) dmax = CMAXD;
+    p.defer = std::min<uint32_t>(p.nstages - 2, dmax);
+  }
   auto go = [&](auto fn) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
