@@ -47,8 +47,9 @@ def parse():
     ap.add_argument("--config", default="C5",
                     help="workload (BASELINE.json configs): C5 BERT-large = the largest single-GPU config, the "
                          "metric's default; C2 ResNet-50, C3 VGG16, C4 BERT-base, C1 d=4096")
-    ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
-                    help="N>1 transport of the push/pull exchange: NVLink peer stores or NCCL send/recv")
+    ap.add_argument("--exchange", choices=["p2p", "nccl", "nvls"], default="p2p",
+                    help="N>1 transport of the push/pull exchange: NVLink peer stores, NCCL send/recv, or "
+                         "peer stores + an NVLS multicast pull")
     ap.add_argument("--optimizer", choices=["adam", "lans", "nag"], default="adam",
                     help="bpc_step update: Adam core (A9), the LANS / CLAN block-normalised update (NEXT #1) "
                          "or NAG (the CNN runs' optimizer, R24)")

@@ -114,9 +114,10 @@ typedef struct {
   float momentum;                /* NAG: mu in [0, 1) */
   int32_t unit_mode;             /* compression unit: 0 = chunks of chunk_elems (R1); 1 = one unit
                                     per tensor, the paper's granularity (NEXT #4),
-                                    scaled sign / dithering / NONE only, tensors <= 2^27 elements:
-                                    worker and server then run two passes (slice partials, a
-                                    per-unit tree, the emitting pass; 20 B/element for onebit+EF) */
+                                    tensors <= 2^27 elements: scaled sign / dithering / NONE run
+                                    two passes (slice partials, a per-unit tree, the emitting pass;
+                                    20 B/element for onebit+EF); top-k / random-k units longer
+                                    than 2^18 take a multi-CTA radix select over the unit */
 } bpc_config;
 
 /* The update of bpc_step (A9).
@@ -153,7 +154,18 @@ typedef enum { BPC_OPT_ADAM = 0, BPC_OPT_LANS = 1, BPC_OPT_NAG = 2 } bpc_optimiz
  *   If the peer mappings cannot be opened on every rank, init falls back to
  *   BPC_EXCHANGE_NCCL (bpc_get_exchange reports what is in use).
  * BPC_EXCHANGE_NCCL: grouped ncclSend/ncclRecv (all-to-all, all-gather). */
-typedef enum { BPC_EXCHANGE_P2P = 0, BPC_EXCHANGE_NCCL = 1 } bpc_exchange_mode;
+/* BPC_EXCHANGE_NVLS: BPC_EXCHANGE_P2P with the pull (A8) through NVLink SHARP
+ * multicast: P is a VMM allocation bound to one multicast
+ * object over the ranks' devices; the server kernel stores each owned unit's p
+ * once through the multicast mapping (multimem.st), the switch writes it into
+ * every rank's P, and the update kernel reads every p from local HBM.  Set up
+ * at bpc_init (collective: rank 0 creates the object and hands its POSIX fd to
+ * the other processes over an abstract unix socket) or bpc_connect_local
+ * (distinct devices); it applies to the fused kinds (scaled sign, dithering,
+ * NONE).  Where multicast is unavailable (no NVSwitch multicast support, a
+ * shared device, a failed step on any rank) the group keeps BPC_EXCHANGE_P2P;
+ * bpc_get_exchange reports BPC_EXCHANGE_NVLS only when it is in use. */
+typedef enum { BPC_EXCHANGE_P2P = 0, BPC_EXCHANGE_NCCL = 1, BPC_EXCHANGE_NVLS = 2 } bpc_exchange_mode;
 
 typedef struct bpc_ctx bpc_ctx;
 

@@ -29,7 +29,7 @@ def context_for(wcfg, *, rank=0, world_size=None, device=0, stream=None, nccl_id
                       chunk_elems=wcfg.chunk_elems or (1 << 18), unit_mode=1 if wcfg.chunk_elems == 0 else 0,
                       threshold_bytes=wcfg.threshold_bytes, beta1=wcfg.beta1,
                       beta2=wcfg.beta2, eps=wcfg.eps, weight_decay=wcfg.weight_decay,
-                      check_finite=check_finite, exchange={"p2p": 0, "nccl": 1}[exchange],
+                      check_finite=check_finite, exchange={"p2p": 0, "nccl": 1, "nvls": 2}[exchange],
                       optimizer={"adam": 0, "lans": 1, "nag": 2}[getattr(wcfg, "optimizer", "adam")],
                       lans_alpha_l=getattr(wcfg, "alpha_l", 0.01), lans_alpha_u=getattr(wcfg, "alpha_u", 10.0),
                       momentum=getattr(wcfg, "momentum", 0.9))

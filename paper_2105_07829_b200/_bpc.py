@@ -22,7 +22,7 @@ BUF_SEND, BUF_RECV, BUF_P, BUF_WORKER_ERR, BUF_SERVER_ERR, BUF_M, BUF_V = range(
 TIMER_NAMES = ("compress", "server", "update", "push", "pull")
 EXCHANGE_P2P, EXCHANGE_NCCL = 0, 1
 OPT_ADAM, OPT_LANS, OPT_NAG = 0, 1, 2
-EXCHANGE_NAMES = ("p2p", "nccl")
+EXCHANGE_NAMES = ("p2p", "nccl", "nvls")
 
 
 class BpcError(RuntimeError):

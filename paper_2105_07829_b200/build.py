@@ -16,8 +16,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libbpc.so")
-SOURCES = ["kernels_sparse.cu", "kernels_update.cu", "kernels_stream.cu", "kernels_cstream.cu", "kernels_p2p.cu", "api.cu"]
-HEADERS = ["device.cuh", "kernels.h", os.path.join("..", "..", "include", "bpc.h")]
+SOURCES = ["kernels_sparse.cu", "kernels_update.cu", "kernels_stream.cu", "kernels_cstream.cu", "kernels_p2p.cu", "nvls.cu",
+           "api.cu"]
+HEADERS = ["device.cuh", "kernels.h", "nvls.h", os.path.join("..", "..", "include", "bpc.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

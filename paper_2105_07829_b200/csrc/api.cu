@@ -14,6 +14,11 @@
 
 #include "bpc.h"
 #include "kernels.h"
+#include "nvls.h"
+
+#include <unistd.h>
+
+#include <memory>
 
 namespace {
 using namespace bpc;
@@ -88,7 +93,7 @@ bpc_status make_plan(const bpc_config* cfg, Plan* P, std::string* err) {
     return fail(BPC_ERR_INVALID_ARGUMENT, "betas must lie in (0, 1)");
   if (!(cfg->eps >= 0.f) || !(cfg->weight_decay >= 0.f))
     return fail(BPC_ERR_INVALID_ARGUMENT, "eps and weight_decay must be >= 0");
-  if (cfg->exchange != BPC_EXCHANGE_P2P && cfg->exchange != BPC_EXCHANGE_NCCL)
+  if (cfg->exchange != BPC_EXCHANGE_P2P && cfg->exchange != BPC_EXCHANGE_NCCL && cfg->exchange != BPC_EXCHANGE_NVLS)
     return fail(BPC_ERR_INVALID_ARGUMENT, "unknown exchange mode");
   if (cfg->optimizer != BPC_OPT_ADAM && cfg->optimizer != BPC_OPT_LANS && cfg->optimizer != BPC_OPT_NAG)
     return fail(BPC_ERR_INVALID_ARGUMENT, "unknown optimizer");
@@ -257,6 +262,14 @@ struct bpc_ctx {
   std::vector<uint8_t*> peer_recv, peer_p;
   std::vector<unsigned long long*> peer_flags;
   bool local_group = false;   // bpc_connect_local: peers are contexts of this process (direct pointers)
+  // BPC_EXCHANGE_NVLS: P bound to a multicast object (nvls.cu); the server
+  // stores p through pbuf_mc, every rank reads it from its own P
+  bool nvls = false;
+  NvlsMap nv;
+  std::shared_ptr<uint64_t> nv_mc;   // the multicast handle (released with the last reference)
+  uint8_t* pbuf_mc = nullptr;
+  uint8_t* pbuf_cm = nullptr;        // the cudaMalloc'd P the NVLS one replaced
+  uint8_t uid[128] = {};             // the NCCL unique id (names the handle socket)
   // LANS (BPC_OPT_LANS): per update tile partial sums, per block coefficients
   double* d_lans_part = nullptr;
   // per-tensor units (unit_mode 1): per side, unit tables and totals
@@ -381,6 +394,11 @@ void free_ctx(bpc_ctx* ctx) {
     if (q) cudaFree(q);
   for (void* q : {(void*)ctx->d_st, (void*)ctx->d_bct})
     if (q) cudaFree(q);
+  if (ctx->nvls) {   // P is the unicast mapping of the multicast-bound allocation
+    nvls_release(&ctx->nv);
+    ctx->nv_mc.reset();
+    ctx->pbuf = ctx->pbuf_cm;
+  }
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   for (void* p : {(void*)ctx->e, (void*)ctx->etl, (void*)ctx->m, (void*)ctx->v, (void*)ctx->send,
                   (void*)ctx->pbuf, (void*)ctx->d_chunks, (void*)ctx->d_witems, (void*)ctx->d_sitems,
@@ -426,10 +444,92 @@ void finish_p2p(bpc_ctx* ctx) {
 // exists): export RECV, P and the flag array as CUDA IPC handles, all-gather
 // them over NCCL, open the peers' handles, and agree (all-reduce min) that every
 // rank could open all of them.  Any failure leaves the context on NCCL.
+// min over ranks of v (NCCL all-reduce on the context's stream); false if the
+// collective itself failed
+bool agree_min(bpc_ctx* ctx, int32_t* v) {
+  int32_t* d = nullptr;
+  bool ok = cudaMalloc((void**)&d, 4) == cudaSuccess && cudaMemcpy(d, v, 4, cudaMemcpyHostToDevice) == cudaSuccess &&
+            ncclAllReduce(d, d, 1, ncclInt32, ncclMin, ctx->comm, ctx->stream) == ncclSuccess &&
+            cudaStreamSynchronize(ctx->stream) == cudaSuccess && cudaMemcpy(v, d, 4, cudaMemcpyDeviceToHost) == cudaSuccess;
+  if (d) cudaFree(d);
+  (void)cudaGetLastError();
+  return ok;
+}
+
+// swap P for the unicast mapping of a multicast-bound allocation
+void nvls_adopt(bpc_ctx* ctx, const NvlsMap& m, std::shared_ptr<uint64_t> mc) {
+  ctx->nvls = true;
+  ctx->nv = m;
+  ctx->nv_mc = std::move(mc);
+  ctx->pbuf_cm = ctx->pbuf;
+  ctx->pbuf = reinterpret_cast<uint8_t*>(m.uc);
+  ctx->pbuf_mc = reinterpret_cast<uint8_t*>(m.mc);
+  cudaMemset(ctx->pbuf, 0, m.size);
+}
+
+std::shared_ptr<uint64_t> mc_ref(uint64_t h) {
+  return std::shared_ptr<uint64_t>(new uint64_t(h), [](uint64_t* p) {
+    nvls_release_handle(*p);
+    delete p;
+  });
+}
+
+// BPC_EXCHANGE_NVLS between processes (collective): rank 0 creates the multicast
+// object and serves its fd over an abstract unix socket named after the NCCL
+// unique id; every rank adds its device, then binds and maps its P.  Every
+// step is agreed over the communicator: all ranks adopt it or none does.
+void setup_nvls_mp(bpc_ctx* ctx) {
+  const int n = ctx->cfg.world_size, rank = ctx->cfg.rank, dev = ctx->cfg.device;
+  std::string err;
+  char tag[48];
+  uint64_t h0 = 1469598103934665603ull;   // FNV-1a of the unique id
+  for (int i = 0; i < 128; i++) h0 = (h0 ^ ctx->uid[i]) * 1099511628211ull;
+  snprintf(tag, sizeof(tag), "%016llx", (unsigned long long)h0);
+  int32_t ok = nvls_supported(dev) ? 1 : 0;
+  uint64_t size = 0;
+  if (ok && !nvls_size(n, dev, ctx->plan.send_bytes, &size, &err)) ok = 0;
+  if (!agree_min(ctx, &ok) || !ok) return;
+  uint64_t mc = 0;
+  int fd = -1, lsock = -1;
+  if (rank == 0) {
+    ok = nvls_create(n, size, &mc, &err) && nvls_export(mc, &fd, &err) && (lsock = fd_listen(tag, &err)) >= 0;
+  }
+  if (!agree_min(ctx, &ok) || !ok) {   // rank 0 is listening (or nobody proceeds)
+    if (lsock >= 0) close(lsock);
+    if (fd >= 0) close(fd);
+    if (mc) nvls_release_handle(mc);
+    return;
+  }
+  if (rank == 0) {
+    ok = fd_serve(lsock, fd, n - 1, &err) ? 1 : 0;
+    close(lsock);
+    close(fd);
+  } else {
+    fd = fd_fetch(tag, 30.0, &err);
+    ok = fd >= 0 && nvls_import(fd, &mc, &err);
+    if (fd >= 0) close(fd);
+  }
+  std::shared_ptr<uint64_t> ref = mc ? mc_ref(mc) : nullptr;
+  if (ok && !nvls_add_device(mc, dev, &err)) ok = 0;
+  if (!agree_min(ctx, &ok) || !ok) return;   // every device added before any bind
+  NvlsMap m;
+  if (!nvls_bind_map(mc, dev, size, &m, &err)) ok = 0;
+  int32_t all = ok;
+  if (!agree_min(ctx, &all) || !all) {
+    nvls_release(&m);
+    if (!err.empty()) ctx->err = "NVLS setup: " + err;
+    return;
+  }
+  nvls_adopt(ctx, m, ref);
+}
+
 bpc_status setup_p2p(bpc_ctx* ctx) {
   const int n = ctx->cfg.world_size, rank = ctx->cfg.rank;
   const Plan& P = ctx->plan;
   cudaError_t ce;
+  // the multicast pull (fused kinds only: the sparse kinds' copy kernels write
+  // into the peers' P)
+  if (ctx->cfg.exchange == BPC_EXCHANGE_NVLS && stream_worker(ctx->cfg.comp.kind)) setup_nvls_mp(ctx);
   CK(cudaMalloc((void**)&ctx->d_xflags, 16ull * n), "alloc exchange flags");
   CK(cudaMemset(ctx->d_xflags, 0, 16ull * n), "zero exchange flags");
   struct Rec {
@@ -439,9 +539,11 @@ bpc_status setup_p2p(bpc_ctx* ctx) {
   };
   Rec mine = {};
   mine.ok = n <= P2P_MAXJ;
-  void* bufs[3] = {ctx->recv, ctx->pbuf, ctx->d_xflags};
+  // (with NVLS nobody reads a peer's P: it is not exported, and a VMM allocation
+  // could not be)
+  void* bufs[3] = {ctx->recv, ctx->nvls ? nullptr : ctx->pbuf, ctx->d_xflags};
   for (int i = 0; i < 3 && mine.ok; i++)
-    if (cudaIpcGetMemHandle(&mine.h[i], bufs[i]) != cudaSuccess) mine.ok = 0;
+    if (bufs[i] && cudaIpcGetMemHandle(&mine.h[i], bufs[i]) != cudaSuccess) mine.ok = 0;
   (void)cudaGetLastError();
   uint8_t* d_all = nullptr;
   int32_t* d_ok = nullptr;
@@ -474,7 +576,9 @@ bpc_status setup_p2p(bpc_ctx* ctx) {
       if (q == rank) continue;
       void* ptr[3] = {nullptr, nullptr, nullptr};
       for (int i = 0; i < 3 && ok; i++)
-        if (cudaIpcOpenMemHandle(&ptr[i], all[q].h[i], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) ok = 0;
+        if ((i != 1 || !ctx->nvls) &&
+            cudaIpcOpenMemHandle(&ptr[i], all[q].h[i], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+          ok = 0;
       ctx->peer_recv[q] = (uint8_t*)ptr[0];
       ctx->peer_p[q] = (uint8_t*)ptr[1];
       ctx->peer_flags[q] = (unsigned long long*)ptr[2];
@@ -963,12 +1067,14 @@ bpc_status bpc_init(const bpc_config* cfg, bpc_ctx** out) {
   if (cfg->nccl_unique_id && n > 1) {
     ncclUniqueId id;
     memcpy(&id, cfg->nccl_unique_id, 128);
+    memcpy(ctx->uid, cfg->nccl_unique_id, 128);
     ncclResult_t r = ncclCommInitRank(&ctx->comm, (int)n, id, (int)rank);
     if (r != ncclSuccess) {
       ctx->comm = nullptr;
       return bail(BPC_ERR_NCCL);
     }
-    if (cfg->exchange == BPC_EXCHANGE_P2P && (s = setup_p2p(ctx)) != BPC_OK) return bail(s);
+    if ((cfg->exchange == BPC_EXCHANGE_P2P || cfg->exchange == BPC_EXCHANGE_NVLS) && (s = setup_p2p(ctx)) != BPC_OK)
+      return bail(s);
   }
   *out = ctx;
   return BPC_OK;
@@ -1012,6 +1118,35 @@ bpc_status bpc_connect_local(bpc_ctx* const* ctxs, int32_t n) {
     if (!ctx->d_xflags) {
       CK(cudaMalloc((void**)&ctx->d_xflags, 16ull * n), "alloc exchange flags");
       CK(cudaMemset(ctx->d_xflags, 0, 16ull * n), "zero exchange flags");
+    }
+  }
+  // BPC_EXCHANGE_NVLS: one multicast object over the group's devices (distinct
+  // devices only; otherwise the group keeps the peer reads of p)
+  bool want = stream_worker(ctxs[0]->cfg.comp.kind);
+  for (int r = 0; r < n && want; r++) {
+    want = ctxs[r]->cfg.exchange == BPC_EXCHANGE_NVLS && nvls_supported(ctxs[r]->cfg.device);
+    for (int q = 0; q < r && want; q++) want = ctxs[q]->cfg.device != ctxs[r]->cfg.device;
+  }
+  if (want) {
+    std::string err;
+    uint64_t size = 0, mc = 0;
+    bool ok = nvls_size(n, ctxs[0]->cfg.device, ctxs[0]->plan.send_bytes, &size, &err) &&
+              nvls_create(n, size, &mc, &err);
+    std::shared_ptr<uint64_t> ref = ok ? mc_ref(mc) : nullptr;
+    for (int r = 0; r < n && ok; r++) ok = nvls_add_device(mc, ctxs[r]->cfg.device, &err);
+    std::vector<NvlsMap> maps(n);
+    for (int r = 0; r < n && ok; r++) {
+      DeviceGuard dg(ctxs[r]->cfg.device);
+      ok = nvls_bind_map(mc, ctxs[r]->cfg.device, size, &maps[r], &err);
+    }
+    if (ok) {
+      for (int r = 0; r < n; r++) {
+        DeviceGuard dg(ctxs[r]->cfg.device);
+        nvls_adopt(ctxs[r], maps[r], ref);
+      }
+    } else {
+      for (int r = 0; r < n; r++) nvls_release(&maps[r]);
+      ctxs[0]->err = "NVLS setup: " + err;   // informational: the group keeps the peer reads
     }
   }
   for (int r = 0; r < n; r++) {
@@ -1181,6 +1316,7 @@ bpc_status bpc_server(bpc_ctx* ctx) {
     if (fused_exchange(ctx)) {   // wait for every rank's push; p stays in the local P; signal
       set_wait(ctx, &q.sync, EP_PUSH);
       set_signal(ctx, &q.sync, EP_PULL);
+      if (ctx->nvls) q.mc_out = ctx->pbuf_mc;   // ... or goes to every rank's P (multicast)
       if (ctx->n_sslices == 0) {   // owns no chunk: no server launch, only the signal
         P2PParams e = {};
         e.sync = peer_sync(ctx, EP_PULL);
@@ -1288,7 +1424,8 @@ bpc_status bpc_step(bpc_ctx* ctx, float* d_params, float lr) {
   p.sync = peer_sync(ctx, EP_UPDATE);
   if (fused_exchange(ctx)) {   // wait for every owner's p, then read it from the owner's P
     set_wait(ctx, &p.sync, EP_PULL);
-    for (int r = 0; r < c.world_size; r++) p.psrc[r] = ctx->peer_p[r];
+    // NVLS: the server multicast p into every rank's P, so every owner's p is local
+    for (int r = 0; r < c.world_size; r++) p.psrc[r] = ctx->nvls ? ctx->pbuf : ctx->peer_p[r];
   }
   cudaEvent_t b = nullptr;
   timer_begin(ctx, BPC_TIMER_UPDATE, &b);
@@ -1448,7 +1585,7 @@ bpc_status bpc_load_state(bpc_ctx* ctx, int32_t which, const void* host_src, uin
 
 bpc_status bpc_get_exchange(const bpc_ctx* ctx, int32_t* mode) {
   if (!ctx || !mode) return BPC_ERR_INVALID_ARGUMENT;
-  *mode = ctx->exchange;
+  *mode = (ctx->exchange == BPC_EXCHANGE_P2P && ctx->nvls) ? BPC_EXCHANGE_NVLS : ctx->exchange;
   return BPC_OK;
 }
 

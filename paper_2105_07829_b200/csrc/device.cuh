@@ -482,6 +482,29 @@ __device__ __forceinline__ float4 load4_masked(const float* p, uint32_t j, uint3
   if (j + 2 < L) r.z = p[j + 2];
   return r;
 }
+// NVLS multicast stores (addresses in a multicast mapping: the switch writes every
+// bound replica); weak stores, ordered for the peers by fence.proxy.alias + a
+// system-scope release
+__device__ __forceinline__ void mm_st_u32(void* a, uint32_t v) {
+  asm volatile("multimem.st.global.b32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void mm_st_f32(void* a, float v) {
+  asm volatile("multimem.st.global.f32 [%0], %1;" ::"l"(a), "f"(v) : "memory");
+}
+__device__ __forceinline__ void mm_st_v4(void* a, float4 v) {
+  asm volatile("multimem.st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(a), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void mm_store4_masked(float* p, uint32_t j, uint32_t L, float4 v) {
+  if (j + 4 <= L) {
+    mm_st_v4(p + j, v);
+    return;
+  }
+  if (j < L) mm_st_f32(p + j, v.x);
+  if (j + 1 < L) mm_st_f32(p + j + 1, v.y);
+  if (j + 2 < L) mm_st_f32(p + j + 2, v.z);
+}
 __device__ __forceinline__ void store4_masked(float* p, uint32_t j, uint32_t L, float4 v) {
   if (j + 4 <= L) {
     st4(p + j, v);

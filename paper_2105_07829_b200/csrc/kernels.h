@@ -145,9 +145,12 @@ struct StreamParams {
   //  worker: ndst = n, the payload of a chunk owned by r goes to dst[r] +
   //          chunk.recv (slot `rank` of r's RECV, IPC-mapped), then signals push;
   //  server: waits for every push, stores p to the local P, then signals pull
-  //          (the update kernels read it from there over NVLink).
+  //          (the update kernels read it from there over NVLink);
+  //          with mc_out (BPC_EXCHANGE_NVLS) p is stored through the multicast
+  //          mapping of P instead (multimem.st: every rank's P holds it).
   uint8_t* dst[P2P_MAXJ];
   uint32_t ndst;
+  uint8_t* mc_out;
   PeerSync sync;
   // sparse kinds (top-k, random-k): this side's candidate lists (kernels_sparse.cu)
   const uint32_t* sp_chunk2u;

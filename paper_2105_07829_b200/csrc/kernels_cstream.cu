@@ -291,6 +291,7 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
         if (!nvb) return;
         uint8_t* dst = nullptr;
         if (o.nslices == 0) {
+          if (SERVER && FUSED && p.mc_out) return;   // NVLS: the consumers multicast raw payloads
           uint8_t* pay = (!SERVER && FUSED) ? p.dst[o.owner] + o.recv : p.out + o.pay;
           dst = pay + 4ull * o.start;
         } else if (p.use_ef && !(SPARSE && SERVER)) {   // the sparse server only reads Delta
@@ -639,10 +640,17 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
   // held stage; the producer bulk-stores it), raw units: ragged tail only
   auto emit = [&](auto full_tag, const CDesc& d, float4* val, uint8_t* pay, const float4 dv) {
     constexpr bool FULL = decltype(full_tag)::value;
+    const bool MC = SERVER && FUSED && p.mc_out != nullptr;   // pay is in the multicast mapping
     const uint32_t L = d.L;
     const uint32_t nvec = d.len >> 2;
     if (d.nslices == 0) {   // raw unit: the producer bulk-stores [0, nvec); the ragged float4 here
-      if (!FULL && (d.len & 3u)) {
+      if (MC) {   // NVLS: the consumers store the whole raw payload through the multicast mapping
+#pragma unroll
+        for (int s = 0; s < 4; s++) {
+          const uint32_t f = lf + ((s + rot) & 3u);
+          if (FULL || 4 * f < d.len) mm_store4_masked(reinterpret_cast<float*>(pay), d.start + 4 * f, L, val[f]);
+        }
+      } else if (!FULL && (d.len & 3u)) {
 #pragma unroll
         for (int s = 0; s < 4; s++) {
           const uint32_t f = lf + ((s + rot) & 3u);
@@ -752,8 +760,15 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
       const uint32_t other = __shfl_xor_sync(0xffffffffu, m16, 1);
       const uint32_t wi = (d.start >> 5) + (lq >> 1);
       if (!(lane & 1) && (FULL || wi < (L + 31) / 32))
-        reinterpret_cast<uint32_t*>(pay + 4)[wi] = m16 | (other << 16);
-      if (d.sidx == 0 && threadIdx.x == 0) *reinterpret_cast<float*>(pay) = sc;
+      {
+        uint32_t* w = reinterpret_cast<uint32_t*>(pay + 4) + wi;
+        if (MC) mm_st_u32(w, m16 | (other << 16));
+        else *w = m16 | (other << 16);
+      }
+      if (d.sidx == 0 && threadIdx.x == 0) {
+        if (MC) mm_st_f32(pay, sc);
+        else *reinterpret_cast<float*>(pay) = sc;
+      }
     } else if (KIND == C_LDITHER || KIND == C_NDITHER) {
       const float N = dv.x, inv = dv.y, unit = dv.z;
       U128 fld{0, 0};   // the lane's 16 codes in element order
@@ -805,8 +820,14 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
       }
 #pragma unroll
       for (uint32_t c = 0; c < 4; c++)
-        if (c < nw && (FULL || w0 + c < nwu)) out[w0 + c] = u128_get(fld, 32 * c);
-      if (d.sidx == 0 && threadIdx.x == 0) *reinterpret_cast<float*>(pay) = N;
+        if (c < nw && (FULL || w0 + c < nwu)) {
+          if (MC) mm_st_u32(out + w0 + c, u128_get(fld, 32 * c));
+          else out[w0 + c] = u128_get(fld, 32 * c);
+        }
+      if (d.sidx == 0 && threadIdx.x == 0) {
+        if (MC) mm_st_f32(pay, N);
+        else *reinterpret_cast<float*>(pay) = N;
+      }
     }
   };
 
@@ -844,7 +865,8 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
       const CDesc d = hd.desc[hs];
       // payload destination: worker -> the owner's RECV slot (fused push) or SEND;
       // server -> the local P
-      uint8_t* const pay = (!SERVER && FUSED) ? p.dst[d.owner] + d.recv : p.out + d.pay;
+      uint8_t* const pay = (!SERVER && FUSED) ? p.dst[d.owner] + d.recv
+                           : (SERVER && FUSED && p.mc_out) ? p.mc_out + d.pay : p.out + d.pay;
       // every slice (raw included) waits for its reducer before the stage is
       // recycled: keeps each mbarrier at most one phase ahead of its waiters
       if (!SPARSE) mbar_wait(&hd.tready[hs], ehb, 0x5000000u | ie);
@@ -868,7 +890,12 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
   if (bad) atomicOr(p.flag, 1u);
   // fused exchange: this step's payload bytes are released to the peers by the
   // launch's last CTA; every launch stores its epoch there
-  if (FUSED && p.pass != 1) __threadfence_system();
+  if (FUSED && p.pass != 1) {
+    // NVLS: order this thread's multicast stores (another virtual alias of the
+    // peers' P) before the release of the pull epoch
+    if (SERVER && p.mc_out) asm volatile("fence.proxy.alias;" ::: "memory");
+    __threadfence_system();
+  }
   cons_sync();
   if (threadIdx.x == 0 && FUSED && p.pass != 1) mbar_wait(&hd.pfin, 0, 0x6000000u);   // the producer's raw stores landed
   launch_end(p.sync, ep, threadIdx.x == 0);

@@ -57,7 +57,10 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         ctx = bpc.context_for(w, rank=rank, world_size=world, device=local, nccl_id=obj[0], check_finite=1,
                               exchange=exchange)
-        assert ctx.exchange == exchange, f"rank {rank}: asked for {exchange}, got {ctx.exchange}"
+        sparse = name in ("topk", "randk", "lans_topk", "nag_topk")
+        # NVLS applies to the fused kinds; the sparse kinds keep the peer copies
+        want = "p2p" if (exchange == "nvls" and sparse) else exchange
+        assert ctx.exchange == want, f"rank {rank}: asked for {exchange}, got {ctx.exchange}"
         x = torch.tensor(gen_params(w), device=dev)
         ocfg = oracle.Cfg.from_workload(w, n=world)
         ost = oracle.State(world, D, gen_params(w))
@@ -94,9 +97,10 @@ def main():
             slot = ctx.summary().recv_slot_bytes
             # the fused exchange (p2p, norm-based kinds) stores payloads straight into the
             # owners' RECV and never writes SEND
-            check_send = exchange == "nccl" or name in ("topk", "randk", "lans_topk", "nag_topk")
-            # ... and leaves p in its owner's P (the update kernels read it over NVLink)
-            check_all_p = check_send
+            check_send = exchange == "nccl" or sparse
+            # ... and leaves p in its owner's P (the update kernels read it over NVLink),
+            # except NVLS, which multicasts it into every rank's P
+            check_all_p = check_send or exchange == "nvls"
             pb = ctx.copy_state(bpc.BUF_P)
             e = f32(ctx.copy_state(bpc.BUF_WORKER_ERR))
             etl = f32(ctx.copy_state(bpc.BUF_SERVER_ERR))

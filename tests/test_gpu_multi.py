@@ -18,7 +18,7 @@ def _ngpus():
 
 
 @pytest.mark.parametrize("launch", ["eager", "graph"])
-@pytest.mark.parametrize("exchange", ["p2p", "nccl"])
+@pytest.mark.parametrize("exchange", ["p2p", "nccl", "nvls"])
 @pytest.mark.parametrize("n", [2, 4, 8])
 def test_multi_parity(n, exchange, launch):
     if _ngpus() < n:
