@@ -47,9 +47,10 @@ def parse():
     ap.add_argument("--config", default="C5",
                     help="workload (BASELINE.json configs): C5 BERT-large = the largest single-GPU config, the "
                          "metric's default; C2 ResNet-50, C3 VGG16, C4 BERT-base, C1 d=4096")
-    ap.add_argument("--exchange", choices=["p2p", "nccl", "nvls"], default="p2p",
+    ap.add_argument("--exchange", choices=["auto", "p2p", "nccl", "nvls"], default="auto",
                     help="N>1 transport of the push/pull exchange: NVLink peer stores, NCCL send/recv, or "
-                         "peer stores + an NVLS multicast pull")
+                         "peer stores + an NVLS multicast pull; auto = nvls for scaled sign with raw units "
+                         "< 25%% of the payload (measured faster: C5), else p2p")
     ap.add_argument("--optimizer", choices=["adam", "lans", "nag"], default="adam",
                     help="bpc_step update: Adam core (A9), the LANS / CLAN block-normalised update (NEXT #1) "
                          "or NAG (the CNN runs' optimizer, R24)")
@@ -316,10 +317,23 @@ def run_ours(args):
         obj = [bpc.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nid = obj[0]
+    exchange = args.exchange
+    if exchange == "auto":
+        # measured at N = 2 / 4: the multicast pull wins where the
+        # payload is sign bits (coalesced 4-byte multimem stores); raw-heavy (C2)
+        # and dithering payloads (strided code words) lose
+        if world > 1 and w.comp.kind == 2:
+            s_, chs = bpc.plan(bpc.make_config(numels, offs, w.comp, world_size=world,
+                                               chunk_elems=w.chunk_elems or (1 << 18),
+                                               threshold_bytes=w.threshold_bytes))
+            raw = sum(c.payload_bytes for c in chs if c.raw)
+            exchange = "nvls" if raw < 0.25 * max(1, s_.payload_total) else "p2p"
+        else:
+            exchange = "p2p"
     stream = torch.cuda.Stream(dev)   # a capturable stream (not the legacy default stream)
     torch.cuda.set_stream(stream)
     ctx = bpc.context_for(w, rank=rank, world_size=world, device=local, stream=stream.cuda_stream, nccl_id=nid,
-                          exchange=args.exchange)
+                          exchange=exchange)
     chunks = ctx.chunks()
     grads = [gen_grad_torch(w, rank, s, dev) for s in (1, 2)]
     x = torch.tensor(gen_params(w), device=dev)

@@ -265,6 +265,7 @@ struct bpc_ctx {
   // BPC_EXCHANGE_NVLS: P bound to a multicast object (nvls.cu); the server
   // stores p through pbuf_mc, every rank reads it from its own P
   bool nvls = false;
+  bool nvls_copy = false;            // the multicast by a copy kernel after the server (else in the server)
   NvlsMap nv;
   std::shared_ptr<uint64_t> nv_mc;   // the multicast handle (released with the last reference)
   uint8_t* pbuf_mc = nullptr;
@@ -459,6 +460,12 @@ bool agree_min(bpc_ctx* ctx, int32_t* v) {
 // swap P for the unicast mapping of a multicast-bound allocation
 void nvls_adopt(bpc_ctx* ctx, const NvlsMap& m, std::shared_ptr<uint64_t> mc) {
   ctx->nvls = true;
+  // default: the server kernel stores p through the multicast mapping itself;
+  // BPC_NVLS_MODE=copy: it writes the local P and one copy kernel multicasts this
+  // rank's whole segment with 16-byte multimem stores (measured slower at N = 2:
+  // C5 2.458 vs 2.396 ms, C4 1.110 vs 1.006 ms; kept for measurements)
+  const char* mode = getenv("BPC_NVLS_MODE");
+  ctx->nvls_copy = mode && strcmp(mode, "copy") == 0;
   ctx->nv = m;
   ctx->nv_mc = std::move(mc);
   ctx->pbuf_cm = ctx->pbuf;
@@ -1313,11 +1320,12 @@ bpc_status bpc_server(bpc_ctx* ctx) {
     q.piece_stride = (uint32_t)round_up((uint64_t)kStreamSlice * bb / 8 + 32, 16);
     q.stage_payload = (uint64_t)q.piece_stride * q.n <= 49152 && ctx->cfg.world_size <= 32;
     q.sync = peer_sync(ctx, EP_SERVER);
+    const bool mcopy = fused_exchange(ctx) && ctx->nvls && ctx->nvls_copy;
     if (fused_exchange(ctx)) {   // wait for every rank's push; p stays in the local P; signal
       set_wait(ctx, &q.sync, EP_PUSH);
-      set_signal(ctx, &q.sync, EP_PULL);
-      if (ctx->nvls) q.mc_out = ctx->pbuf_mc;   // ... or goes to every rank's P (multicast)
-      if (ctx->n_sslices == 0) {   // owns no chunk: no server launch, only the signal
+      if (!mcopy) set_signal(ctx, &q.sync, EP_PULL);   // (NVLS copy: the copy kernel signals)
+      if (ctx->nvls && !mcopy) q.mc_out = ctx->pbuf_mc;   // ... or goes to every rank's P (multicast)
+      if (ctx->n_sslices == 0 && !mcopy) {   // owns no chunk: no server launch, only the signal
         P2PParams e = {};
         e.sync = peer_sync(ctx, EP_PULL);
         set_signal(ctx, &e.sync, EP_PULL);
@@ -1326,6 +1334,23 @@ bpc_status bpc_server(bpc_ctx* ctx) {
       }
     }
     CK(launch_stream_side(ctx, true, q), "server stream launch");
+    if (mcopy) {   // this rank's p segment (contiguous, 16-byte slots) to every rank's P, then signal
+      const Plan& P = ctx->plan;
+      const int rank = ctx->cfg.rank;
+      P2PParams e = {};
+      if (P.seg_bytes[rank]) {
+        e.src[0] = ctx->pbuf + P.seg_off[rank];
+        e.dst[0] = ctx->pbuf_mc + P.seg_off[rank];
+        e.len[0] = P.seg_bytes[rank];
+        e.njobs = 1;
+      }
+      e.mc = 1;
+      e.sync = peer_sync(ctx, EP_PULL);
+      set_signal(ctx, &e.sync, EP_PULL);
+      const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(2ull * ctx->num_sms, (P.seg_bytes[rank] + 32767) / 32768));
+      CK(launch_p2p_copy(e, grid, ctx->stream), "multicast copy launch");
+      ctx->launches++;
+    }
   } else {
     if (sparse_p2p(ctx)) {   // every rank's delta has landed in RECV
       if (bpc_status st = launch_flag_wait(ctx, EP_PUSH, "push wait launch")) return st;

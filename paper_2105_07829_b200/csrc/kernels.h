@@ -222,6 +222,7 @@ struct P2PParams {
   uint8_t* dst[P2P_MAXJ];           // local or a peer's IPC-mapped buffer
   uint64_t len[P2P_MAXJ];           // bytes, multiples of 16
   int njobs;
+  int mc;                           // dst is a multicast mapping (BPC_EXCHANGE_NVLS): multimem.st.v4
   PeerSync sync;                    // fam = sig_fam = EP_PUSH / EP_PULL: the copy's epoch, released to the peers
 };
 struct P2PWait {

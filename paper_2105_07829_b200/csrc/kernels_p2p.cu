@@ -21,17 +21,24 @@ __global__ void __launch_bounds__(512) p2p_copy_signal(const __grid_constant__ P
     const int4* s = reinterpret_cast<const int4*>(p.src[jb]);
     int4* d = reinterpret_cast<int4*>(p.dst[jb]);
     uint64_t w = g0;
+    auto put = [&](uint64_t i, int4 v) {
+      if (p.mc) mm_st_v4(d + i, make_float4(__int_as_float(v.x), __int_as_float(v.y), __int_as_float(v.z),
+                                            __int_as_float(v.w)));
+      else d[i] = v;
+    };
     for (; w + 3 * stride < nw; w += 4 * stride) {   // 4 independent 16-byte copies in flight
       const int4 a = __ldg(s + w), b = __ldg(s + w + stride), c = __ldg(s + w + 2 * stride),
                  e = __ldg(s + w + 3 * stride);
-      d[w] = a;
-      d[w + stride] = b;
-      d[w + 2 * stride] = c;
-      d[w + 3 * stride] = e;
+      put(w, a);
+      put(w + stride, b);
+      put(w + 2 * stride, c);
+      put(w + 3 * stride, e);
     }
-    for (; w < nw; w += stride) d[w] = __ldg(s + w);
+    for (; w < nw; w += stride) put(w, __ldg(s + w));
   }
-  // make this CTA's peer stores visible system-wide; the last CTA releases the epoch
+  // make this CTA's peer (or multicast) stores visible system-wide; the last CTA
+  // releases the epoch
+  if (p.mc) asm volatile("fence.proxy.alias;" ::: "memory");
   __threadfence_system();
   __syncthreads();
   launch_end(p.sync, ep, threadIdx.x == 0);
