@@ -93,8 +93,9 @@ def main(src, dst):
             for d in rows:
                 name = d.get("Kernel Name", "")
                 t = num(d, "gpu__time_duration.sum")
-                if units.get("gpu__time_duration.sum") == "nsecond" and t is not None:
-                    t /= 1e3
+                tu = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}
+                if t is not None:
+                    t *= tu.get(units.get("gpu__time_duration.sum", "us"), 1.0)   # -> microseconds
                 rb = num(d, "dram__bytes_read.sum") or 0.0
                 wb = num(d, "dram__bytes_write.sum") or 0.0
                 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
