@@ -277,6 +277,7 @@ __device__ __forceinline__ uint32_t unit_ns(const DevChunk& c) { return (c.len +
 struct WarpSel {
   uint32_t idx[SW_CAP];   // candidate indices, ascending
   uint32_t key[SW_CAP];   // keys, then the selected indices
+  uint32_t x[SW_CAP];     // the keys still sharing T's prefix (the threshold search)
 };
 
 template <int KIND>
@@ -340,18 +341,55 @@ __global__ void __launch_bounds__(32 * SW_WARPS) sparse_select_warp_kernel(const
     }
   }
   __syncwarp();
-  // T = the k-th largest key: the largest t with #{key >= t} >= k, bit by bit
-  // from the top (no atomics, no barriers: one warp, keys in shared memory)
-  uint32_t T = 0;
+  // T = the k-th largest key, bit by bit from the top over the keys that still
+  // share T's prefix (x[]): a bit on which they all agree is taken as it is; a
+  // bit that splits them is decided by one counting pass, and the chosen half
+  // is compacted into x[] (in place: writes never pass reads), so the passes
+  // shrink with the set instead of scanning every candidate 32 times
+  const uint32_t* A = s.key;
+  uint32_t na = cnt, above = 0, prefix = 0;
+  auto agree = [&](const uint32_t* a, uint32_t n, uint32_t* andv, uint32_t* orv) {
+    uint32_t x0 = 0xffffffffu, x1 = 0u;
+    for (uint32_t i = lane; i < n; i += 32) {
+      const uint32_t v = a[i];
+      x0 &= v;
+      x1 |= v;
+    }
+    *andv = __reduce_and_sync(0xffffffffu, x0);
+    *orv = __reduce_or_sync(0xffffffffu, x1);
+  };
+  uint32_t andv, orv;
+  agree(A, na, &andv, &orv);
   for (int bit = 31; bit >= 0; bit--) {
-    const uint32_t t = T | (1u << bit);
-    uint32_t n_ge = 0;
-    for (uint32_t i = lane; i < cnt; i += 32) n_ge += s.key[i] >= t;
-    if (__reduce_add_sync(0xffffffffu, n_ge) >= k) T = t;
+    const uint32_t m = 1u << bit;
+    if (!((andv ^ orv) & m)) {   // every key left agrees on this bit
+      prefix |= andv & m;
+      continue;
+    }
+    uint32_t c = 0;
+    for (uint32_t i = lane; i < na; i += 32) c += (A[i] & m) ? 1u : 0u;
+    c = __reduce_add_sync(0xffffffffu, c);
+    const bool take1 = above + c >= k;   // the k-th largest has this bit set
+    if (take1) prefix |= m;
+    else above += c;
+    // keep the chosen half: compact into x[] in index order of A
+    uint32_t out = 0;
+    for (uint32_t i0 = 0; i0 < na; i0 += 32) {
+      const uint32_t i = i0 + lane;
+      const uint32_t v = i < na ? A[i] : 0u;
+      const bool keep = i < na && (((v & m) != 0) == take1);
+      const uint32_t bl = __ballot_sync(0xffffffffu, keep);
+      __syncwarp();
+      if (keep) s.x[out + __popc(bl & ((1u << lane) - 1))] = v;
+      out += __popc(bl);
+    }
+    __syncwarp();
+    A = s.x;
+    na = out;
+    agree(A, na, &andv, &orv);
   }
-  uint32_t n_gt = 0;
-  for (uint32_t i = lane; i < cnt; i += 32) n_gt += s.key[i] > T;
-  const uint32_t need = k - __reduce_add_sync(0xffffffffu, n_gt);   // T-ties to take, lowest indices first
+  const uint32_t T = prefix;
+  const uint32_t need = k - above;   // T-ties to take (lowest indices first)
   // ordered pass over the index-sorted candidates: the selected indices, in
   // order, compacted to the front of key[] (position <= read position)
   uint32_t eq_run = 0, out_run = 0;
