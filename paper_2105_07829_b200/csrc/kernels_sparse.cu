@@ -23,8 +23,9 @@
 //   sparse_select  if the unit has k <= c <= cap candidates, every element
 //                  outside them has key < G <= T (the k-th largest key), so the
 //                  exact selection (keys desc, index asc, R9/R10) is a radix
-//                  select over the c candidates: one WARP per unit (c <= 4096,
-//                  k <= 512), else one CTA per unit (c <= SEL_CAP), else an exact
+//                  select over the c candidates: one 128-thread CTA per unit
+//                  (c <= 4096, k <= 512), else one 512-thread CTA per unit
+//                  (c <= SEL_CAP), else an exact
 //                  radix select + ordered compaction over the whole unit.  Emits
 //                  the payload [u64 k][k idx asc][k val] (l.6 / l.11) and the
 //                  operator-fused EF update e_j = q_j - val_j at the k selected
@@ -39,9 +40,8 @@ enum { SP_TOPK = 3, SP_RANDK = 4 };
 constexpr int SG_NT = 256;        // prep kernel threads
 constexpr int SG_S = 4096;        // sample size (16 runs of 256)
 constexpr int SE_NT = 512;        // CTA select kernel threads
-constexpr int SW_WARPS = 4;       // warp select: units (warps) per CTA
-constexpr uint32_t SW_CAP = 4096; // warp select: max candidates
-constexpr uint32_t SW_KMAX = 512; // warp select: max k
+constexpr uint32_t SW_CAP = 4096; // unit select: max candidates
+constexpr uint32_t SW_KMAX = 512; // unit select: max k
 constexpr int SA_NT = 256;        // server apply: entries per block
 
 __device__ __forceinline__ uint32_t topk_key(float v) { return __float_as_uint(v) & 0x7fffffffu; }
@@ -273,58 +273,76 @@ __device__ __forceinline__ void emit_entry(const SparseParams& p, float* V, uint
 // a slice overflowed its sub-list
 __device__ __forceinline__ uint32_t unit_ns(const DevChunk& c) { return (c.len + 8191u) / 8192u; }
 
-// ---- one warp per unit: c <= SW_CAP candidates, k <= SW_KMAX
-struct WarpSel {
+// ---- one small CTA (SU_NT threads) per unit: c <= SW_CAP candidates, k <= SW_KMAX
+constexpr int SU_NT = 128;                 // threads of the unit select
+constexpr int SU_W = SU_NT / 32;
+constexpr int SU_R = SW_CAP / SU_NT;       // candidates per thread (registers)
+struct UnitSel {
   uint32_t idx[SW_CAP];   // candidate indices, ascending
   uint32_t key[SW_CAP];   // keys, then the selected indices
   uint32_t x[SW_CAP];     // the keys still sharing T's prefix (the threshold search)
+  uint32_t sbase[33];     // the sub-lists' offsets in the concatenated list; [32] = count
+  uint32_t red[4][SU_W];  // per-warp partials of the block reductions
 };
 
+// block reductions over SU_NT threads (all threads call; a barrier inside)
+__device__ __forceinline__ uint32_t su_sum(uint32_t v, uint32_t (&red)[SU_W], uint32_t lane, uint32_t w) {
+  v = __reduce_add_sync(0xffffffffu, v);
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  uint32_t t = 0;
+#pragma unroll
+  for (int i = 0; i < SU_W; i++) t += red[i];
+  return t;
+}
+
 template <int KIND>
-__global__ void __launch_bounds__(32 * SW_WARPS) sparse_select_warp_kernel(const __grid_constant__ SparseParams p) {
-  extern __shared__ __align__(16) unsigned char swraw[];
-  const uint32_t w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t u = blockIdx.x * SW_WARPS + w;
-  if (u >= p.n_units) return;
-  WarpSel& s = reinterpret_cast<WarpSel*>(swraw)[w];
+__global__ void __launch_bounds__(SU_NT) sparse_select_unit_kernel(const __grid_constant__ SparseParams p) {
+  extern __shared__ __align__(16) unsigned char suraw[];
+  UnitSel& s = *reinterpret_cast<UnitSel*>(suraw);
+  const uint32_t tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const uint32_t u = blockIdx.x;
   const DevChunk c = p.chunks[p.items[u]];
   const uint32_t L = c.len, k = c.k;
   if (L > SEL_LMAX) return;   // per-tensor unit: the large-unit path (sparse_large_*)
   const uint32_t ns = unit_ns(c), cs = (p.cand_off[u + 1] - p.cand_off[u]) / ns;
-  // lane l: slice l's count (a chunk unit has <= 32 slices)
-  const uint32_t sc = (uint32_t)lane < ns ? p.scnt[p.first_slice[u] + lane] : 0u;
-  const bool ovf = __any_sync(0xffffffffu, sc > cs);
-  uint32_t incl = sc;
+  if (w == 0) {   // lane l: slice l's count (a chunk unit has <= 32 slices)
+    const uint32_t sc = lane < ns ? p.scnt[p.first_slice[u] + lane] : 0u;
+    const bool ovf = __any_sync(0xffffffffu, sc > cs);
+    uint32_t incl = sc;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= (uint32_t)o) incl += y;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= (uint32_t)o) incl += y;
+    }
+    s.sbase[lane] = incl - sc;
+    if (lane == 31) s.sbase[32] = ovf ? 0xffffffffu : incl;
   }
-  const uint32_t cnt = __shfl_sync(0xffffffffu, incl, 31);
-  if (ovf || cnt < k || cnt > SW_CAP || k > SW_KMAX) {
-    if (lane == 0) p.big[u] = 1;   // the CTA select kernel takes this unit
+  __syncthreads();
+  const uint32_t cnt = s.sbase[32];
+  if (cnt == 0xffffffffu || cnt < k || cnt > SW_CAP || k > SW_KMAX) {
+    if (tid == 0) p.big[u] = 1;   // the CTA select kernel takes this unit
     return;
   }
   float* V = const_cast<float*>(unit_values(p, c));
   uint8_t* pay = p.out + c.pay;
   const uint2* cand = p.cand + p.cand_off[u];
-  // the sub-lists (index, key), concatenated in slice order (= index order): 8
-  // slices at a time, two entries per lane and slice, 16 loads in flight (cs <=
-  // 2^13, but the counts are ~3x below cs: the lanes loop while a slice has more)
-  for (uint32_t s0 = 0; s0 < ns; s0 += 8) {
+  // the sub-lists (index, key), concatenated in slice order (= index order): warp
+  // w takes slices w, w + 4, ..; two entries per lane and slice, 16 loads in flight
+  {
     uint2 v[16];
 #pragma unroll
     for (int q = 0; q < 8; q++) {
-      const uint32_t sl = s0 + q;
-      const uint32_t n_sl = __shfl_sync(0xffffffffu, sc, sl & 31);
-      v[2 * q] = (sl < ns && lane < n_sl) ? cand[sl * cs + lane] : make_uint2(0u, 0u);
-      v[2 * q + 1] = (sl < ns && lane + 32 < n_sl) ? cand[sl * cs + lane + 32] : make_uint2(0u, 0u);
+      const uint32_t sl = w + SU_W * q;
+      const uint32_t n_sl = sl < ns ? (sl + 1 < ns ? s.sbase[sl + 1] : cnt) - s.sbase[sl] : 0u;
+      v[2 * q] = lane < n_sl ? cand[sl * cs + lane] : make_uint2(0u, 0u);
+      v[2 * q + 1] = lane + 32 < n_sl ? cand[sl * cs + lane + 32] : make_uint2(0u, 0u);
     }
 #pragma unroll
     for (int q = 0; q < 8; q++) {
-      const uint32_t sl = s0 + q;
-      const uint32_t n_sl = __shfl_sync(0xffffffffu, sc, sl & 31), b_sl = __shfl_sync(0xffffffffu, incl - sc, sl & 31);
+      const uint32_t sl = w + SU_W * q;
       if (sl >= ns) continue;
+      const uint32_t b_sl = s.sbase[sl], n_sl = (sl + 1 < ns ? s.sbase[sl + 1] : cnt) - b_sl;
       if (lane < n_sl) {
         s.idx[b_sl + lane] = v[2 * q].x;
         s.key[b_sl + lane] = v[2 * q].y;
@@ -340,95 +358,157 @@ __global__ void __launch_bounds__(32 * SW_WARPS) sparse_select_warp_kernel(const
       }
     }
   }
-  __syncwarp();
+  __syncthreads();
   // T = the k-th largest key, bit by bit from the top over the keys that still
-  // share T's prefix (x[]): a bit on which they all agree is taken as it is; a
-  // bit that splits them is decided by one counting pass, and the chosen half
-  // is compacted into x[] (in place: writes never pass reads), so the passes
-  // shrink with the set instead of scanning every candidate 32 times
+  // share T's prefix: a bit on which they all agree is taken as it is; a bit
+  // that splits them is decided by one count, and the chosen half is compacted
+  // into x[] (the set is first read into registers, so the writes are safe)
   const uint32_t* A = s.key;
   uint32_t na = cnt, above = 0, prefix = 0;
-  auto agree = [&](const uint32_t* a, uint32_t n, uint32_t* andv, uint32_t* orv) {
-    uint32_t x0 = 0xffffffffu, x1 = 0u;
-    for (uint32_t i = lane; i < n; i += 32) {
-      const uint32_t v = a[i];
-      x0 &= v;
-      x1 |= v;
-    }
-    *andv = __reduce_and_sync(0xffffffffu, x0);
-    *orv = __reduce_or_sync(0xffffffffu, x1);
-  };
   uint32_t andv, orv;
-  agree(A, na, &andv, &orv);
+  {
+    uint32_t x0 = 0xffffffffu, x1 = 0u;
+    for (uint32_t i = tid; i < na; i += SU_NT) {
+      x0 &= A[i];
+      x1 |= A[i];
+    }
+    x0 = __reduce_and_sync(0xffffffffu, x0);
+    x1 = __reduce_or_sync(0xffffffffu, x1);
+    if (lane == 0) {
+      s.red[0][w] = x0;
+      s.red[1][w] = x1;
+    }
+    __syncthreads();
+    andv = 0xffffffffu;
+    orv = 0u;
+#pragma unroll
+    for (int i = 0; i < SU_W; i++) {
+      andv &= s.red[0][i];
+      orv |= s.red[1][i];
+    }
+    __syncthreads();
+  }
   for (int bit = 31; bit >= 0; bit--) {
     const uint32_t m = 1u << bit;
     if (!((andv ^ orv) & m)) {   // every key left agrees on this bit
       prefix |= andv & m;
       continue;
     }
-    uint32_t c = 0;
-    for (uint32_t i = lane; i < na; i += 32) c += (A[i] & m) ? 1u : 0u;
-    c = __reduce_add_sync(0xffffffffu, c);
-    const bool take1 = above + c >= k;   // the k-th largest has this bit set
-    if (take1) prefix |= m;
-    else above += c;
-    // keep the chosen half: compact into x[] in index order of A
-    uint32_t out = 0;
-    for (uint32_t i0 = 0; i0 < na; i0 += 32) {
-      const uint32_t i = i0 + lane;
-      const uint32_t v = i < na ? A[i] : 0u;
-      const bool keep = i < na && (((v & m) != 0) == take1);
-      const uint32_t bl = __ballot_sync(0xffffffffu, keep);
-      __syncwarp();
-      if (keep) s.x[out + __popc(bl & ((1u << lane) - 1))] = v;
-      out += __popc(bl);
+    uint32_t r[SU_R];
+    uint32_t c1 = 0;
+#pragma unroll
+    for (int j = 0; j < SU_R; j++) {
+      const uint32_t i = tid + SU_NT * j;
+      r[j] = i < na ? A[i] : 0u;
+      c1 += (i < na && (r[j] & m)) ? 1u : 0u;
     }
-    __syncwarp();
+    const uint32_t cset = su_sum(c1, s.red[2], lane, w);   // (barrier: every read of A done)
+    const bool take1 = above + cset >= k;   // the k-th largest has this bit set
+    if (take1) prefix |= m;
+    else above += cset;
+    // keep the chosen half: warp counts -> warp bases -> ballot positions
+    uint32_t kept = 0;
+#pragma unroll
+    for (int j = 0; j < SU_R; j++) {
+      const uint32_t i = tid + SU_NT * j;
+      kept += (i < na && (((r[j] & m) != 0) == take1)) ? 1u : 0u;
+    }
+    kept = __reduce_add_sync(0xffffffffu, kept);
+    if (lane == 0) s.red[3][w] = kept;
+    __syncthreads();
+    uint32_t base = 0, total = 0;
+#pragma unroll
+    for (int i = 0; i < SU_W; i++) {
+      base += (uint32_t)i < w ? s.red[3][i] : 0u;
+      total += s.red[3][i];
+    }
+    uint32_t x0 = 0xffffffffu, x1 = 0u;
+#pragma unroll
+    for (int j = 0; j < SU_R; j++) {
+      const uint32_t i = tid + SU_NT * j;
+      const bool keep = i < na && (((r[j] & m) != 0) == take1);
+      const uint32_t bl = __ballot_sync(0xffffffffu, keep);
+      if (keep) {
+        s.x[base + __popc(bl & ((1u << lane) - 1))] = r[j];
+        x0 &= r[j];
+        x1 |= r[j];
+      }
+      base += __popc(bl);
+    }
+    x0 = __reduce_and_sync(0xffffffffu, x0);
+    x1 = __reduce_or_sync(0xffffffffu, x1);
+    if (lane == 0) {
+      s.red[0][w] = x0;
+      s.red[1][w] = x1;
+    }
+    __syncthreads();
+    andv = 0xffffffffu;
+    orv = 0u;
+#pragma unroll
+    for (int i = 0; i < SU_W; i++) {
+      andv &= s.red[0][i];
+      orv |= s.red[1][i];
+    }
     A = s.x;
-    na = out;
-    agree(A, na, &andv, &orv);
+    na = total;
+    __syncthreads();   // red[] is reused
   }
   const uint32_t T = prefix;
   const uint32_t need = k - above;   // T-ties to take (lowest indices first)
-  // ordered pass over the index-sorted candidates: the selected indices, in
-  // order, compacted to the front of key[] (position <= read position)
+  // ordered pass over the index-sorted candidates, SU_NT at a time: the selected
+  // indices, in order, compacted to the front of key[] (read before any write)
   uint32_t eq_run = 0, out_run = 0;
-  for (uint32_t i0 = 0; i0 < cnt; i0 += 32) {
-    const uint32_t i = i0 + lane;
+  for (uint32_t i0 = 0; i0 < cnt; i0 += SU_NT) {
+    const uint32_t i = i0 + tid;
     const uint32_t key = i < cnt ? s.key[i] : 0u;
+    const uint32_t ix = i < cnt ? s.idx[i] : 0u;
     const bool eq = i < cnt && key == T;
     const uint32_t be = __ballot_sync(0xffffffffu, eq);
-    const uint32_t er = eq_run + __popc(be & ((1u << lane) - 1));
+    if (lane == 0) s.red[0][w] = __popc(be);
+    __syncthreads();
+    uint32_t eb = eq_run, et = 0;
+#pragma unroll
+    for (int q = 0; q < SU_W; q++) {
+      eb += (uint32_t)q < w ? s.red[0][q] : 0u;
+      et += s.red[0][q];
+    }
+    const uint32_t er = eb + __popc(be & ((1u << lane) - 1));
     const bool sel = i < cnt && (key > T || (eq && er < need));
     const uint32_t bs = __ballot_sync(0xffffffffu, sel);
-    __syncwarp();
-    if (sel) s.key[out_run + __popc(bs & ((1u << lane) - 1))] = s.idx[i];
-    __syncwarp();
-    eq_run += __popc(be);
-    out_run += __popc(bs);
+    if (lane == 0) s.red[1][w] = __popc(bs);
+    __syncthreads();
+    uint32_t ob = out_run, ot = 0;
+#pragma unroll
+    for (int q = 0; q < SU_W; q++) {
+      ob += (uint32_t)q < w ? s.red[1][q] : 0u;
+      ot += s.red[1][q];
+    }
+    if (sel) s.key[ob + __popc(bs & ((1u << lane) - 1))] = ix;   // position <= i0 < later reads
+    eq_run += et;
+    out_run += ot;
+    __syncthreads();
   }
-  __syncwarp();
-  // emit, value reads batched 8 deep
+  // emit, value reads batched 4 deep per thread
   const bool scaled = KIND == SP_RANDK && p.randk_scaled;
   const float scale = (float)((double)L / (double)k);
-  for (uint32_t i0 = 0; i0 < k; i0 += 256) {
-    float qv[8];
-    uint32_t jj[8];
+  for (uint32_t i0 = 0; i0 < k; i0 += 4 * SU_NT) {
+    float qv[4];
+    uint32_t jj[4];
 #pragma unroll
-    for (int r = 0; r < 8; r++) {
-      const uint32_t i = i0 + 32 * r + lane;
+    for (int r = 0; r < 4; r++) {
+      const uint32_t i = i0 + SU_NT * r + tid;
       jj[r] = i < k ? s.key[i] : 0u;
       qv[r] = i < k ? V[jj[r]] : 0.f;
     }
 #pragma unroll
-    for (int r = 0; r < 8; r++) {
-      const uint32_t i = i0 + 32 * r + lane;
+    for (int r = 0; r < 4; r++) {
+      const uint32_t i = i0 + SU_NT * r + tid;
       if (i < k) emit_entry(p, V, pay, k, i, jj[r], qv[r], scaled, scale);
     }
   }
-  __syncwarp();
-  if (p.server && !p.use_ef) clear_scratch(p, c, V, lane, 32);
-  if (lane == 0) *reinterpret_cast<uint64_t*>(pay) = (uint64_t)k;
+  __syncthreads();
+  if (p.server && !p.use_ef) clear_scratch(p, c, V, tid, SU_NT);
+  if (tid == 0) *reinterpret_cast<uint64_t*>(pay) = (uint64_t)k;
 }
 
 // ---- one CTA per unit: larger candidate lists, or the exact whole-unit path
@@ -808,10 +888,10 @@ static cudaError_t launch_prep_t(const SparseParams& p, cudaStream_t s) {
 template <int KIND>
 static cudaError_t launch_select_t(const SparseParams& p, cudaStream_t s) {
   if (!p.n_units) return cudaSuccess;
-  const size_t ws = sizeof(WarpSel) * SW_WARPS;
-  cudaError_t e = cudaFuncSetAttribute(sparse_select_warp_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ws);
+  const size_t ws = sizeof(UnitSel);
+  cudaError_t e = cudaFuncSetAttribute(sparse_select_unit_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ws);
   if (e != cudaSuccess) return e;
-  sparse_select_warp_kernel<KIND><<<(p.n_units + SW_WARPS - 1) / SW_WARPS, 32 * SW_WARPS, ws, s>>>(p);
+  sparse_select_unit_kernel<KIND><<<p.n_units, SU_NT, ws, s>>>(p);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   const size_t smem = sparse_select_smem(p.sel_cap);
   e = cudaFuncSetAttribute(sparse_select_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
