@@ -398,6 +398,7 @@ __global__ void __launch_bounds__(SU_NT) sparse_select_unit_kernel(const __grid_
     uint32_t c1 = 0;
 #pragma unroll
     for (int j = 0; j < SU_R; j++) {
+      if (SU_NT * (uint32_t)j >= na) break;   // (uniform: the loops run ceil(na / SU_NT) times)
       const uint32_t i = tid + SU_NT * j;
       r[j] = i < na ? A[i] : 0u;
       c1 += (i < na && (r[j] & m)) ? 1u : 0u;
@@ -410,6 +411,7 @@ __global__ void __launch_bounds__(SU_NT) sparse_select_unit_kernel(const __grid_
     uint32_t kept = 0;
 #pragma unroll
     for (int j = 0; j < SU_R; j++) {
+      if (SU_NT * (uint32_t)j >= na) break;
       const uint32_t i = tid + SU_NT * j;
       kept += (i < na && (((r[j] & m) != 0) == take1)) ? 1u : 0u;
     }
@@ -425,6 +427,7 @@ __global__ void __launch_bounds__(SU_NT) sparse_select_unit_kernel(const __grid_
     uint32_t x0 = 0xffffffffu, x1 = 0u;
 #pragma unroll
     for (int j = 0; j < SU_R; j++) {
+      if (SU_NT * (uint32_t)j >= na) break;
       const uint32_t i = tid + SU_NT * j;
       const bool keep = i < na && (((r[j] & m) != 0) == take1);
       const uint32_t bl = __ballot_sync(0xffffffffu, keep);
