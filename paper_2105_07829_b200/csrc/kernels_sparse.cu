@@ -185,6 +185,8 @@ __global__ void __launch_bounds__(SA_NT) sparse_apply_kernel(const __grid_consta
 template <int KIND>
 __global__ void __launch_bounds__(SG_NT) sparse_prep_kernel(const __grid_constant__ SparseParams p) {
   __shared__ uint32_t red[SG_NT / 32];
+  __shared__ uint32_t hist[2048];
+  __shared__ uint32_t pick[2];
   const uint32_t u = blockIdx.x;
   const DevChunk c = p.chunks[p.items[u]];
   const uint32_t L = c.len, k = c.k;
@@ -220,23 +222,53 @@ __global__ void __launch_bounds__(SG_NT) sparse_prep_kernel(const __grid_constan
         key[r] = topk_key(v);
       }
     }
-    // the m-th largest sample key, bit by bit from the top (22 bits: G is the
-    // lower edge of a 2^-13-wide magnitude bin holding it, G <= that key)
+    // the m-th largest sample key, its bits 30..10 by two radix passes (11 + 10
+    // bits, shared-memory histograms): G is the lower edge of the 2^-13-wide
+    // magnitude bin holding it, the largest multiple of 2^10 with >= m sample
+    // keys at or above it
     const uint32_t m = L <= (uint32_t)SG_S ? k : (uint32_t)min(S, sparse_sample_rank(k, L));
-    uint32_t g = 0;
-    for (int bit = 30; bit >= 10; bit--) {
-      const uint32_t t = g | (1u << bit);
-      uint32_t cnt = 0;
-#pragma unroll
-      for (int r = 0; r < 16; r++) cnt += key[r] >= t;
-      cnt = __reduce_add_sync(0xffffffffu, cnt);
-      if (lane == 0) red[warp] = cnt;
+    uint32_t g = 0, rank = m;
+    for (int pass = 0; pass < 2; pass++) {
+      const int sh = pass ? 10 : 20, nb = pass ? 1024 : 2048, per = nb / SG_NT;
+      for (int b = threadIdx.x; b < nb; b += SG_NT) hist[b] = 0;
       __syncthreads();
+#pragma unroll
+      for (int r = 0; r < 16; r++) {
+        const uint32_t sidx = threadIdx.x + r * SG_NT;
+        if (sidx < S && (pass == 0 || (key[r] >> 20) == (g >> 20)))
+          atomicAdd(&hist[(key[r] >> sh) & (uint32_t)(nb - 1)], 1u);
+      }
+      __syncthreads();
+      // thread t owns bins nb - 1 - per t - j (descending): block scan of the counts
+      // from the top; the owner of the rank-th largest publishes (bin, keys above it)
       uint32_t tot = 0;
+      for (int j = 0; j < per; j++) tot += hist[nb - 1 - per * threadIdx.x - j];
+      uint32_t incl = tot;
 #pragma unroll
-      for (int w = 0; w < SG_NT / 32; w++) tot += red[w];
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (uint32_t)o) incl += y;
+      }
+      if (lane == 31) red[warp] = incl;
       __syncthreads();
-      if (tot >= m) g = t;
+      for (int w = 0; w < warp; w++) incl += red[w];
+      const uint32_t before = incl - tot;
+      if (before < rank && rank <= incl) {
+        uint32_t run = before;
+        for (int j = 0; j < per; j++) {
+          const uint32_t cj = hist[nb - 1 - per * threadIdx.x - j];
+          if (run + cj >= rank) {
+            pick[0] = (uint32_t)(nb - 1 - per * threadIdx.x - j);
+            pick[1] = run;
+            break;
+          }
+          run += cj;
+        }
+      }
+      __syncthreads();
+      g |= pick[0] << sh;
+      rank -= pick[1];
+      __syncthreads();   // hist, red and pick are reused by the next pass
     }
     // key 0 (magnitude +-0) is never a useful threshold: with fewer than k nonzero
     // values the select kernel takes its exact whole-unit path
