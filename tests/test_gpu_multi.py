@@ -24,15 +24,18 @@ def test_multi_parity(n, exchange, launch):
     if _ngpus() < n:
         pytest.skip(f"needs {n} GPUs")
     import socket
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    port = s.getsockname()[1]
-    s.close()
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", "--master-port", str(port),
-           os.path.join(ROOT, "tests", "multigpu_parity.py"), "", exchange, launch]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
-    out = r.stdout + r.stderr
+    for attempt in range(3):   # the rendezvous port can be taken between the probe and the bind
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port),
+               os.path.join(ROOT, "tests", "multigpu_parity.py"), "", exchange, launch]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+        out = r.stdout + r.stderr
+        if r.returncode == 0 or "EADDRINUSE" not in out:
+            break
     assert r.returncode == 0, out[-4000:]
     for rank in range(n):
         for name in ("onebit", "topk", "randk", "ldither", "lans_onebit", "lans_topk", "units_onebit", "nag_topk"):
