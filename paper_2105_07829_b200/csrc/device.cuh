@@ -143,6 +143,9 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity
     }
   }
 }
+#ifndef BPC_CTR_POLL_NS
+#define BPC_CTR_POLL_NS 128   // poll of a cross-CTA unit counter (512 measured slower, profiles/r2/ab/)
+#endif
 // gpu-scope release add / acquire load on unit counters (cross-CTA unit reductions)
 __device__ __forceinline__ void red_release_add(unsigned long long* p, unsigned long long v) {
   asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -164,7 +167,7 @@ __device__ __forceinline__ void wait_counter(const unsigned long long* p, unsign
   if (v < target) {
     const long long t0 = clock64_v();
     for (uint32_t it = 1; (v = ld_relaxed(p)) < target; it++) {
-      __nanosleep(512);
+      __nanosleep(BPC_CTR_POLL_NS);
       if ((it & 63) == 0) {
         if (clock64_v() - t0 > BPC_WATCHDOG_CYCLES) watchdog_fire("counter", tag, 0, v, target);
       }

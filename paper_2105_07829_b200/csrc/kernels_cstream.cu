@@ -62,6 +62,9 @@ constexpr int CMAXH = 8;                 // max held stages
 constexpr int CNI = 2;                   // input stages
 constexpr int CMAXD = 3;                 // max emit deferral (D = 4 measured slower for the server)
 constexpr int CRED_R = CMAXD + 1;        // ring of the consumer warps' slice subtrees (>= D + 1)
+#ifndef BPC_RED_POLL_NS
+#define BPC_RED_POLL_NS 200    // reducer poll of the slice-produced barrier (1000: C2 server +2.5 %)
+#endif
 constexpr int CSL = 8192;                // elements per slice
 constexpr int CLE = 16;                  // elements per consumer lane per slice
 constexpr int CUNITSL = (1 << 18) / CSL; // max slices per unit (32)
@@ -413,9 +416,10 @@ __global__ void __launch_bounds__(CSNT, 1) cstream_kernel(const __grid_constant_
       const uint32_t hs = i % NH;
       // slice i produced.  Cannot alias: slice i + NH needs stage hs back, which
       // needs this reducer's tready arrive for slice i first.
-      // the emit of slice i runs D slices later: a 1 us poll costs it nothing and
-      // keeps the waiting warps off the issue slots the consumers need
-      mbar_wait_backoff(&hd.pready[hs], (i / NH) & 1, 1000, 0x2000000u | i);
+      // the emit of slice i runs D slices later; a slept poll (200 ns) keeps the
+      // waiting warps off the issue slots the consumers need.  A 1 us poll
+      // delayed the unit totals: onebit server +2.5 % (C2), +2 % (C5)
+      mbar_wait_backoff(&hd.pready[hs], (i / NH) & 1, BPC_RED_POLL_NS, 0x2000000u | i);
       const uint32_t ns = SPARSE ? 0u : hd.desc[hs].nslices;   // sparse kinds: no unit norm
       if (ns > 0) {   // the slice partial: pairwise tree over the 16 consumer warps' subtrees
         double r = lane < CCW ? hd.red[i % CRED_R][lane] : 0.0;
